@@ -1,0 +1,177 @@
+/*
+ * bhcp_b200.h -- C ABI of the B200-native PinT QBVM/MQBVM solver library
+ * (libbhcp_b200.so, sm_100a).
+ *
+ * The reference (pure Python, package `bhcp`) has no FFI; its boundary is the
+ * Python signatures exported from pkg/src/bhcp/__init__.py:11-69. Every entry
+ * point below replaces the numeric core of one of those functions; the
+ * Python package `paper_2107_06381_b200` wraps them with the reference's
+ * signatures and error types (see INTEGRATION.md for the ctypes binding).
+ *
+ *   bhcp_sine_transform     <- space.sine_transform / SpatialSpectrum.transform
+ *                              (pkg/src/bhcp/space.py:163-177, 223-231)
+ *   bhcp_step_b             <- pint.step_b_parallel + space.shifted_solve
+ *                              (pkg/src/bhcp/pint.py:26-66; space.py:234-283)
+ *   bhcp_to_eigenspace      <- circulant.to_eigenspace / apply_inverse_basis
+ *                              (pkg/src/bhcp/circulant.py:99-106, 156-164)
+ *   bhcp_from_eigenspace    <- circulant.from_eigenspace / apply_basis
+ *                              (pkg/src/bhcp/circulant.py:108-115, 167-190)
+ *   bhcp_pint_solve         <- pint.solve_pint (pkg/src/bhcp/pint.py:69-110),
+ *                              fused dataflow
+ *   bhcp_pint_solve_unfused <- pint.solve_pint, literal 3-step dataflow
+ *   bhcp_pint_modes / bhcp_pint_levels
+ *                           <- the two halves of solve_pint used by the slab-
+ *                              decomposed multi-GPU driver
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Device pointers are CUDA device memory
+ *     on the plan's device; `stream` is a cudaStream_t passed as void*.
+ *   - complex128 data is interleaved (re, im) doubles, i.e. the memory layout
+ *     of numpy.complex128 / torch.complex128.
+ *   - "level-major" means a C-contiguous (levels, n_space) array, i.e. one
+ *     spatial field per time level, matching the trajectory layout of
+ *     pint.py:99 (SolveResult.trajectory is (n_levels, n_space)).
+ *   - Spatial fields are flattened in C order, first axis outermost
+ *     (space.py:64-74); the sine transform runs along axis -1, then -2
+ *     (then -3 for the 3D extension), space.py:175-176.
+ *   - Functions only enqueue work; results that need a host decision
+ *     (singular shift, imaginary residue) are read with bhcp_read_status,
+ *     which synchronises the stream.
+ *   - Return codes: BHCP_OK, or one of the BHCP_ERR_* below. The message of
+ *     the last error on the calling thread is bhcp_last_error().
+ */
+#ifndef BHCP_B200_H
+#define BHCP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BHCP_OK = 0,
+  BHCP_ERR_SINGULAR_SHIFT = 1,     /* space.py:234-246 SingularShiftError */
+  BHCP_ERR_IMAGINARY_RESIDUE = 2,  /* circulant.py:182-189 ImaginaryResidueError */
+  BHCP_ERR_INVALID = 3,            /* ValueError analogues */
+  BHCP_ERR_CUDA = 4
+};
+
+typedef struct bhcp_space_plan bhcp_space_plan;
+typedef struct bhcp_time_plan bhcp_time_plan;
+
+/* Outcome of a solve, filled by bhcp_read_status. */
+typedef struct {
+  int code;             /* BHCP_OK / BHCP_ERR_SINGULAR_SHIFT / BHCP_ERR_IMAGINARY_RESIDUE */
+  int64_t bad_column;   /* first singular column j (pint.py:52-56), -1 if none */
+  double residue;       /* ||Im Y||_F  (circulant.py:184) */
+  double norm;          /* ||Y||_F     (circulant.py:183) */
+} bhcp_status;
+
+/* Size of the small device status block used by the solve / step-b /
+ * from-eigenspace entry points (bad column + norm accumulators). */
+size_t bhcp_status_bytes(void);
+
+int bhcp_version(void);
+const char* bhcp_last_error(void);
+
+/* Space plan: Dirichlet grid with num_cells subdivisions per axis, dim in
+ * {1,2,3} (3 is this library's extension; the reference stops at 2,
+ * space.py:42-43). mu1_host holds the m = num_cells-1 one-dimensional
+ * eigenvalues (4/h^2) sin^2(k pi / 2M) computed by the caller with the
+ * reference expression (space.py:209-211), so shifts match bit for bit. */
+int bhcp_space_plan_create(int device, int dim, int num_cells,
+                           const double* mu1_host, bhcp_space_plan** out);
+void bhcp_space_plan_destroy(bhcp_space_plan* plan);
+
+/* Time plan: n_levels = N+1 (circulant.py:50-53). gamma_host and
+ * gamma_inv_host are 2*n_levels doubles (diagonal of Gamma and its inverse,
+ * circulant.py:148); shifts_host is 2*n_levels doubles, s_j = d_j / tau
+ * (pint.py:95). */
+int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host,
+                          const double* gamma_inv_host, const double* shifts_host,
+                          bhcp_time_plan** out);
+void bhcp_time_plan_destroy(bhcp_time_plan* plan);
+
+/* Orthonormal DST-I over the spatial axes of `batch` level-major fields.
+ * in/out may alias. is_complex selects complex128 vs float64 data. */
+int bhcp_sine_transform(const bhcp_space_plan* sp, const void* in, void* out,
+                        int is_complex, int64_t batch, void* stream);
+
+/* Step (b): for each level j < batch solve (shift_j I - lap) x = rhs_j with
+ * the spectral method (DST, divide by shift_j + mu_k, DST). in/out are
+ * level-major complex128 (batch, n_space) and may alias; shifts_dev holds
+ * 2*batch doubles. The first singular column is recorded in status_dev. */
+int bhcp_step_b(const bhcp_space_plan* sp, const void* in, void* out,
+                const double* shifts_dev, int64_t batch, void* status_dev,
+                void* stream);
+
+/* Step (a): out = ifft_ortho(in * gamma) along the time axis for `batch`
+ * sequences. Element t of sequence b is at in[b*in_sb + t*in_st] (element
+ * units). One of the two strides must be 1. in_is_complex selects
+ * float64/complex128 input; output is complex128. */
+int bhcp_to_eigenspace(const bhcp_time_plan* tp, const void* in, int in_is_complex,
+                       int64_t batch, int64_t in_sb, int64_t in_st, void* out,
+                       int64_t out_sb, int64_t out_st, void* stream);
+
+/* Step (c): Y = fft_ortho(in) / gamma along the time axis; writes Re Y
+ * (out_is_complex = 0, float64) or Y (complex128); accumulates ||Re Y||^2 and
+ * ||Im Y||^2 into status_dev (reset it with bhcp_status_reset first). */
+int bhcp_from_eigenspace(const bhcp_time_plan* tp, const void* in, int64_t batch,
+                         int64_t in_sb, int64_t in_st, void* out, int out_is_complex,
+                         int64_t out_sb, int64_t out_st, void* status_dev,
+                         void* stream);
+
+/* Reset a status block (bad column = none, norms = 0). */
+int bhcp_status_reset(void* status_dev, void* stream);
+
+/* Synchronise `stream`, read the status block and apply the reference's
+ * decision rules: singular shift first (pint.py:52-56), then the imaginary
+ * residue test ||Im|| > tol * max(||Y||, tiny) (circulant.py:182-189). */
+int bhcp_read_status(const void* status_dev, double tol, bhcp_status* st, void* stream);
+
+/* Fused solve: y (n_levels, n_space) float64 from the
+ * final data g (n_space float64) and the condition divisor (methods.py:85-96).
+ * ws must hold bhcp_pint_workspace_bytes() bytes of device memory; the status
+ * block is inside ws (bhcp_pint_status_ptr). */
+size_t bhcp_pint_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp);
+void* bhcp_pint_status_ptr(const bhcp_space_plan* sp, const bhcp_time_plan* tp, void* ws);
+int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
+                    const double* g_dev, double divisor, double* y_dev, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* Literal 3-step dataflow of pint.py:89-99 on level-major complex buffers:
+ * rhs assembly, step (a) time transform, step (b), step (c). ws must hold
+ * bhcp_pint_unfused_workspace_bytes() bytes. */
+size_t bhcp_pint_unfused_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp);
+void* bhcp_pint_unfused_status_ptr(const bhcp_space_plan* sp, const bhcp_time_plan* tp, void* ws);
+int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
+                            const double* g_dev, double divisor, double* y_dev,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* Slab halves of the fused solve for the multi-GPU driver.
+ * bhcp_pint_ghat: ghat = DST(g) * scale (n_space float64), scale = 1/(divisor*n).
+ * bhcp_pint_modes: for spatial modes [k_begin, k_end) write
+ *   W[t, k - k_begin] = ghat[k] * Re(gamma_inv_t * FFT_t(1/(s_j + mu_k)))
+ *   into w_dev with row stride w_ld (elements), accumulating norms / singular
+ *   column into status_dev.
+ * bhcp_pint_levels: inverse DST of `batch` level-major float64 fields,
+ *   in -> out (may alias). */
+int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
+                   double* ghat_dev, void* stream);
+int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
+                    const double* ghat_dev, int64_t k_begin, int64_t k_end,
+                    double* w_dev, int64_t w_ld, void* status_dev, void* stream);
+int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
+                     int64_t batch, void* stream);
+
+/* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
+int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,
+                   int elem_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BHCP_B200_H */

@@ -1,0 +1,1034 @@
+// bhcp_b200.cu -- sm_100a kernels and the C ABI (include/bhcp_b200.h) of the
+// PinT QBVM/MQBVM direct solver.
+//
+// Reference path (pkg/src/bhcp): solve_pint (pint.py:69-110) =
+//   (a) to_eigenspace: ifft_ortho(rhs * gamma) along time   (circulant.py:99-106)
+//   (b) per level j: DST, divide by s_j + mu_k, DST          (pint.py:26-66, space.py:249-283)
+//   (c) from_eigenspace: fft_ortho / gamma, residue, Re      (circulant.py:108-115, 167-190)
+// Kernels here:
+//   k_time        general time-axis transforms (steps (a)/(c), any layout)
+//   k_dst_rows    DST-I along the contiguous spatial axis (+ fused 1D shifted solve)
+//   k_dst_cols    DST-I along a strided spatial axis (+ fused divide on the outer axis)
+//   k_modes       fused solve pass A: shifts -> time FFT -> Gamma^-1 -> Re, per mode
+//   k_rhs, k_transpose, k_scale helpers
+// All arithmetic is fp64; no tensor cores (the work is FFT/elementwise).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/bhcp_b200.h"
+#include "fft_engine.cuh"
+#include "plan.h"
+
+namespace bhcp {
+
+struct StatusDev {
+  unsigned long long bad_col;  // first singular column, ULLONG_MAX if none
+  double sum_re2;              // sum of (Re Y)^2
+  double sum_im2;              // sum of (Im Y)^2
+  double pad[5];
+};
+static_assert(sizeof(StatusDev) == 64, "status block is 64 bytes");
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+
+// Block-wide sum of two doubles; result valid in thread 0. Deterministic tree.
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) { red[2 * w] = a; red[2 * w + 1] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = 0; i < nw; ++i) { s0 += red[2 * i]; s1 += red[2 * i + 1]; }
+    a = s0; b = s1;
+  }
+}
+
+__device__ __forceinline__ void flag_singular(StatusDev* st, long long col) {
+  atomicMin(&st->bad_col, (unsigned long long)col);
+}
+
+// mu for flattened mode index (C order, first axis outermost) -- same
+// association as numpy add.outer (space.py:215; 3D restated as ((a+b)+c)).
+__device__ __forceinline__ double mode_mu(const double* __restrict__ mu1, int m, int dim, long long k) {
+  if (dim == 1) return __ldg(mu1 + k);
+  if (dim == 2) {
+    const int k1 = (int)(k / m), k2 = (int)(k - (long long)k1 * m);
+    return __ldg(mu1 + k1) + __ldg(mu1 + k2);
+  }
+  const long long mm = (long long)m * m;
+  const int k1 = (int)(k / mm);
+  const long long r = k - k1 * mm;
+  const int k2 = (int)(r / m), k3 = (int)(r - (long long)k2 * m);
+  return (__ldg(mu1 + k1) + __ldg(mu1 + k2)) + __ldg(mu1 + k3);
+}
+
+// Divide by (s + mu) the way numpy does complex / complex for these operands:
+// x * conj(den) / |den|^2. Flags the column when |s + mu| <= 1e-14 |s|
+// (space.py:237-240).
+__device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double mu, StatusDev* st,
+                                                  long long col) {
+  const double dr = s.x + mu, di = s.y;
+  const double den2 = dr * dr + di * di;
+  const double s2 = s.x * s.x + s.y * s.y;
+  if (den2 <= 1e-28 * s2) flag_singular(st, col);
+  const double inv = 1.0 / den2;
+  return make_double2((x.x * dr + x.y * di) * inv, (x.y * dr - x.x * di) * inv);
+}
+
+template <int V> struct VT;
+template <> struct VT<V256> { static constexpr int T = 256, CAP = 16, MINB = 2; };
+template <> struct VT<V512> { static constexpr int T = 512, CAP = 16, MINB = 1; };
+template <> struct VT<V768> { static constexpr int T = 768, CAP = 12, MINB = 1; };
+
+// ------------------------------------------------------------------ DST helpers
+// Orthonormal DST-I of length m via a complex FFT of length L = 2(m+1) of the
+// odd extension [0, x_1..x_m, 0, -x_m..-x_1]: X_k = -2i sum_j x_j sin(pi jk/(m+1)),
+// so DST_k = sqrt(2/(m+1)) * (i/2) X_k. Real data are packed two lines per
+// complex sequence (DST is real-linear), complex lines one per sequence.
+__device__ __forceinline__ void dst_put(const FftPlanDev& p, double2* buf, int ld, int seq, int m,
+                                        int e, double2 x) {
+  if (p.blue) {
+    buf[seq * ld + e + 1] = cmul(x, __ldg(p.chirp + e + 1));
+    buf[seq * ld + p.L - 1 - e] = cmul(make_double2(-x.x, -x.y), __ldg(p.chirp + p.L - 1 - e));
+  } else {
+    buf[seq * ld + e + 1] = x;
+    buf[seq * ld + p.L - 1 - e] = make_double2(-x.x, -x.y);
+  }
+}
+__device__ __forceinline__ void dst_put_zeros(const FftPlanDev& p, double2* buf, int ld, int nseq, int m) {
+  // positions 0 and m+1 of each sequence, plus the Bluestein tail
+  for (int q = threadIdx.x; q < nseq; q += blockDim.x) {
+    buf[q * ld] = make_double2(0.0, 0.0);
+    buf[q * ld + m + 1] = make_double2(0.0, 0.0);
+  }
+  if (p.blue) {
+    const int pad = p.Lc - p.L;
+    for (int i = threadIdx.x; i < nseq * pad; i += blockDim.x) {
+      const int q = i / pad;
+      buf[q * ld + p.L + (i - q * pad)] = make_double2(0.0, 0.0);
+    }
+  }
+}
+__device__ __forceinline__ double2 gen_get(const FftPlanDev& p, const double2* buf, int ld, int seq, int k) {
+  double2 x = buf[seq * ld + k];
+  if (p.blue) x = cmul(cconj(x), __ldg(p.chirp + k));
+  return x;
+}
+__device__ __forceinline__ void gen_put(const FftPlanDev& p, double2* buf, int ld, int seq, int j, double2 x) {
+  if (p.blue) x = cmul(x, __ldg(p.chirp + j));
+  buf[seq * ld + j] = x;
+}
+__device__ __forceinline__ void gen_zero_tail(const FftPlanDev& p, double2* buf, int ld, int nseq) {
+  if (!p.blue) return;
+  const int pad = p.Lc - p.L;
+  for (int i = threadIdx.x; i < nseq * pad; i += blockDim.x) {
+    const int q = i / pad;
+    buf[q * ld + p.L + (i - q * pad)] = make_double2(0.0, 0.0);
+  }
+}
+
+// Stockham core over nseq sequences of stride ld. V768 only instantiates the
+// {2,3,4,5} stages (its plans are factored with those radices only) to keep
+// the register budget of 768-thread CTAs.
+template <int V, int CAP> struct BigStage {
+  static __device__ __forceinline__ void run(int R, double2* buf, int nseq, int Lc, int ld, int Ns,
+                                             const double2* tw) {
+    switch (R) {
+      case 7: fft_stage_ld<7, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 8: fft_stage_ld<8, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 11: fft_stage_ld<11, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 13: fft_stage_ld<13, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 17: fft_stage_ld<17, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 19: fft_stage_ld<19, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      case 23: fft_stage_ld<23, CAP>(buf, nseq, Lc, ld, Ns, tw); break;
+      default: __trap();
+    }
+  }
+};
+template <int CAP> struct BigStage<V768, CAP> {
+  static __device__ __forceinline__ void run(int, double2*, int, int, int, int, const double2*) { __trap(); }
+};
+
+template <int V>
+__device__ __forceinline__ void fft_run(const FftPlanDev& p, double2* buf, int ld, int nseq) {
+  constexpr int CAP = VT<V>::CAP;
+  int Ns = 1;
+  for (int s = 0; s < p.nst; ++s) {
+    const int R = p.radix[s];
+    switch (R) {
+      case 2: fft_stage_ld<2, CAP>(buf, nseq, p.Lc, ld, Ns, p.tw); break;
+      case 3: fft_stage_ld<3, CAP>(buf, nseq, p.Lc, ld, Ns, p.tw); break;
+      case 4: fft_stage_ld<4, CAP>(buf, nseq, p.Lc, ld, Ns, p.tw); break;
+      case 5: fft_stage_ld<5, CAP>(buf, nseq, p.Lc, ld, Ns, p.tw); break;
+      default: BigStage<V, CAP>::run(R, buf, nseq, p.Lc, ld, Ns, p.tw);
+    }
+    Ns *= R;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void fft_exec_ld(const FftPlanDev& p, double2* buf, int ld, int nseq) {
+  fft_run<V>(p, buf, ld, nseq);
+  if (p.blue) {
+    for (int i = threadIdx.x; i < nseq * p.Lc; i += blockDim.x) {
+      const int q = i / p.Lc;
+      const int k = i - q * p.Lc;
+      double2* x = buf + q * ld + k;
+      *x = cconj(cmul(*x, __ldg(p.bhat + k)));
+    }
+    __syncthreads();
+    fft_run<V>(p, buf, ld, nseq);
+  }
+}
+
+// ------------------------------------------------------------------ k_time
+// MODE 0 (step a): out = ifft_ortho(in * gamma)   -- circulant.py:99-106
+// MODE 1 (step c): Y = fft_ortho(in) * gamma_inv  -- circulant.py:108-115, 182-190
+struct TimeArgs {
+  FftPlanDev p;
+  int ld, nseq, n;
+  const double* in;
+  int in_cplx;
+  long long B, in_sb, in_st;
+  double* out;
+  int out_cplx;
+  long long out_sb, out_st;
+  const double2* gam;  // gamma (MODE 0) or gamma_inv (MODE 1)
+  double scale;        // 1/sqrt(n)
+  StatusDev* st;
+};
+
+template <int V, int MODE>
+__global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_time(TimeArgs a) {
+  extern __shared__ double2 smem[];
+  __shared__ double red[64];
+  const int n = a.n, nseq = a.nseq;
+  const long long q0 = (long long)blockIdx.x * nseq;
+  const bool rows_in = (a.in_st == 1);
+  gen_zero_tail(a.p, smem, a.ld, nseq);
+  for (int i = threadIdx.x; i < nseq * n; i += blockDim.x) {
+    int q, t;
+    if (rows_in) { q = i / n; t = i - q * n; } else { t = i / nseq; q = i - t * nseq; }
+    const long long qq = q0 + q;
+    double2 x = make_double2(0.0, 0.0);
+    if (qq < a.B) {
+      const long long off = qq * a.in_sb + (long long)t * a.in_st;
+      if (a.in_cplx) x = ld2(a.in + 2 * off); else x = make_double2(a.in[off], 0.0);
+    }
+    if (MODE == 0) {
+      x = cconj(cmul(x, __ldg(a.gam + t)));  // inverse DFT via conj(FFT(conj))
+    }
+    gen_put(a.p, smem, a.ld, q, t, x);
+  }
+  __syncthreads();
+  fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  const bool rows_out = (a.out_st == 1);
+  double sre = 0.0, sim = 0.0;
+  for (int i = threadIdx.x; i < nseq * n; i += blockDim.x) {
+    int q, t;
+    if (rows_out) { q = i / n; t = i - q * n; } else { t = i / nseq; q = i - t * nseq; }
+    const long long qq = q0 + q;
+    if (qq >= a.B) continue;
+    double2 X = gen_get(a.p, smem, a.ld, q, t);
+    const long long off = qq * a.out_sb + (long long)t * a.out_st;
+    if (MODE == 0) {
+      X = cconj(X);
+      X.x *= a.scale; X.y *= a.scale;
+      reinterpret_cast<double2*>(a.out)[off] = X;
+    } else {
+      X.x *= a.scale; X.y *= a.scale;
+      const double2 Y = cmul(X, __ldg(a.gam + t));
+      sre = fma(Y.x, Y.x, sre);
+      sim = fma(Y.y, Y.y, sim);
+      if (a.out_cplx) reinterpret_cast<double2*>(a.out)[off] = Y; else a.out[off] = Y.x;
+    }
+  }
+  if (MODE == 1) {
+    block_sum2(sre, sim, red);
+    if (threadIdx.x == 0) {
+      atomicAdd(&a.st->sum_re2, sre);
+      atomicAdd(&a.st->sum_im2, sim);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ DST kernels
+// EPI 0: plain orthonormal DST.
+// EPI 1: DST, divide by (shift[level] + mu[mode]), DST  (fused shifted solve on
+//        the outermost spatial axis; level/mode from the line geometry).
+struct DstArgs {
+  FftPlanDev p;
+  int ld, nseq, m, dim;
+  const double* in;
+  double* out;
+  long long nlines;      // rows kernel: number of lines (real or complex)
+  long long ni, no;      // cols kernel: inner / outer line counts
+  long long es, os;      // cols kernel: element / outer strides (elements)
+  double f;              // sqrt(2/(m+1)) / 2
+  const double2* shifts; // EPI 1
+  const double* mu1;     // EPI 1
+  int axis_depth;        // cols kernel: 1 = axis -2, 2 = axis -3
+  StatusDev* st;
+};
+
+// k-th DST coefficient (1-based k) of sequence seq from the FFT buffer.
+__device__ __forceinline__ double2 dst_coef(const DstArgs& a, const double2* buf, int seq, int k) {
+  const double2 X = gen_get(a.p, buf, a.ld, seq, k);
+  return make_double2(-a.f * X.y, a.f * X.x);
+}
+
+// Rows: lines are contiguous; line l occupies [l*m, (l+1)*m).
+template <int V, int CPLX, int EPI>
+__global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_dst_rows(DstArgs a) {
+  extern __shared__ double2 smem[];
+  constexpr int CAP = VT<V>::CAP;
+  const int m = a.m, nseq = a.nseq;
+  const long long s0 = (long long)blockIdx.x * nseq;  // first sequence of the CTA
+  dst_put_zeros(a.p, smem, a.ld, nseq, m);
+  for (int i = threadIdx.x; i < nseq * m; i += blockDim.x) {
+    const int q = i / m, e = i - q * m;
+    const long long s = s0 + q;
+    double2 x = make_double2(0.0, 0.0);
+    if (CPLX) {
+      if (s < a.nlines) x = ld2(a.in + 2 * (s * m + e));
+    } else {
+      const long long l0 = 2 * s, l1 = 2 * s + 1;
+      if (l0 < a.nlines) x.x = a.in[l0 * m + e];
+      if (l1 < a.nlines) x.y = a.in[l1 * m + e];
+    }
+    dst_put(a.p, smem, a.ld, q, m, e, x);
+  }
+  __syncthreads();
+  fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  if (EPI == 1) {
+    // divide in registers, then rebuild the odd extension and transform again
+    constexpr int MAXI = CAP / 2 + 1;
+    double2 hold[MAXI];
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int i = threadIdx.x + u * blockDim.x;
+      if (i < nseq * m) {
+        const int q = i / m, e = i - q * m;
+        const long long s = s0 + q;
+        double2 c = dst_coef(a, smem, q, e + 1);
+        if (s < a.nlines) c = shifted_divide(c, a.shifts[s], __ldg(a.mu1 + e), a.st, s);
+        hold[u] = c;
+      }
+    }
+    __syncthreads();
+    dst_put_zeros(a.p, smem, a.ld, nseq, m);
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int i = threadIdx.x + u * blockDim.x;
+      if (i < nseq * m) {
+        const int q = i / m, e = i - q * m;
+        dst_put(a.p, smem, a.ld, q, m, e, hold[u]);
+      }
+    }
+    __syncthreads();
+    fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  }
+  for (int i = threadIdx.x; i < nseq * m; i += blockDim.x) {
+    const int q = i / m, e = i - q * m;
+    const long long s = s0 + q;
+    const double2 c = dst_coef(a, smem, q, e + 1);
+    if (CPLX) {
+      if (s < a.nlines) reinterpret_cast<double2*>(a.out)[s * m + e] = c;
+    } else {
+      const long long l0 = 2 * s, l1 = 2 * s + 1;
+      if (l0 < a.nlines) a.out[l0 * m + e] = c.x;
+      if (l1 < a.nlines) a.out[l1 * m + e] = c.y;
+    }
+  }
+}
+
+// Cols: element e of line (o, i) at o*os + i + e*es; the CTA takes one outer
+// index and a tile of consecutive inner indices (coalesced loads/stores).
+template <int V, int CPLX, int EPI>
+__global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_dst_cols(DstArgs a) {
+  extern __shared__ double2 smem[];
+  constexpr int CAP = VT<V>::CAP;
+  const int m = a.m, nseq = a.nseq;
+  const int lines_per_cta = CPLX ? nseq : 2 * nseq;
+  const long long ntile = (a.ni + lines_per_cta - 1) / lines_per_cta;
+  const long long o = blockIdx.x / ntile;
+  const long long i0 = (blockIdx.x - o * ntile) * lines_per_cta;
+  const double* base_in = a.in + (CPLX ? 2 : 1) * (o * a.os);
+  double* base_out = a.out + (CPLX ? 2 : 1) * (o * a.os);
+  dst_put_zeros(a.p, smem, a.ld, nseq, m);
+  for (int idx = threadIdx.x; idx < nseq * m; idx += blockDim.x) {
+    const int e = idx / nseq, q = idx - e * nseq;
+    double2 x = make_double2(0.0, 0.0);
+    if (CPLX) {
+      const long long i = i0 + q;
+      if (i < a.ni) x = ld2(base_in + 2 * (i + e * a.es));
+    } else {
+      const long long i = i0 + 2 * q;
+      if (i < a.ni) x.x = base_in[i + e * a.es];
+      if (i + 1 < a.ni) x.y = base_in[i + 1 + e * a.es];
+    }
+    dst_put(a.p, smem, a.ld, q, m, e, x);
+  }
+  __syncthreads();
+  fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  if (EPI == 1) {
+    constexpr int MAXI = CAP / 2 + 1;
+    double2 hold[MAXI];
+    const double2 sh = a.shifts[o];  // outermost axis: o enumerates levels
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int idx = threadIdx.x + u * blockDim.x;
+      if (idx < nseq * m) {
+        const int e = idx / nseq, q = idx - e * nseq;
+        const long long i = i0 + q;
+        double2 c = dst_coef(a, smem, q, e + 1);
+        if (i < a.ni) {
+          double mu;
+          if (a.axis_depth == 1) {
+            mu = __ldg(a.mu1 + e) + __ldg(a.mu1 + i);
+          } else {
+            const int k2 = (int)(i / m), k3 = (int)(i - (long long)k2 * m);
+            mu = (__ldg(a.mu1 + e) + __ldg(a.mu1 + k2)) + __ldg(a.mu1 + k3);
+          }
+          c = shifted_divide(c, sh, mu, a.st, o);
+        }
+        hold[u] = c;
+      }
+    }
+    __syncthreads();
+    dst_put_zeros(a.p, smem, a.ld, nseq, m);
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int idx = threadIdx.x + u * blockDim.x;
+      if (idx < nseq * m) {
+        const int e = idx / nseq, q = idx - e * nseq;
+        dst_put(a.p, smem, a.ld, q, m, e, hold[u]);
+      }
+    }
+    __syncthreads();
+    fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  }
+  for (int idx = threadIdx.x; idx < nseq * m; idx += blockDim.x) {
+    const int e = idx / nseq, q = idx - e * nseq;
+    const double2 c = dst_coef(a, smem, q, e + 1);
+    if (CPLX) {
+      const long long i = i0 + q;
+      if (i < a.ni) reinterpret_cast<double2*>(base_out)[i + e * a.es] = c;
+    } else {
+      const long long i = i0 + 2 * q;
+      if (i < a.ni) base_out[i + e * a.es] = c.x;
+      if (i + 1 < a.ni) base_out[i + 1 + e * a.es] = c.y;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ k_modes
+// Fused solve, pass A: for spatial mode k,
+//   W[t, k] = ghat_k * Re( gamma_inv_t * sum_j exp(-2 pi i jt/n) / (s_j + mu_k) )
+// ghat already carries DST(g) / (divisor * n).
+struct ModesArgs {
+  FftPlanDev p;
+  int ld, nseq, n, m, dim;
+  const double2* shifts;
+  const double2* gaminv;
+  const double* mu1;
+  const double* ghat;
+  double cscale;         // 1 / (divisor * n) applied to ghat
+  long long k_begin, k_count;
+  double* W;
+  long long w_ld;
+  StatusDev* st;
+};
+
+template <int V>
+__global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_modes(ModesArgs a) {
+  extern __shared__ double2 smem[];
+  __shared__ double red[64];
+  __shared__ double s_mu[64];
+  __shared__ double s_c[64];
+  const int n = a.n, nseq = a.nseq;
+  const long long kl0 = (long long)blockIdx.x * nseq;  // local mode offset
+  for (int q = threadIdx.x; q < nseq; q += blockDim.x) {
+    const long long kl = kl0 + q;
+    if (kl < a.k_count) {
+      const long long k = a.k_begin + kl;
+      s_mu[q] = mode_mu(a.mu1, a.m, a.dim, k);
+      s_c[q] = a.ghat[k] * a.cscale;
+    } else {
+      s_mu[q] = 0.0;
+      s_c[q] = 0.0;
+    }
+  }
+  gen_zero_tail(a.p, smem, a.ld, nseq);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nseq * n; i += blockDim.x) {
+    const int q = i / n, j = i - q * n;
+    const double2 s = __ldg(a.shifts + j);
+    double2 v = make_double2(0.0, 0.0);
+    if (kl0 + q < a.k_count) {
+      const double dr = s.x + s_mu[q], di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, j);
+      const double inv = 1.0 / den2;
+      v = make_double2(dr * inv, -di * inv);
+    }
+    gen_put(a.p, smem, a.ld, q, j, v);
+  }
+  __syncthreads();
+  fft_exec_ld<V>(a.p, smem, a.ld, nseq);
+  double sre = 0.0, sim = 0.0;
+  for (int i = threadIdx.x; i < nseq * n; i += blockDim.x) {
+    const int t = i / nseq, q = i - t * nseq;
+    const long long kl = kl0 + q;
+    if (kl >= a.k_count) continue;
+    const double2 X = gen_get(a.p, smem, a.ld, q, t);
+    const double2 Z = cmul(X, __ldg(a.gaminv + t));
+    const double c = s_c[q];
+    const double wr = c * Z.x, wi = c * Z.y;
+    sre = fma(wr, wr, sre);
+    sim = fma(wi, wi, sim);
+    a.W[(long long)t * a.w_ld + kl] = wr;
+  }
+  block_sum2(sre, sim, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.st->sum_re2, sre);
+    atomicAdd(&a.st->sum_im2, sim);
+  }
+}
+
+// ------------------------------------------------------------------ small kernels
+__global__ void k_status_reset(StatusDev* st) {
+  if (threadIdx.x == 0) {
+    st->bad_col = ~0ull;
+    st->sum_re2 = 0.0;
+    st->sum_im2 = 0.0;
+  }
+}
+
+// rhs block of methods.py:158-162: zeros with row 0 = g / divisor.
+__global__ void k_rhs(const double* __restrict__ g, double inv_divisor_mul, double divisor, long long nx,
+                      long long total, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    out[i] = (i < nx) ? g[i] / divisor : 0.0;
+  }
+}
+
+__global__ void k_scale(const double* __restrict__ in, double s, long long n, double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i] * s;
+}
+
+template <typename E>
+__global__ void k_transpose(const E* __restrict__ in, E* __restrict__ out, long long rows, long long cols) {
+  __shared__ E tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * cols + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
+}  // namespace bhcp
+
+// ====================================================================== host
+using namespace bhcp;
+
+struct bhcp_space_plan {
+  int device, dim, num_cells, m;
+  long long nx;          // m^dim interior unknowns
+  double* mu1_dev;       // m doubles
+  FftPlanHost dst;       // FFT of length 2(m+1)
+};
+
+struct bhcp_time_plan {
+  int device, n;
+  double2* tables;       // gamma | gamma_inv | shifts  (3n double2)
+  FftPlanHost fft;       // FFT of length n
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  return fail(BHCP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+std::mutex g_init_mutex;
+bool g_init_done[64] = {false};
+
+template <typename K>
+void allow_smem(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+#define BHCP_FOR_VARIANTS(X) X(V256) X(V512) X(V768)
+
+void set_all_attributes() {
+#define BHCP_ATTR(VV)                                   \
+  allow_smem(k_time<VV, 0>);                            \
+  allow_smem(k_time<VV, 1>);                            \
+  allow_smem(k_dst_rows<VV, 0, 0>);                     \
+  allow_smem(k_dst_rows<VV, 1, 0>);                     \
+  allow_smem(k_dst_rows<VV, 1, 1>);                     \
+  allow_smem(k_dst_cols<VV, 0, 0>);                     \
+  allow_smem(k_dst_cols<VV, 1, 0>);                     \
+  allow_smem(k_dst_cols<VV, 1, 1>);                     \
+  allow_smem(k_modes<VV>);
+  BHCP_FOR_VARIANTS(BHCP_ATTR)
+#undef BHCP_ATTR
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+size_t smem_bytes(const FftPlanHost& p, int nseq) { return size_t(nseq) * p.ld * sizeof(double2); }
+
+// --- DST pass launchers --------------------------------------------------------
+int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
+                int epi, const double2* shifts, StatusDev* st, cudaStream_t s) {
+  const FftPlanHost& P = sp->dst;
+  const int nseq_max = P.max_seqs(kSmemBudget);
+  if (nseq_max < 1) return fail(BHCP_ERR_INVALID, "DST length does not fit the FFT engine");
+  const long long seqs = cplx ? nlines : (nlines + 1) / 2;
+  const int nseq = (int)(seqs < nseq_max ? seqs : nseq_max);
+  if (seqs == 0) return BHCP_OK;
+  DstArgs a{};
+  a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.m = sp->m; a.dim = sp->dim;
+  a.in = in; a.out = out; a.nlines = nlines;
+  a.f = sqrt(2.0 / (sp->m + 1)) * 0.5;
+  a.shifts = shifts; a.mu1 = sp->mu1_dev; a.st = st;
+  const long long grid = (seqs + nseq - 1) / nseq;
+  const size_t sm = smem_bytes(P, nseq);
+#define BHCP_ROWS(VV)                                                                  \
+  case VV:                                                                             \
+    if (epi) k_dst_rows<VV, 1, 1><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);            \
+    else if (cplx) k_dst_rows<VV, 1, 0><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);      \
+    else k_dst_rows<VV, 0, 0><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);                \
+    break;
+  switch (P.variant) { BHCP_FOR_VARIANTS(BHCP_ROWS) }
+#undef BHCP_ROWS
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_rows launch");
+  return BHCP_OK;
+}
+
+int launch_cols(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long ni,
+                long long no, int depth, int epi, const double2* shifts, StatusDev* st, cudaStream_t s) {
+  const FftPlanHost& P = sp->dst;
+  const int nseq_max = P.max_seqs(kSmemBudget);
+  if (nseq_max < 1) return fail(BHCP_ERR_INVALID, "DST length does not fit the FFT engine");
+  const long long lines_needed = ni;
+  long long seqs_needed = cplx ? lines_needed : (lines_needed + 1) / 2;
+  const int nseq = (int)(seqs_needed < nseq_max ? seqs_needed : nseq_max);
+  if (ni == 0 || no == 0) return BHCP_OK;
+  DstArgs a{};
+  a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.m = sp->m; a.dim = sp->dim;
+  a.in = in; a.out = out; a.ni = ni; a.no = no; a.es = ni; a.os = (long long)sp->m * ni;
+  a.f = sqrt(2.0 / (sp->m + 1)) * 0.5;
+  a.shifts = shifts; a.mu1 = sp->mu1_dev; a.axis_depth = depth; a.st = st;
+  const int lines_per_cta = cplx ? nseq : 2 * nseq;
+  const long long ntile = (ni + lines_per_cta - 1) / lines_per_cta;
+  const long long grid = ntile * no;
+  if (grid > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "grid too large");
+  const size_t sm = smem_bytes(P, nseq);
+#define BHCP_COLS(VV)                                                                  \
+  case VV:                                                                             \
+    if (epi) k_dst_cols<VV, 1, 1><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);            \
+    else if (cplx) k_dst_cols<VV, 1, 0><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);      \
+    else k_dst_cols<VV, 0, 0><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);                \
+    break;
+  switch (P.variant) { BHCP_FOR_VARIANTS(BHCP_COLS) }
+#undef BHCP_COLS
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_cols launch");
+  return BHCP_OK;
+}
+
+long long ipow(long long b, int e) {
+  long long r = 1;
+  while (e-- > 0) r *= b;
+  return r;
+}
+
+// Orthonormal DST over all spatial axes of `batch` fields: axis -1, -2, -3.
+int sine_passes(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long batch,
+                cudaStream_t s) {
+  const int d = sp->dim, m = sp->m;
+  int rc = launch_rows(sp, in, out, cplx, batch * ipow(m, d - 1), 0, nullptr, nullptr, s);
+  if (rc) return rc;
+  for (int depth = 1; depth < d; ++depth) {
+    rc = launch_cols(sp, out, out, cplx, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0,
+                     nullptr, nullptr, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
+}
+
+// Step (b) on level-major complex fields: forward DST on the inner axes, a
+// fused DST-divide-DST on the outermost axis, inverse DST on the inner axes.
+int step_b_passes(const bhcp_space_plan* sp, const double* in, double* out, long long batch,
+                  const double2* shifts, StatusDev* st, cudaStream_t s) {
+  const int d = sp->dim, m = sp->m;
+  if (d == 1) return launch_rows(sp, in, out, 1, batch, 1, shifts, st, s);
+  int rc = launch_rows(sp, in, out, 1, batch * ipow(m, d - 1), 0, nullptr, nullptr, s);
+  if (rc) return rc;
+  for (int depth = 1; depth < d - 1; ++depth) {
+    rc = launch_cols(sp, out, out, 1, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0, nullptr,
+                     nullptr, s);
+    if (rc) return rc;
+  }
+  rc = launch_cols(sp, out, out, 1, ipow(m, d - 1), batch, d - 1, 1, shifts, st, s);
+  if (rc) return rc;
+  for (int depth = d - 2; depth >= 1; --depth) {
+    rc = launch_cols(sp, out, out, 1, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0, nullptr,
+                     nullptr, s);
+    if (rc) return rc;
+  }
+  return launch_rows(sp, out, out, 1, batch * ipow(m, d - 1), 0, nullptr, nullptr, s);
+}
+
+int launch_time(const bhcp_time_plan* tp, int mode, const double* in, int in_cplx, long long B, long long in_sb,
+                long long in_st, double* out, int out_cplx, long long out_sb, long long out_st, StatusDev* st,
+                cudaStream_t s) {
+  if (B == 0) return BHCP_OK;
+  if (in_st != 1 && in_sb != 1) return fail(BHCP_ERR_INVALID, "one input stride must be 1");
+  const FftPlanHost& P = tp->fft;
+  int nseq = P.max_seqs(kSmemBudget);
+  if (nseq < 1) return fail(BHCP_ERR_INVALID, "time length does not fit the FFT engine");
+  if (nseq > 32) nseq = 32;
+  if (B < nseq) nseq = (int)B;
+  TimeArgs a{};
+  a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.n = tp->n;
+  a.in = in; a.in_cplx = in_cplx; a.B = B; a.in_sb = in_sb; a.in_st = in_st;
+  a.out = out; a.out_cplx = out_cplx; a.out_sb = out_sb; a.out_st = out_st;
+  a.gam = mode == 0 ? tp->tables : tp->tables + tp->n;
+  a.scale = 1.0 / sqrt((double)tp->n);
+  a.st = st;
+  const long long grid = (B + nseq - 1) / nseq;
+  const size_t sm = smem_bytes(P, nseq);
+#define BHCP_TIME(VV)                                                             \
+  case VV:                                                                        \
+    if (mode == 0) k_time<VV, 0><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);        \
+    else k_time<VV, 1><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a);                  \
+    break;
+  switch (P.variant) { BHCP_FOR_VARIANTS(BHCP_TIME) }
+#undef BHCP_TIME
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_time launch");
+  return BHCP_OK;
+}
+
+int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
+                 long long k_begin, long long k_end, double* W, long long w_ld, StatusDev* st, cudaStream_t s) {
+  const long long kc = k_end - k_begin;
+  if (kc <= 0) return BHCP_OK;
+  const FftPlanHost& P = tp->fft;
+  int nseq = P.max_seqs(kSmemBudget);
+  if (nseq < 1) return fail(BHCP_ERR_INVALID, "time length does not fit the FFT engine");
+  if (nseq > 64) nseq = 64;
+  if (kc < nseq) nseq = (int)kc;
+  ModesArgs a{};
+  a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.n = tp->n; a.m = sp->m; a.dim = sp->dim;
+  a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev;
+  a.ghat = ghat; a.cscale = cscale; a.k_begin = k_begin; a.k_count = kc; a.W = W; a.w_ld = w_ld; a.st = st;
+  const long long grid = (kc + nseq - 1) / nseq;
+  const size_t sm = smem_bytes(P, nseq);
+#define BHCP_MODES(VV) \
+  case VV: k_modes<VV><<<(unsigned)grid, VT<VV>::T, sm, s>>>(a); break;
+  switch (P.variant) { BHCP_FOR_VARIANTS(BHCP_MODES) }
+#undef BHCP_MODES
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes launch");
+  return BHCP_OK;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace
+
+namespace bhcp {
+bool ensure_device_constants(int device, std::string* err) {
+  std::lock_guard<std::mutex> lk(g_init_mutex);
+  if (device < 0 || device >= 64) { *err = "bad device"; return false; }
+  if (g_init_done[device]) return true;
+  double cs[kOddRootsTotal], sn[kOddRootsTotal];
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int R : {3, 5, 7, 11, 13, 17, 19, 23}) {
+    const int off = odd_root_offset(R);
+    for (int q = 0; q < R; ++q) {
+      long double ang = 2.0L * pi * (long double)q / (long double)R;
+      cs[off + q] = (double)cosl(ang);
+      sn[off + q] = (double)sinl(ang);
+    }
+  }
+  if (cudaMemcpyToSymbol(c_root_cos, cs, sizeof(cs)) != cudaSuccess ||
+      cudaMemcpyToSymbol(c_root_sin, sn, sizeof(sn)) != cudaSuccess) {
+    *err = std::string("cudaMemcpyToSymbol: ") + cudaGetErrorString(cudaGetLastError());
+    return false;
+  }
+  set_all_attributes();
+  g_init_done[device] = true;
+  return true;
+}
+}  // namespace bhcp
+
+// ====================================================================== C ABI
+extern "C" {
+
+int bhcp_version(void) { return 100; }
+const char* bhcp_last_error(void) { return g_last_error.c_str(); }
+size_t bhcp_status_bytes(void) { return sizeof(StatusDev); }
+
+int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1_host, bhcp_space_plan** out) {
+  if (!out || !mu1_host) return fail(BHCP_ERR_INVALID, "null argument");
+  if (dim < 1 || dim > 3) return fail(BHCP_ERR_INVALID, "dim must be 1, 2 or 3");
+  if (num_cells < 2) return fail(BHCP_ERR_INVALID, "need at least 2 cells per edge");
+  DeviceGuard g(device);
+  std::string err;
+  if (!ensure_device_constants(device, &err)) return fail(BHCP_ERR_CUDA, err);
+  auto* sp = new bhcp_space_plan();
+  sp->device = device; sp->dim = dim; sp->num_cells = num_cells; sp->m = num_cells - 1;
+  sp->nx = ipow(sp->m, dim);
+  if (!build_fft_plan(2 * num_cells, &sp->dst, &err)) { delete sp; return fail(BHCP_ERR_INVALID, err); }
+  if (cudaMalloc(&sp->mu1_dev, sizeof(double) * sp->m) != cudaSuccess) {
+    free_fft_plan(&sp->dst); delete sp; return cuda_fail("cudaMalloc mu1");
+  }
+  cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
+  *out = sp;
+  return BHCP_OK;
+}
+
+void bhcp_space_plan_destroy(bhcp_space_plan* sp) {
+  if (!sp) return;
+  DeviceGuard g(sp->device);
+  free_fft_plan(&sp->dst);
+  cudaFree(sp->mu1_dev);
+  delete sp;
+}
+
+int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, const double* gamma_inv_host,
+                          const double* shifts_host, bhcp_time_plan** out) {
+  if (!out || !gamma_host || !gamma_inv_host || !shifts_host) return fail(BHCP_ERR_INVALID, "null argument");
+  if (n_levels < 1) return fail(BHCP_ERR_INVALID, "n_levels must be >= 1");
+  DeviceGuard g(device);
+  std::string err;
+  if (!ensure_device_constants(device, &err)) return fail(BHCP_ERR_CUDA, err);
+  auto* tp = new bhcp_time_plan();
+  tp->device = device; tp->n = n_levels;
+  if (!build_fft_plan(n_levels, &tp->fft, &err)) { delete tp; return fail(BHCP_ERR_INVALID, err); }
+  const size_t nb = sizeof(double2) * n_levels;
+  if (cudaMalloc(&tp->tables, 3 * nb) != cudaSuccess) {
+    free_fft_plan(&tp->fft); delete tp; return cuda_fail("cudaMalloc time tables");
+  }
+  cudaMemcpy(tp->tables, gamma_host, nb, cudaMemcpyHostToDevice);
+  cudaMemcpy(tp->tables + n_levels, gamma_inv_host, nb, cudaMemcpyHostToDevice);
+  cudaMemcpy(tp->tables + 2 * n_levels, shifts_host, nb, cudaMemcpyHostToDevice);
+  *out = tp;
+  return BHCP_OK;
+}
+
+void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
+  if (!tp) return;
+  DeviceGuard g(tp->device);
+  free_fft_plan(&tp->fft);
+  cudaFree(tp->tables);
+  delete tp;
+}
+
+int bhcp_status_reset(void* status_dev, void* stream) {
+  if (!status_dev) return fail(BHCP_ERR_INVALID, "null status");
+  k_status_reset<<<1, 32, 0, as_stream(stream)>>>(reinterpret_cast<StatusDev*>(status_dev));
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("status reset");
+  return BHCP_OK;
+}
+
+int bhcp_read_status(const void* status_dev, double tol, bhcp_status* st, void* stream) {
+  if (!status_dev || !st) return fail(BHCP_ERR_INVALID, "null argument");
+  if (cudaStreamSynchronize(as_stream(stream)) != cudaSuccess) return cuda_fail("stream sync");
+  StatusDev h;
+  if (cudaMemcpy(&h, status_dev, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_fail("status copy");
+  st->bad_column = h.bad_col == ~0ull ? -1 : (int64_t)h.bad_col;
+  st->norm = sqrt(h.sum_re2 + h.sum_im2);
+  st->residue = sqrt(h.sum_im2);
+  st->code = BHCP_OK;
+  if (st->bad_column >= 0) st->code = BHCP_ERR_SINGULAR_SHIFT;
+  else if (st->residue > tol * fmax(st->norm, 2.2250738585072014e-308)) st->code = BHCP_ERR_IMAGINARY_RESIDUE;
+  return BHCP_OK;
+}
+
+int bhcp_sine_transform(const bhcp_space_plan* sp, const void* in, void* out, int is_complex, int64_t batch,
+                        void* stream) {
+  if (!sp || !in || !out || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  return sine_passes(sp, (const double*)in, (double*)out, is_complex ? 1 : 0, batch, as_stream(stream));
+}
+
+int bhcp_step_b(const bhcp_space_plan* sp, const void* in, void* out, const double* shifts_dev, int64_t batch,
+                void* status_dev, void* stream) {
+  if (!sp || !in || !out || !shifts_dev || !status_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  return step_b_passes(sp, (const double*)in, (double*)out, batch, (const double2*)shifts_dev,
+                       (StatusDev*)status_dev, as_stream(stream));
+}
+
+int bhcp_to_eigenspace(const bhcp_time_plan* tp, const void* in, int in_is_complex, int64_t batch, int64_t in_sb,
+                       int64_t in_st, void* out, int64_t out_sb, int64_t out_st, void* stream) {
+  if (!tp || !in || !out || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(tp->device);
+  return launch_time(tp, 0, (const double*)in, in_is_complex ? 1 : 0, batch, in_sb, in_st, (double*)out, 1,
+                     out_sb, out_st, nullptr, as_stream(stream));
+}
+
+int bhcp_from_eigenspace(const bhcp_time_plan* tp, const void* in, int64_t batch, int64_t in_sb, int64_t in_st,
+                         void* out, int out_is_complex, int64_t out_sb, int64_t out_st, void* status_dev,
+                         void* stream) {
+  if (!tp || !in || !out || !status_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(tp->device);
+  return launch_time(tp, 1, (const double*)in, 1, batch, in_sb, in_st, (double*)out, out_is_complex ? 1 : 0,
+                     out_sb, out_st, (StatusDev*)status_dev, as_stream(stream));
+}
+
+size_t bhcp_pint_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
+  if (!sp || !tp) return 0;
+  return align256(sizeof(StatusDev)) + align256(sizeof(double) * sp->nx) +
+         align256(sizeof(double) * sp->nx * (size_t)tp->n);
+}
+
+void* bhcp_pint_status_ptr(const bhcp_space_plan*, const bhcp_time_plan*, void* ws) { return ws; }
+
+int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale, double* ghat_dev, void* stream) {
+  if (!sp || !g_dev || !ghat_dev) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  int rc = sine_passes(sp, g_dev, ghat_dev, 0, 1, s);
+  if (rc) return rc;
+  if (scale != 1.0) {
+    k_scale<<<(unsigned)((sp->nx + 255) / 256 < 4096 ? (sp->nx + 255) / 256 : 4096), 256, 0, s>>>(ghat_dev, scale,
+                                                                                                  sp->nx, ghat_dev);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_scale");
+  }
+  return BHCP_OK;
+}
+
+int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat_dev, int64_t k_begin,
+                    int64_t k_end, double* w_dev, int64_t w_ld, void* status_dev, void* stream) {
+  if (!sp || !tp || !ghat_dev || !w_dev || !status_dev) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (k_begin < 0 || k_end > sp->nx || k_begin > k_end) return fail(BHCP_ERR_INVALID, "bad mode range");
+  DeviceGuard g(sp->device);
+  return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, w_dev, w_ld, (StatusDev*)status_dev,
+                      as_stream(stream));
+}
+
+int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t batch,
+                     void* stream) {
+  if (!sp || !in_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  return sine_passes(sp, in_dev, out_dev, 0, batch, as_stream(stream));
+}
+
+int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* g_dev, double divisor,
+                    double* y_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!sp || !tp || !g_dev || !y_dev || !ws) return fail(BHCP_ERR_INVALID, "null argument");
+  if (ws_bytes < bhcp_pint_workspace_bytes(sp, tp)) return fail(BHCP_ERR_INVALID, "workspace too small");
+  if (sp->device != tp->device) return fail(BHCP_ERR_INVALID, "plans on different devices");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  char* w = (char*)ws;
+  StatusDev* st = (StatusDev*)w;
+  double* ghat = (double*)(w + align256(sizeof(StatusDev)));
+  double* W = (double*)(w + align256(sizeof(StatusDev)) + align256(sizeof(double) * sp->nx));
+  k_status_reset<<<1, 32, 0, s>>>(st);
+  int rc = sine_passes(sp, g_dev, ghat, 0, 1, s);
+  if (rc) return rc;
+  const double cscale = 1.0 / (divisor * (double)tp->n);
+  rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, sp->nx, st, s);
+  if (rc) return rc;
+  return sine_passes(sp, W, y_dev, 0, tp->n, s);
+}
+
+size_t bhcp_pint_unfused_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
+  if (!sp || !tp) return 0;
+  return align256(sizeof(StatusDev)) + align256(sizeof(double2) * sp->nx * (size_t)tp->n);
+}
+
+void* bhcp_pint_unfused_status_ptr(const bhcp_space_plan*, const bhcp_time_plan*, void* ws) { return ws; }
+
+int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* g_dev,
+                            double divisor, double* y_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!sp || !tp || !g_dev || !y_dev || !ws) return fail(BHCP_ERR_INVALID, "null argument");
+  if (ws_bytes < bhcp_pint_unfused_workspace_bytes(sp, tp)) return fail(BHCP_ERR_INVALID, "workspace too small");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  char* w = (char*)ws;
+  StatusDev* st = (StatusDev*)w;
+  double* S = (double*)(w + align256(sizeof(StatusDev)));
+  const long long nx = sp->nx, n = tp->n, total = nx * n;
+  k_status_reset<<<1, 32, 0, s>>>(st);
+  // rhs assembly (methods.py:158-162) into y, used as scratch
+  k_rhs<<<(unsigned)(total / 256 + 1 < 65535 ? total / 256 + 1 : 65535), 256, 0, s>>>(g_dev, 0.0, divisor, nx,
+                                                                                      total, y_dev);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_rhs");
+  // step (a): sequences are spatial points x, time stride nx
+  int rc = launch_time(tp, 0, y_dev, 0, nx, 1, nx, S, 1, 1, nx, nullptr, s);
+  if (rc) return rc;
+  // step (b): level-major complex fields
+  rc = step_b_passes(sp, S, S, n, tp->tables + 2 * n, st, s);
+  if (rc) return rc;
+  // step (c)
+  return launch_time(tp, 1, S, 1, nx, 1, nx, y_dev, 0, 1, nx, st, s);
+}
+
+int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols, int elem_bytes, void* stream) {
+  if (!in || !out || rows < 0 || cols < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (rows == 0 || cols == 0) return BHCP_OK;
+  dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (grid.y > 65535) return fail(BHCP_ERR_INVALID, "transpose too tall");
+  dim3 block(32, 8);
+  if (elem_bytes == 8)
+    k_transpose<double><<<grid, block, 0, as_stream(stream)>>>((const double*)in, (double*)out, rows, cols);
+  else if (elem_bytes == 16)
+    k_transpose<double2><<<grid, block, 0, as_stream(stream)>>>((const double2*)in, (double2*)out, rows, cols);
+  else
+    return fail(BHCP_ERR_INVALID, "elem_bytes must be 8 or 16");
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_transpose");
+  return BHCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,182 @@
+// plan.cpp -- host construction of FFT plans: factorisation, twiddles, and
+// Bluestein chirp/filter tables, all computed in long double and rounded once.
+#include "plan.h"
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+namespace bhcp {
+
+namespace {
+
+using cld = std::complex<long double>;
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+bool is_direct_prime(int p) {
+  return p == 2 || p == 3 || p == 5 || p == 7 || p == 11 || p == 13 || p == 17 || p == 19 || p == 23;
+}
+
+// Factor L into Stockham radices. restricted: only {2,3,4,5} (V768 register budget).
+bool factor_direct(int L, bool restricted, std::vector<int>* radices) {
+  radices->clear();
+  int a = 0;
+  while (L % 2 == 0) { L /= 2; ++a; }
+  if (restricted) {
+    while (a >= 2) { radices->push_back(4); a -= 2; }
+  } else {
+    while (a >= 3) { radices->push_back(8); a -= 3; }
+    if (a == 2) { radices->push_back(4); a = 0; }
+  }
+  if (a == 1) radices->push_back(2);
+  for (int p = 3; L > 1; p += 2) {
+    while (L % p == 0) {
+      if (!is_direct_prime(p)) return false;
+      if (restricted && p > 5) return false;
+      radices->push_back(p);
+      L /= p;
+    }
+    if (p > 23 && L > 1) return false;
+  }
+  return true;
+}
+
+bool smooth235(int n) {
+  for (int p : {2, 3, 5}) while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+// Simple recursive mixed-radix DFT in long double (host; smooth sizes only),
+// forward sign exp(-2 pi i jk / n).
+void host_dft(std::vector<cld>& x) {
+  const int n = (int)x.size();
+  if (n <= 1) return;
+  int p = 2;
+  while (n % p) ++p;
+  const int m = n / p;
+  std::vector<std::vector<cld>> sub(p, std::vector<cld>(m));
+  for (int r = 0; r < p; ++r)
+    for (int j = 0; j < m; ++j) sub[r][j] = x[j * p + r];
+  for (int r = 0; r < p; ++r) host_dft(sub[r]);
+  for (int k = 0; k < n; ++k) {
+    cld acc = 0;
+    for (int r = 0; r < p; ++r) {
+      long long e = ((long long)r * k) % n;
+      long double ang = -2.0L * kPi * (long double)e / (long double)n;
+      acc += sub[r][k % m] * cld(cosl(ang), sinl(ang));
+    }
+    x[k] = acc;
+  }
+}
+
+double2 to_d2(cld z) { return make_double2((double)z.real(), (double)z.imag()); }
+
+}  // namespace
+
+int variant_capacity(const std::vector<int>& rad, int variant) {
+  int c = 1 << 30;
+  for (int R : rad) {
+    const int s = stage_capacity(R, kVariantCap[variant]);
+    if (s < c) c = s;
+  }
+  if (rad.empty()) c = kVariantCap[variant];
+  return c * kVariantThreads[variant];
+}
+
+bool smooth23(int n) {
+  for (int p : {2, 3}) while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
+  if (L < 1) { *err = "FFT length must be >= 1"; return false; }
+  FftPlanHost p;
+  std::vector<int> rad;
+  int Lc = L;
+  bool blue = false;
+  bool ok = false;
+  // 1) direct mixed-radix plan on a 256/512-thread CTA
+  if (factor_direct(L, false, &rad)) {
+    for (int v : {V256, V512}) {
+      if (variant_capacity(rad, v) >= L) { p.variant = v; ok = true; break; }
+    }
+  }
+  // 2) direct plan with the small radix set on a 768-thread CTA
+  if (!ok && factor_direct(L, true, &rad) && variant_capacity(rad, V768) >= L) {
+    p.variant = V768;
+    ok = true;
+  }
+  // 3) Bluestein with a 5-smooth length, then a 3-smooth one on 768 threads
+  if (!ok) {
+    blue = true;
+    Lc = 2 * L - 1;
+    while (!smooth235(Lc)) ++Lc;
+    factor_direct(Lc, false, &rad);
+    for (int v : {V256, V512}) {
+      if (variant_capacity(rad, v) >= Lc) { p.variant = v; ok = true; break; }
+    }
+    if (!ok) {
+      Lc = 2 * L - 1;
+      while (!smooth23(Lc)) ++Lc;
+      factor_direct(Lc, true, &rad);
+      if (variant_capacity(rad, V768) >= Lc) { p.variant = V768; ok = true; }
+    }
+  }
+  if (!ok) {
+    *err = "transform length " + std::to_string(L) + " is beyond the shared-memory FFT engine";
+    return false;
+  }
+  p.cap_elems = variant_capacity(rad, p.variant);
+  if ((int)rad.size() > kMaxStages) { *err = "too many FFT stages"; return false; }
+  if (L == 1) rad.clear();
+  p.d.L = L;
+  p.d.Lc = Lc;
+  p.d.blue = blue ? 1 : 0;
+  p.d.nst = (int)rad.size();
+  for (size_t i = 0; i < rad.size(); ++i) p.d.radix[i] = rad[i];
+  p.ld = (Lc % 2 == 0) ? Lc + 1 : Lc;
+
+  // Host tables
+  std::vector<double2> tw(Lc), chirp, bhat;
+  for (int k = 0; k < Lc; ++k) {
+    long double ang = -2.0L * kPi * (long double)k / (long double)Lc;
+    tw[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  if (blue) {
+    chirp.resize(L);
+    std::vector<cld> cl(L);
+    for (int j = 0; j < L; ++j) {
+      long long e = ((long long)j * j) % (2LL * L);
+      long double ang = -kPi * (long double)e / (long double)L;
+      cl[j] = cld(cosl(ang), sinl(ang));
+      chirp[j] = to_d2(cl[j]);
+    }
+    std::vector<cld> b(Lc, cld(0, 0));
+    for (int j = 0; j < L; ++j) b[j] = std::conj(cl[j]);
+    for (int j = 1; j < L; ++j) b[Lc - j] = std::conj(cl[j]);
+    host_dft(b);
+    bhat.resize(Lc);
+    for (int k = 0; k < Lc; ++k) bhat[k] = to_d2(b[k] / (long double)Lc);
+  }
+  size_t bytes = (tw.size() + chirp.size() + bhat.size()) * sizeof(double2);
+  if (cudaMalloc(&p.mem, bytes) != cudaSuccess) { *err = "cudaMalloc failed for FFT plan"; return false; }
+  double2* base = (double2*)p.mem;
+  cudaMemcpy(base, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  p.d.tw = base;
+  if (blue) {
+    cudaMemcpy(base + Lc, chirp.data(), chirp.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    cudaMemcpy(base + Lc + L, bhat.data(), bhat.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    p.d.chirp = base + Lc;
+    p.d.bhat = base + Lc + L;
+  }
+  if (cudaGetLastError() != cudaSuccess) { *err = "cudaMemcpy failed for FFT plan"; return false; }
+  *out = p;
+  return true;
+}
+
+void free_fft_plan(FftPlanHost* p) {
+  if (p->mem) cudaFree(p->mem);
+  p->mem = nullptr;
+}
+
+}  // namespace bhcp

@@ -1,0 +1,42 @@
+// plan.h -- host-side FFT / DST / time plans (built once, immutable afterwards).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "fft_types.h"
+
+namespace bhcp {
+
+// Kernel variants: threads per CTA and per-thread register capacity (complex
+// values held per Stockham stage). The host picks the smallest variant whose
+// CAP*T covers one sequence of the core length.
+enum Variant { V256 = 0, V512 = 1, V768 = 2 };
+constexpr int kVariantThreads[3] = {256, 512, 768};
+constexpr int kVariantCap[3] = {16, 16, 12};
+
+struct FftPlanHost {
+  FftPlanDev d{};
+  int ld = 0;           // shared-memory stride per sequence (odd -> conflict-light)
+  int variant = 0;
+  int cap_elems = 0;    // complex elements one CTA can transform (all stages)
+  void* mem = nullptr;  // device allocation (twiddles, chirp, bhat)
+  int capacity() const { return cap_elems; }
+  int threads() const { return kVariantThreads[variant]; }
+  // max sequences per CTA given the register capacity and a shared-memory budget
+  int max_seqs(size_t smem_budget) const {
+    int a = capacity() / d.Lc;
+    int b = (int)(smem_budget / (size_t(ld) * sizeof(double2)));
+    return a < b ? a : b;
+  }
+};
+
+// Builds the plan on the current device; returns false and sets err on failure.
+bool build_fft_plan(int L, FftPlanHost* out, std::string* err);
+void free_fft_plan(FftPlanHost* p);
+
+// Upload the odd-radix codelet constants to the current device (idempotent).
+bool ensure_device_constants(int device, std::string* err);
+
+}  // namespace bhcp
