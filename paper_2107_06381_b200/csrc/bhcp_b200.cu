@@ -597,9 +597,14 @@ struct DeviceGuard {
 std::mutex g_init_mutex;
 bool g_init_done[64] = {false};
 
+int g_smem_optin = 0;
+
 template <typename K>
 void allow_smem(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) != cudaSuccess) return;
+  const int dyn = g_smem_optin - (int)fa.sharedSizeBytes;
+  if (dyn > 0) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
 }
 
 #define BHCP_FOR_VARIANTS(X) X(V256) X(V512) X(V768)
@@ -802,7 +807,13 @@ bool ensure_device_constants(int device, std::string* err) {
     *err = std::string("cudaMemcpyToSymbol: ") + cudaGetErrorString(cudaGetLastError());
     return false;
   }
+  cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   set_all_attributes();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    *err = std::string("kernel attribute setup: ") + cudaGetErrorString(e);
+    return false;
+  }
   g_init_done[device] = true;
   return true;
 }

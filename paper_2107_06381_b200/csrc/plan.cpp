@@ -159,6 +159,7 @@ bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
     for (int k = 0; k < Lc; ++k) bhat[k] = to_d2(b[k] / (long double)Lc);
   }
   size_t bytes = (tw.size() + chirp.size() + bhat.size()) * sizeof(double2);
+  cudaGetLastError();  // clear any stale error before checking our own calls
   if (cudaMalloc(&p.mem, bytes) != cudaSuccess) { *err = "cudaMalloc failed for FFT plan"; return false; }
   double2* base = (double2*)p.mem;
   cudaMemcpy(base, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
@@ -169,7 +170,8 @@ bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
     p.d.chirp = base + Lc;
     p.d.bhat = base + Lc + L;
   }
-  if (cudaGetLastError() != cudaSuccess) { *err = "cudaMemcpy failed for FFT plan"; return false; }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { *err = std::string("FFT plan upload: ") + cudaGetErrorString(e); return false; }
   *out = p;
   return true;
 }
