@@ -1,0 +1,343 @@
+"""Benchmark of the PinT QBVM/MQBVM all-at-once solve on B200.
+
+Contract (see the task statement): ``python bench.py --gpus N --steps K
+--warmup W`` prints ONE JSON line on rank 0. A "step" is one complete solve
+of BASELINE.json config 2 (2D pint-mqbvm, 511^2 interior, N = 512 steps,
+133,955,073 space-time DOFs) with the data g already resident in HBM; the
+metric is space-time DOFs/s over all ranks.
+
+* value      -- K solves timed with CUDA events on the launching stream,
+                barrier + synchronize on both sides, max over ranks.
+* e2e        -- the same solve through the C-ABI call with HOST buffers:
+                pinned g -> device, bhcp_pint_solve, full trajectory -> pinned
+                host, every step inside the timed region.
+* roofline   -- dominant kernel of the step, algorithmic bytes / its average
+                CUDA-event duration vs the measured HBM copy bandwidth.
+* cpu_baseline -- the reference 3-step algorithm (oracle port, bit-identical
+                to the reference on the golden vectors) on a bounded sample of
+                the same workload, 1 host core, rank 0 at N=1.
+* ``--impl reference`` times that CPU path with all host threads instead.
+
+N > 1: slab decomposition (mode slabs -> NCCL all-to-all -> level slabs),
+strong scaling of the one c2 problem over the ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG_NAME = "c2"
+METRIC = "space-time DOFs/s of QBVM/MQBVM all-at-once solve; % of HBM roofline"
+UNIT = "DOF/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default=CONFIG_NAME)
+    p.add_argument("--cpu-fraction", type=float, default=0.1,
+                   help="fraction of every per-unit operation in the CPU-baseline sample")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the GPU is loaded."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_sample(w, kind, alpha, fraction, workers):
+    from oracle import bhcp_oracle as O
+
+    dof, secs = O.solve_pint_sample(kind, alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
+                                    w.g_delta, fraction, workers=workers)
+    return dof, secs
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return
+    from paper_2107_06381_b200 import workloads
+
+    w = workloads.make(args.config)
+    kind, alpha = w.kinds[0], w.alphas[0]
+    cores = os.cpu_count() or 1
+    frac = args.cpu_fraction
+    for _ in range(args.warmup):
+        cpu_sample(w, kind, alpha, frac / 4, cores)
+    total_dof, total_s = 0.0, 0.0
+    for _ in range(args.steps):
+        dof, s = cpu_sample(w, kind, alpha, frac, cores)
+        total_dof += dof
+        total_s += s
+    value = total_dof / total_s
+    sample = (f"{args.config}: per step, fraction {frac} of every per-unit op of the 3-step solve "
+              f"(time FFTs of {frac:.0%} of rows, shifted solves of {frac:.0%} of levels on {cores} threads)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config construction)",
+        "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, alpha=1e-2",
+                   "dof_per_solve": w.dof},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2107_06381_b200 import _lib, plans, workloads
+    from paper_2107_06381_b200 import distributed as D
+    import paper_2107_06381_b200 as B
+
+    w = workloads.make(args.config)
+    kind, alpha = w.kinds[0], w.alphas[0]
+    grid = B.build_grid(w.dim, w.length, w.num_cells)
+    tg = B.TimeGrid(w.horizon, w.num_steps)
+    system = B.assemble(B.MethodKind(kind), alpha, grid, tg, w.g_delta)
+    divisor = system.method.condition_divisor(tg.tau)
+    dev = torch.device("cuda", local)
+    g_dev = torch.from_numpy(w.g_delta).to(dev)
+    stream = torch.cuda.current_stream()
+    lib = _lib.lib()
+    nx, n = w.n_space, w.n_levels
+
+    if world == 1:
+        plan = B.PintPlan(grid, n, tg.tau, system.omega)
+        y = torch.empty((n, nx), dtype=torch.float64, device=dev)
+        ws = plan.workspace()
+        wsp = ws.data_ptr()
+        status = ctypes.c_void_p(wsp)
+        ghat = ctypes.c_void_p(wsp + 256)
+        W = ctypes.c_void_p(wsp + 256 + ((8 * nx + 255) // 256) * 256)
+        sh = plans.stream_handle()
+        sp, tp = plan.sp.handle, plan.tp.handle
+        ev = None
+
+        def step(record=None):
+            # phases: [0] ghat, [1] k_modes, [2 + a] DST axis pass a
+            if record:
+                record[0].record()
+            _lib.check(lib.bhcp_status_reset(status, sh), "reset")
+            _lib.check(lib.bhcp_pint_ghat(sp, plans.ptr(g_dev), 1.0 / (divisor * n), ghat, sh), "ghat")
+            if record:
+                record[1].record()
+            _lib.check(lib.bhcp_pint_modes(sp, tp, ghat, 0, nx, W, nx, status, sh), "modes")
+            if record:
+                record[2].record()
+            for a in range(w.dim):
+                src = W if a == 0 else plans.ptr(y)
+                _lib.check(lib.bhcp_sine_axis(sp, src, plans.ptr(y), 0, n, a, sh), "axis")
+                if record:
+                    record[3 + a].record()
+
+        launches_per_step = 1 + (w.dim + 1) + 1 + w.dim  # reset, ghat passes + scale, modes, level passes
+        sampler = ClockSampler(local)
+        sampler.start()
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        plan.check_status()
+        nph = 3 + w.dim
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nph)] for _ in range(args.steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0.record()
+        for k in range(args.steps):
+            step(evs[k])
+        t1.record()
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        plan.check_status()
+        total_ms = t0.elapsed_time(t1)
+        phase_ms = np.zeros(nph - 1)
+        for k in range(args.steps):
+            for p in range(nph - 1):
+                phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
+        phase_ms /= args.steps
+        names = ["ghat (DST of g)", "k_modes (shifts + time FFT + Gamma^-1 + Re)"] + \
+                [f"k_dst {'rows' if a == 0 else 'cols'} axis -{a + 1}" for a in range(w.dim)]
+        dom = int(np.argmax(phase_ms))
+        # algorithmic bytes per launch of each kernel
+        dof = w.dof
+        alg_bytes = [16.0 * nx, 8.0 * dof + 8.0 * nx] + [16.0 * dof] * w.dim
+        hbm, peak_kind = peaks()
+        achieved = alg_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
+        traffic = None
+        tfile = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
+        if tfile.exists():
+            traffic = json.loads(tfile.read_text()).get(names[dom].split()[0] if dom != 1 else "k_modes")
+        ms_per_step = total_ms / args.steps
+        value = dof / (ms_per_step * 1e-3)
+
+        # ---- e2e through the C-ABI with host buffers
+        g_host = torch.from_numpy(w.g_delta).pin_memory()
+        y_host = torch.empty((n, nx), dtype=torch.float64).pin_memory()
+        g_e2e = torch.empty_like(g_dev)
+        wsb = plan.ws_bytes
+
+        def e2e_step():
+            g_e2e.copy_(g_host, non_blocking=True)
+            _lib.check(lib.bhcp_pint_solve(sp, tp, plans.ptr(g_e2e), divisor, plans.ptr(y), ctypes.c_void_p(wsp),
+                                           wsb, sh), "solve")
+            y_host.copy_(y, non_blocking=True)
+
+        e2e_steps = max(3, min(args.steps, 10))
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(e2e_steps):
+            e2e_step()
+        a1.record()
+        torch.cuda.synchronize()
+        plan.check_status()
+        e2e_ms = a0.elapsed_time(a1) / e2e_steps
+        e2e_value = dof / (e2e_ms * 1e-3)
+
+        # ---- unfused literal 3-step dataflow for comparison (same kernels family)
+        yu, wsu = plan.solve_unfused_device(g_dev, divisor)
+        torch.cuda.synchronize()
+        u0 = torch.cuda.Event(enable_timing=True)
+        u1 = torch.cuda.Event(enable_timing=True)
+        u0.record()
+        for _ in range(3):
+            plan.solve_unfused_device(g_dev, divisor, out=yu)
+        u1.record()
+        torch.cuda.synchronize()
+        unfused_ms = u0.elapsed_time(u1) / 3
+        del yu, wsu
+
+        cpu = None
+        if not args.no_cpu_baseline:
+            dof_s, secs = cpu_sample(w, kind, alpha, args.cpu_fraction, None)
+            cpu = {"value": dof_s / secs, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"{args.config}, fraction {args.cpu_fraction} of every per-unit op of the reference "
+                             f"3-step solve ({secs:.1f} s, single thread = reference default workers=None)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config construction)",
+            "config": {"workload": f"{args.config}: 2D pint-mqbvm, 511^2 interior x 513 levels, alpha=1e-2",
+                       "dof_per_solve": dof, "l2": "working set (W + y = 2.1 GB) larger than L2; no flush"},
+            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_kind,
+                         "alg_bytes_per_launch": alg_bytes[dom]},
+            "phases_ms": {nm: float(t) for nm, t in zip(names, phase_ms)},
+            "pipeline_72B_per_dof": {"achieved_GBps": 72.0 * dof / (ms_per_step * 1e-3) / 1e9,
+                                     "frac": 72.0 * dof / (ms_per_step * 1e-3) / 1e9 / hbm,
+                                     "note": "SURVEY 8(d) 3-step algorithmic bytes; >1 means fused dataflow"},
+            "unfused_3step_ms": unfused_ms,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * nx, "d2h_bytes_per_step": 8 * n * nx,
+                    "ms_per_step": e2e_ms},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    # ---------------- N > 1: slab-decomposed solve
+    line = D.bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, METRIC, UNIT)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

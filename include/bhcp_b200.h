@@ -99,6 +99,12 @@ void bhcp_time_plan_destroy(bhcp_time_plan* plan);
 int bhcp_sine_transform(const bhcp_space_plan* sp, const void* in, void* out,
                         int is_complex, int64_t batch, void* stream);
 
+/* One axis pass of the orthonormal DST-I over `batch` level-major fields:
+ * axis 0 = the contiguous axis (-1), 1 = axis -2, 2 = axis -3. in/out may
+ * alias. bhcp_sine_transform is the sequence of passes 0..dim-1. */
+int bhcp_sine_axis(const bhcp_space_plan* sp, const void* in, void* out,
+                   int is_complex, int64_t batch, int axis, void* stream);
+
 /* Step (b): for each level j < batch solve (shift_j I - lap) x = rhs_j with
  * the spectral method (DST, divide by shift_j + mu_k, DST). in/out are
  * level-major complex128 (batch, n_space) and may alias; shifts_dev holds

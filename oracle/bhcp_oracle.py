@@ -302,3 +302,61 @@ def rel_l2(a, b) -> float:
 def parity_tolerance(n_levels: int, omega: float) -> float:
     """max(1e-10, 10 * cond(Gamma) * DBL_EPSILON)."""
     return max(1e-10, 10.0 * condition_gamma(n_levels, omega) * np.finfo(float).eps)
+
+
+# --------------------------------------------------------------------------
+# bounded CPU-baseline sample (bench.py cpu_baseline / --impl reference)
+# --------------------------------------------------------------------------
+
+def solve_pint_sample(kind, alpha, dim, length, num_cells, horizon, num_steps, data,
+                      fraction: float, workers=None):
+    """Time the reference 3-step solve (pint.py:89-99) on a bounded sample.
+
+    The sample performs a fraction ``f`` of every per-unit operation of the
+    full solve: step (a) time transforms of ceil(f*N_x) spatial rows
+    (circulant.py:106), step (b) shifted solves of ceil(f*N_t) columns
+    (pint.py:59-65, with a ThreadPoolExecutor of ``workers`` threads exactly
+    like the reference's optional pool), step (c) back transforms + residue of
+    ceil(f*N_x) rows (circulant.py:115, 182-190). Returns
+    (dof_equivalent, seconds) with dof_equivalent = f * N_t * N_x.
+    """
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+
+    tau = tau_of(horizon, num_steps)
+    n = num_steps + 1
+    gamma, eig = diagonalize(n, omega_of(kind, alpha, tau))
+    shifts = eig / tau
+    data = np.asarray(data, dtype=float)
+    nx = data.shape[0]
+    m = num_cells - 1
+    mu = mode_eigenvalues(dim, length, num_cells)
+    rows = max(1, int(np.ceil(fraction * nx)))
+    cols = max(1, int(np.ceil(fraction * n)))
+    start = time.perf_counter()
+    # (a) rhs block rows (methods.py:158-162) and their time transform
+    rhs_rows = np.zeros((rows, n))
+    rhs_rows[:, 0] = data[:rows] / condition_divisor(kind, alpha, tau)
+    s1_rows = to_eigenspace(rhs_rows, gamma)
+    # (b) full spatial columns; column j of S1 is rhs_0 / sqrt(n) (the values
+    # do not change the work; they are the exact step-(a) output)
+    col = (data / condition_divisor(kind, alpha, tau) / np.sqrt(n)).astype(np.complex128)
+
+    def solve_column(j):
+        coeffs = sine_transform(col, dim, m)
+        return sine_transform(coeffs / (shifts[j] + mu), dim, m)
+
+    out = np.empty((nx, cols), dtype=np.complex128)
+    if workers is None:
+        for j in range(cols):
+            out[:, j] = solve_column(j)
+    else:
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            for j, c in enumerate(pool.map(solve_column, range(cols))):
+                out[:, j] = c
+    # (c) back transform of sample rows + residue norms
+    back = apply_basis(s1_rows, gamma)
+    _ = np.linalg.norm(back), np.linalg.norm(back.imag)
+    _ = np.ascontiguousarray(back.real)
+    elapsed = time.perf_counter() - start
+    return fraction * n * nx, elapsed

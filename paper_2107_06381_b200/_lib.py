@@ -54,6 +54,7 @@ SIGNATURES = {
     "bhcp_time_plan_create": (_int, [_int, _int, _dp, _dp, _dp, ctypes.POINTER(_vp)]),
     "bhcp_time_plan_destroy": (None, [_vp]),
     "bhcp_sine_transform": (_int, [_vp, _vp, _vp, _int, _i64, _vp]),
+    "bhcp_sine_axis": (_int, [_vp, _vp, _vp, _int, _i64, _int, _vp]),
     "bhcp_step_b": (_int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "bhcp_to_eigenspace": (_int, [_vp, _vp, _int, _i64, _i64, _i64, _vp, _i64, _i64, _vp]),
     "bhcp_from_eigenspace": (_int, [_vp, _vp, _i64, _i64, _i64, _vp, _int, _i64, _i64, _vp, _vp]),

@@ -911,6 +911,20 @@ int bhcp_sine_transform(const bhcp_space_plan* sp, const void* in, void* out, in
   return sine_passes(sp, (const double*)in, (double*)out, is_complex ? 1 : 0, batch, as_stream(stream));
 }
 
+int bhcp_sine_axis(const bhcp_space_plan* sp, const void* in, void* out, int is_complex, int64_t batch, int axis,
+                   void* stream) {
+  if (!sp || !in || !out || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (axis < 0 || axis >= sp->dim) return fail(BHCP_ERR_INVALID, "axis out of range");
+  DeviceGuard g(sp->device);
+  const int d = sp->dim, m = sp->m;
+  const int cplx = is_complex ? 1 : 0;
+  if (axis == 0)
+    return launch_rows(sp, (const double*)in, (double*)out, cplx, batch * ipow(m, d - 1), 0, nullptr, nullptr,
+                       as_stream(stream));
+  return launch_cols(sp, (const double*)in, (double*)out, cplx, ipow(m, axis), batch * ipow(m, d - 1 - axis), axis,
+                     0, nullptr, nullptr, as_stream(stream));
+}
+
 int bhcp_step_b(const bhcp_space_plan* sp, const void* in, void* out, const double* shifts_dev, int64_t batch,
                 void* status_dev, void* stream) {
   if (!sp || !in || !out || !shifts_dev || !status_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
