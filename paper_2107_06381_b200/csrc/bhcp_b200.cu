@@ -16,6 +16,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
 #include <string>
@@ -88,6 +89,10 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
   const double inv = 1.0 / den2;
   return make_double2((x.x * dr + x.y * di) * inv, (x.y * dr - x.x * di) * inv);
 }
+
+}  // namespace bhcp
+#include "fast_kernels.cuh"
+namespace bhcp {
 
 template <int V> struct VT;
 template <> struct VT<V256> { static constexpr int T = 256, CAP = 16, MINB = 2; };
@@ -622,7 +627,45 @@ void set_all_attributes() {
   allow_smem(k_modes<VV>);
   BHCP_FOR_VARIANTS(BHCP_ATTR)
 #undef BHCP_ATTR
+#define BHCP_FATTR(LL)                                  \
+  allow_smem(fastk::k_dst_rows_fast<LL, 0>);            \
+  allow_smem(fastk::k_dst_rows_fast<LL, 1>);            \
+  allow_smem(fastk::k_dst_cols_fast<LL, 0>);            \
+  allow_smem(fastk::k_dst_cols_fast<LL, 1>);
+  BHCP_FATTR(512) BHCP_FATTR(1024) BHCP_FATTR(2048) BHCP_FATTR(8192)
+#undef BHCP_FATTR
+  allow_smem(fastk::k_modes_fast<513>);
 }
+
+// --- specialised fast paths (fast_kernels.cuh) ---------------------------------
+template <int L>
+void rows_fast(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
+               cudaStream_t s) {
+  using namespace fastk;
+  FastDstArgs a{};
+  a.in = in; a.out = out; a.nlines = nlines; a.tw = sp->dst.d.tw;
+  a.f = sqrt(2.0 / (L / 2)) * 0.5;
+  const long long seqs = cplx ? nlines : (nlines + 1) / 2;
+  const long long grid = (seqs + RowsShape<L>::S - 1) / RowsShape<L>::S;
+  if (cplx) k_dst_rows_fast<L, 1><<<(unsigned)grid, RowsShape<L>::T, rows_smem<L>(), s>>>(a);
+  else k_dst_rows_fast<L, 0><<<(unsigned)grid, RowsShape<L>::T, rows_smem<L>(), s>>>(a);
+}
+
+template <int L>
+void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long ni, long long no,
+               cudaStream_t s) {
+  using namespace fastk;
+  FastDstArgs a{};
+  a.in = in; a.out = out; a.ni = ni; a.no = no; a.es = ni; a.os = (long long)sp->m * ni; a.tw = sp->dst.d.tw;
+  a.f = sqrt(2.0 / (L / 2)) * 0.5;
+  const int lines_per_cta = cplx ? ColsShape<L>::S : 2 * ColsShape<L>::S;
+  const long long grid = ((ni + lines_per_cta - 1) / lines_per_cta) * no;
+  if (cplx) k_dst_cols_fast<L, 1><<<(unsigned)grid, ColsShape<L>::T, cols_smem<L>(), s>>>(a);
+  else k_dst_cols_fast<L, 0><<<(unsigned)grid, ColsShape<L>::T, cols_smem<L>(), s>>>(a);
+}
+
+bool fast_dst_length(int L) { return L == 512 || L == 1024 || L == 2048 || L == 8192; }
+bool g_disable_fast = false;
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -632,6 +675,16 @@ size_t smem_bytes(const FftPlanHost& p, int nseq) { return size_t(nseq) * p.ld *
 int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
                 int epi, const double2* shifts, StatusDev* st, cudaStream_t s) {
   const FftPlanHost& P = sp->dst;
+  if (!epi && !g_disable_fast && fast_dst_length(2 * (sp->m + 1)) && nlines > 0) {
+    switch (2 * (sp->m + 1)) {
+      case 512: rows_fast<512>(sp, in, out, cplx, nlines, s); break;
+      case 1024: rows_fast<1024>(sp, in, out, cplx, nlines, s); break;
+      case 2048: rows_fast<2048>(sp, in, out, cplx, nlines, s); break;
+      case 8192: rows_fast<8192>(sp, in, out, cplx, nlines, s); break;
+    }
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_rows_fast launch");
+    return BHCP_OK;
+  }
   const int nseq_max = P.max_seqs(kSmemBudget);
   if (nseq_max < 1) return fail(BHCP_ERR_INVALID, "DST length does not fit the FFT engine");
   const long long seqs = cplx ? nlines : (nlines + 1) / 2;
@@ -659,6 +712,16 @@ int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cp
 int launch_cols(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long ni,
                 long long no, int depth, int epi, const double2* shifts, StatusDev* st, cudaStream_t s) {
   const FftPlanHost& P = sp->dst;
+  if (!epi && !g_disable_fast && fast_dst_length(2 * (sp->m + 1)) && ni > 0 && no > 0) {
+    switch (2 * (sp->m + 1)) {
+      case 512: cols_fast<512>(sp, in, out, cplx, ni, no, s); break;
+      case 1024: cols_fast<1024>(sp, in, out, cplx, ni, no, s); break;
+      case 2048: cols_fast<2048>(sp, in, out, cplx, ni, no, s); break;
+      case 8192: cols_fast<8192>(sp, in, out, cplx, ni, no, s); break;
+    }
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_cols_fast launch");
+    return BHCP_OK;
+  }
   const int nseq_max = P.max_seqs(kSmemBudget);
   if (nseq_max < 1) return fail(BHCP_ERR_INVALID, "DST length does not fit the FFT engine");
   const long long lines_needed = ni;
@@ -765,6 +828,17 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
+  if (!g_disable_fast && tp->n == 513) {
+    using namespace fastk;
+    FastModesArgs f{};
+    f.shifts = tp->tables + 2 * tp->n; f.gaminv = tp->tables + tp->n; f.mu1 = sp->mu1_dev; f.ghat = ghat;
+    f.cscale = cscale; f.k_begin = k_begin; f.k_count = kc; f.W = W; f.w_ld = w_ld; f.m = sp->m; f.dim = sp->dim;
+    f.tw = P.d.tw; f.st = st;
+    const long long grid = (kc + ModesPlan<513>::S - 1) / ModesPlan<513>::S;
+    k_modes_fast<513><<<(unsigned)grid, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_fast launch");
+    return BHCP_OK;
+  }
   int nseq = P.max_seqs(kSmemBudget);
   if (nseq < 1) return fail(BHCP_ERR_INVALID, "time length does not fit the FFT engine");
   if (nseq > 64) nseq = 64;
@@ -808,6 +882,10 @@ bool ensure_device_constants(int device, std::string* err) {
     return false;
   }
   cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  {
+    const char* e = getenv("BHCP_DISABLE_FAST");
+    g_disable_fast = (e && e[0] == '1');
+  }
   set_all_attributes();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
