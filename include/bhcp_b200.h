@@ -172,6 +172,15 @@ int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
 int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
                      int64_t batch, void* stream);
 
+/* Level-slab inverse DST of the slab-decomposed solve (dim >= 2). in_dev is
+ * the all-to-all receive buffer holding, for every mode slab, a block of W
+ * rows; line (t, k1, r) of level t (r enumerating the axes after k1) starts
+ * at koff[k1] + t * kstride[k1] + r * m (element units; device int64 tables
+ * of length m). out_dev receives `batch` contiguous level-major fields. */
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev,
+                             const int64_t* koff_dev, const int64_t* kstride_dev,
+                             double* out_dev, int64_t batch, void* stream);
+
 /* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,
                    int elem_bytes, void* stream);

@@ -360,3 +360,29 @@ def solve_pint_sample(kind, alpha, dim, length, num_cells, horizon, num_steps, d
     _ = np.ascontiguousarray(back.real)
     elapsed = time.perf_counter() - start
     return fraction * n * nx, elapsed
+
+
+# --------------------------------------------------------------------------
+# numpy restatement of the device's fused halves (tests of the multi-rank
+# orchestration on CPU; see paper_2107_06381_b200/pint.py docstring)
+# --------------------------------------------------------------------------
+
+def fused_pass_a(kind, alpha, dim, length, num_cells, horizon, num_steps, data, k_begin, k_end):
+    """W[t, k] = ghat_k / (divisor n) * Re(gamma_inv_t * FFT_j(1 / (s_j + mu_k)))
+    for modes [k_begin, k_end); returns (W (n, S), sum Re^2, sum Im^2)."""
+    tau = tau_of(horizon, num_steps)
+    n = num_steps + 1
+    gamma, eig = diagonalize(n, omega_of(kind, alpha, tau))
+    shifts = eig / tau
+    m = num_cells - 1
+    mu = mode_eigenvalues(dim, length, num_cells)[k_begin:k_end]
+    ghat = sine_transform(np.asarray(data, float), dim, m)[k_begin:k_end]
+    c = ghat / (condition_divisor(kind, alpha, tau) * n)
+    X = np.fft.fft(1.0 / (shifts[:, None] + mu[None, :]), axis=0)
+    Z = X * (1.0 / gamma)[:, None] * c[None, :]
+    return np.ascontiguousarray(Z.real), float(np.sum(Z.real**2)), float(np.sum(Z.imag**2))
+
+
+def fused_pass_b(W_full_levels, dim, m):
+    """Inverse DST of level-major real fields (L, m**dim)."""
+    return sine_transform(W_full_levels, dim, m)

@@ -288,7 +288,21 @@ struct DstArgs {
   const double* mu1;     // EPI 1
   int axis_depth;        // cols kernel: 1 = axis -2, 2 = axis -3
   StatusDev* st;
+  // rows kernel, blocked input (slab all-to-all buffer): line (t, k1, r) at
+  // koff[k1] + t * kstride[k1] + r * m; null koff = contiguous lines
+  const long long* koff;
+  const long long* kstride;
+  long long lines_per_level, inner_div;
 };
+
+__device__ __forceinline__ long long line_base(const DstArgs& a, long long l) {
+  if (!a.koff) return l * a.m;
+  const long long t = l / a.lines_per_level;
+  const long long rem = l - t * a.lines_per_level;
+  const long long k1 = rem / a.inner_div;
+  const long long r2 = rem - k1 * a.inner_div;
+  return __ldg(a.koff + k1) + t * __ldg(a.kstride + k1) + r2 * a.m;
+}
 
 // k-th DST coefficient (1-based k) of sequence seq from the FFT buffer.
 __device__ __forceinline__ double2 dst_coef(const DstArgs& a, const double2* buf, int seq, int k) {
@@ -312,8 +326,8 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_dst_rows(DstArgs a) {
       if (s < a.nlines) x = ld2(a.in + 2 * (s * m + e));
     } else {
       const long long l0 = 2 * s, l1 = 2 * s + 1;
-      if (l0 < a.nlines) x.x = a.in[l0 * m + e];
-      if (l1 < a.nlines) x.y = a.in[l1 * m + e];
+      if (l0 < a.nlines) x.x = a.in[line_base(a, l0) + e];
+      if (l1 < a.nlines) x.y = a.in[line_base(a, l1) + e];
     }
     dst_put(a.p, smem, a.ld, q, m, e, x);
   }
@@ -638,12 +652,14 @@ void set_all_attributes() {
 }
 
 // --- specialised fast paths (fast_kernels.cuh) ---------------------------------
-template <int L>
+struct Blocked;
+template <int L, class B>
 void rows_fast(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
-               cudaStream_t s) {
+               cudaStream_t s, const B& blk) {
   using namespace fastk;
   FastDstArgs a{};
-  a.in = in; a.out = out; a.nlines = nlines; a.tw = sp->dst.d.tw;
+  a.in = in; a.out = out; a.nlines = nlines; a.tw = sp->dst.d.tw; a.m = sp->m;
+  a.koff = blk.koff; a.kstride = blk.kstride; a.lines_per_level = blk.lines_per_level; a.inner_div = blk.inner_div;
   a.f = sqrt(2.0 / (L / 2)) * 0.5;
   const long long seqs = cplx ? nlines : (nlines + 1) / 2;
   const long long grid = (seqs + RowsShape<L>::S - 1) / RowsShape<L>::S;
@@ -672,15 +688,21 @@ cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 size_t smem_bytes(const FftPlanHost& p, int nseq) { return size_t(nseq) * p.ld * sizeof(double2); }
 
 // --- DST pass launchers --------------------------------------------------------
+struct Blocked {
+  const long long* koff = nullptr;
+  const long long* kstride = nullptr;
+  long long lines_per_level = 1, inner_div = 1;
+};
+
 int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
-                int epi, const double2* shifts, StatusDev* st, cudaStream_t s) {
+                int epi, const double2* shifts, StatusDev* st, cudaStream_t s, const Blocked& blk = Blocked()) {
   const FftPlanHost& P = sp->dst;
   if (!epi && !g_disable_fast && fast_dst_length(2 * (sp->m + 1)) && nlines > 0) {
     switch (2 * (sp->m + 1)) {
-      case 512: rows_fast<512>(sp, in, out, cplx, nlines, s); break;
-      case 1024: rows_fast<1024>(sp, in, out, cplx, nlines, s); break;
-      case 2048: rows_fast<2048>(sp, in, out, cplx, nlines, s); break;
-      case 8192: rows_fast<8192>(sp, in, out, cplx, nlines, s); break;
+      case 512: rows_fast<512>(sp, in, out, cplx, nlines, s, blk); break;
+      case 1024: rows_fast<1024>(sp, in, out, cplx, nlines, s, blk); break;
+      case 2048: rows_fast<2048>(sp, in, out, cplx, nlines, s, blk); break;
+      case 8192: rows_fast<8192>(sp, in, out, cplx, nlines, s, blk); break;
     }
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_rows_fast launch");
     return BHCP_OK;
@@ -695,6 +717,7 @@ int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cp
   a.in = in; a.out = out; a.nlines = nlines;
   a.f = sqrt(2.0 / (sp->m + 1)) * 0.5;
   a.shifts = shifts; a.mu1 = sp->mu1_dev; a.st = st;
+  a.koff = blk.koff; a.kstride = blk.kstride; a.lines_per_level = blk.lines_per_level; a.inner_div = blk.inner_div;
   const long long grid = (seqs + nseq - 1) / nseq;
   const size_t sm = smem_bytes(P, nseq);
 #define BHCP_ROWS(VV)                                                                  \
@@ -1084,6 +1107,28 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, sp->nx, st, s);
   if (rc) return rc;
   return sine_passes(sp, W, y_dev, 0, tp->n, s);
+}
+
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev,
+                             const int64_t* kstride_dev, double* out_dev, int64_t batch, void* stream) {
+  if (!sp || !in_dev || !koff_dev || !kstride_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  const int d = sp->dim, m = sp->m;
+  Blocked blk;
+  blk.koff = (const long long*)koff_dev;
+  blk.kstride = (const long long*)kstride_dev;
+  blk.lines_per_level = ipow(m, d - 1);
+  blk.inner_div = ipow(m, d - 2);
+  int rc = launch_rows(sp, in_dev, out_dev, 0, batch * ipow(m, d - 1), 0, nullptr, nullptr, s, blk);
+  if (rc) return rc;
+  for (int depth = 1; depth < d; ++depth) {
+    rc = launch_cols(sp, out_dev, out_dev, 0, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0, nullptr,
+                     nullptr, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
 }
 
 size_t bhcp_pint_unfused_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {

@@ -44,13 +44,28 @@ struct FastDstArgs {
   long long ni, no, es, os;  // cols geometry
   const double2* tw;
   double f;          // sqrt(2/N)/2
+  int m;
+  // rows, blocked input (see DstArgs in bhcp_b200.cu); null koff = contiguous
+  const long long* koff;
+  const long long* kstride;
+  long long lines_per_level, inner_div;
 };
+
+__device__ __forceinline__ long long fast_line_base(const FastDstArgs& a, long long l) {
+  if (!a.koff) return l * a.m;
+  const long long t = l / a.lines_per_level;
+  const long long rem = l - t * a.lines_per_level;
+  const long long k1 = rem / a.inner_div;
+  const long long r2 = rem - k1 * a.inner_div;
+  return __ldg(a.koff + k1) + t * __ldg(a.kstride + k1) + r2 * a.m;
+}
 
 // ---------------------------------------------------------------- rows
 template <int L, int CPLX>
 struct RowsGen {
   const double* in;
   long long s0, nlines;
+  const long long* base;  // shared: start of each line of the CTA (2 per sequence)
   __device__ __forceinline__ double2 operator()(int q, int idx) const {
     constexpr int N = L / 2, m = N - 1;
     if (idx == 0 || idx == N) return make_double2(0.0, 0.0);
@@ -62,8 +77,8 @@ struct RowsGen {
       if (s < nlines) x = __ldg(reinterpret_cast<const double2*>(in) + s * m + e);
     } else {
       const long long l0 = 2 * s;
-      if (l0 < nlines) x.x = __ldg(in + l0 * m + e);
-      if (l0 + 1 < nlines) x.y = __ldg(in + (l0 + 1) * m + e);
+      if (l0 < nlines) x.x = __ldg(in + base[2 * q] + e);
+      if (l0 + 1 < nlines) x.y = __ldg(in + base[2 * q + 1] + e);
     }
     return neg ? make_double2(-x.x, -x.y) : x;
   }
@@ -95,8 +110,14 @@ __global__ void __launch_bounds__(RowsShape<L>::T) k_dst_rows_fast(FastDstArgs a
   constexpr int S = RowsShape<L>::S, T = RowsShape<L>::T;
   using Lay = SeqMajorPad<L, DstPlan<L>::R1>;
   extern __shared__ double2 smem[];
+  __shared__ long long s_base[2 * S];
   const long long s0 = (long long)blockIdx.x * S;
-  RowsGen<L, CPLX> gen{a.in, s0, a.nlines};
+  if (!CPLX && threadIdx.x < 2 * S) {
+    const long long l = 2 * s0 + threadIdx.x;
+    s_base[threadIdx.x] = l < a.nlines ? fast_line_base(a, l) : 0;
+  }
+  __syncthreads();
+  RowsGen<L, CPLX> gen{a.in, s0, a.nlines, s_base};
   RowsSink<L, CPLX> sink{a.out, s0, a.nlines, a.f};
   DstPlan<L>::template F<S, T, Lay>::run(smem, a.tw, gen, sink);
 }

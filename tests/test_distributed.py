@@ -1,0 +1,166 @@
+"""Slab-decomposed multi-rank orchestration (distributed.py).
+
+CPU: world_size-2 gloo process group running the real orchestration
+(partitions, all-to-all split sizes, blocked receive tables, status
+reductions) with a numpy restatement of the two device passes.
+GPU: the same orchestration emulated in one process on one GPU (ranks run
+sequentially, the all-to-all is a device concatenation), which exercises the
+device kernels on the blocked layout; results must be bit-identical to the
+single-GPU solve.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from oracle import bhcp_oracle as O
+from paper_2107_06381_b200 import distributed as D
+from paper_2107_06381_b200 import workloads
+
+
+def test_partition_balanced_and_uneven():
+    assert D.partition(10, 4) == [(0, 3), (3, 6), (6, 8), (8, 10)]
+    assert D.partition(3, 8)[-1] == (3, 3)
+    for total, parts in [(511, 2), (511, 8), (513, 8), (1023, 8), (255, 3)]:
+        p = D.partition(total, parts)
+        sizes = [b - a for a, b in p]
+        assert sum(sizes) == total and max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("dim,m,n,world", [(2, 7, 9, 2), (2, 5, 6, 3), (3, 4, 5, 2), (2, 3, 4, 4)])
+def test_layout_tables_address_every_line_once(dim, m, n, world):
+    L = D.SlabLayout(dim, m, n, world)
+    for r in range(world):
+        koff, kstride = L.block_tables(r)
+        total = sum(L.recv_splits(r))
+        seen = np.zeros(total, dtype=int)
+        for t in range(L.levels(r)):
+            for k1 in range(m):
+                for r2 in range(m ** (dim - 2)):
+                    start = koff[k1] + t * kstride[k1] + r2 * m
+                    seen[start:start + m] += 1
+        assert (seen == 1).all()
+    assert sum(sum(L.send_splits(r)) for r in range(world)) == n * m**dim
+
+
+def test_layout_rejects_1d():
+    with pytest.raises(ValueError):
+        D.SlabLayout(1, 255, 257, 2)
+
+
+class NumpyOps:
+    """numpy restatement of the device passes (test-only injection)."""
+
+    def __init__(self, kind, alpha, w):
+        self.args = (kind, alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps, w.g_delta)
+        self.dim, self.m = w.dim, w.num_cells - 1
+        self.sums = (0.0, 0.0)
+
+    def modes(self, kb, ke):
+        import torch
+        W, sre, sim = O.fused_pass_a(*self.args, kb, ke)
+        self.sums = (sre, sim)
+        return torch.from_numpy(W)
+
+    def tables(self, layout, rank):
+        return layout.block_tables(rank)
+
+    def levels_blocked(self, recv, koff, kstride, L):
+        import torch
+        recv = recv.numpy()
+        m, d = self.m, self.dim
+        F = np.zeros((L, m**d))
+        for t in range(L):
+            for k1 in range(m):
+                for r2 in range(m ** (d - 2)):
+                    s = koff[k1] + t * kstride[k1] + r2 * m
+                    base = k1 * m ** (d - 1) + r2 * m
+                    F[t, base:base + m] = recv[s:s + m]
+        return torch.from_numpy(O.fused_pass_b(F, d, m))
+
+
+def _worker(rank, world, port, kind, dim, cells, steps, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = workloads.make_small(dim, cells, steps, seed=11)
+    layout = D.SlabLayout(dim, cells - 1, steps + 1, world)
+    ops = NumpyOps(kind, 1e-2, w)
+    comm = D.TorchComm(torch.device("cpu"))
+    y, (c, d) = D.sharded_solve(ops, comm, layout, rank)
+    sre, sim, bad = D.reduce_status(comm, ops.sums[0], ops.sums[1], -1)
+    q.put((rank, c, d, y.numpy(), sre, sim, bad))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,dim,cells,steps", [("pint-mqbvm", 2, 8, 8), ("pint-qbvm", 2, 9, 6),
+                                                   ("pint-mqbvm", 3, 5, 5)])
+def test_gloo_world2_matches_oracle(kind, dim, cells, steps):
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, dim, cells, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    outs.sort(key=lambda o: o[0])
+    y = np.concatenate([o[3] for o in outs], axis=0)
+    assert outs[0][1] == 0 and outs[-1][2] == steps + 1
+    w = workloads.make_small(dim, cells, steps, seed=11)
+    ref = O.spectral_oracle(kind, 1e-2, dim, w.length, cells, w.horizon, steps, w.g_delta)
+    assert np.linalg.norm(y - ref) / np.linalg.norm(ref) <= 1e-11
+    # both ranks agree on the reduced residue accumulators and no singular column
+    assert outs[0][4] == outs[1][4] and outs[0][5] == outs[1][5]
+    assert outs[0][6] == -1 and outs[1][6] == -1
+    assert np.sqrt(outs[0][5]) <= 1e-8 * np.sqrt(outs[0][4] + outs[0][5])
+
+
+# ---------------------------------------------------------------- GPU emulation
+
+def emulate(system, world):
+    import torch
+
+    import paper_2107_06381_b200 as B
+    from paper_2107_06381_b200 import plans
+
+    grid, tg = system.grid, system.timegrid
+    layout = D.SlabLayout(grid.dim, grid.num_cells - 1, tg.n_levels, world)
+    plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
+    ops = D.DeviceOps(plan, plans.to_device(system.data, torch.float64),
+                      system.method.condition_divisor(tg.tau))
+    Ws = [ops.modes(*layout.mode_range(r)).clone() for r in range(world)]
+    ys = []
+    for q in range(world):
+        c, d = layout.lev[q]
+        recv = torch.cat([Wr[c:d].reshape(-1) for Wr in Ws])
+        koff, kstride = ops.tables(layout, q)
+        ys.append(ops.levels_blocked(recv, koff, kstride, d - c).clone())
+    return torch.cat(ys).cpu().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,cells,steps,world", [(2, 16, 12, 2), (2, 20, 9, 3), (3, 8, 6, 2), (3, 9, 7, 4),
+                                                   (2, 512, 512, 8)])
+def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
+    import paper_2107_06381_b200 as B
+
+    w = workloads.make_small(dim, cells, steps, seed=3) if cells < 512 else workloads.make("c2")
+    grid = B.build_grid(dim, w.length, cells)
+    tg = B.TimeGrid(w.horizon, steps)
+    system = B.assemble(B.MethodKind.PINT_MQBVM, 1e-2, grid, tg, w.g_delta)
+    single = B.solve_pint(system).trajectory
+    multi = emulate(system, world)
+    assert np.array_equal(single, multi)
