@@ -48,8 +48,8 @@ UNIT = "DOF/s"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=CONFIG_NAME)
     p.add_argument("--cpu-fraction", type=float, default=0.1,
@@ -213,18 +213,18 @@ def main():
             _lib.check(lib.bhcp_pint_ghat(sp, plans.ptr(g_dev), 1.0 / (divisor * n), ghat, sh), "ghat")
             if record:
                 record[1].record()
-            _lib.check(lib.bhcp_pint_modes(sp, tp, ghat, 0, nx, W, nx, status, sh), "modes")
+            _lib.check(lib.bhcp_pint_modes(sp, tp, ghat, 0, nx, W, 0, None, status, sh), "modes")
             if record:
                 record[2].record()
             for a in range(w.dim):
-                src = W if a == 0 else plans.ptr(y)
-                _lib.check(lib.bhcp_sine_axis(sp, src, plans.ptr(y), 0, n, a, sh), "axis")
+                _lib.check(lib.bhcp_pint_level_pass(sp, W, None, n, plans.ptr(y), n, a, sh), "level pass")
                 if record:
                     record[3 + a].record()
 
         launches_per_step = 1 + (w.dim + 1) + 1 + w.dim  # reset, ghat passes + scale, modes, level passes
         sampler = ClockSampler(local)
         sampler.start()
+        time.sleep(0.5)  # let nvidia-smi start sampling before the GPU is loaded
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
@@ -247,8 +247,8 @@ def main():
             for p in range(nph - 1):
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
-        names = ["ghat (DST of g)", "k_modes (shifts + time FFT + Gamma^-1 + Re)"] + \
-                [f"k_dst {'rows' if a == 0 else 'cols'} axis -{a + 1}" for a in range(w.dim)]
+        names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"] + \
+                [f"k_dst_gather pass {a} (axis -{a + 1})" for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof

@@ -156,30 +156,42 @@ int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
                             const double* g_dev, double divisor, double* y_dev,
                             void* ws, size_t ws_bytes, void* stream);
 
-/* Slab halves of the fused solve for the multi-GPU driver.
+/* The two halves of the fused solve (also used by the slab-decomposed
+ * multi-GPU driver).
  * bhcp_pint_ghat: ghat = DST(g) * scale (n_space float64), scale = 1/(divisor*n).
  * bhcp_pint_modes: for spatial modes [k_begin, k_end) write
- *   W[t, k - k_begin] = ghat[k] * Re(gamma_inv_t * FFT_t(1/(s_j + mu_k)))
- *   into w_dev with row stride w_ld (elements), accumulating norms / singular
- *   column into status_dev.
- * bhcp_pint_levels: inverse DST of `batch` level-major float64 fields,
- *   in -> out (may alias). */
+ *   W(k, t) = ghat[k] * Re(gamma_inv_t * FFT_t(1/(s_j + mu_k)))
+ *   and accumulate the residue norms / first singular column into status_dev.
+ *   Layout of W (K = k_end - k_begin, k local):
+ *     nslabs == 0, dim 1:  level-major, W[t * K + k]
+ *     nslabs == 0, dim>=2: mode-major,  W[k * n + t]
+ *     nslabs >= 1:         mode-major per level slab s (bounds b, host array of
+ *                          nslabs+1 int64, b[0] = 0, b[nslabs] = n):
+ *                          W[K * b[s] + k * (b[s+1] - b[s]) + t - b[s]]
+ *                          (one contiguous all-to-all chunk per destination).
+ * bhcp_pint_level_pass: pass 0 = inverse DST along the last spatial axis from
+ *   W (native layout, or mode-major blocks whose mode (k1, 0..) starts at
+ *   koff_dev[k1] with level stride lin when koff_dev is not null) into the
+ *   level-major y (nlev, n_space); pass p >= 1 = inverse DST along axis
+ *   -(p+1) in place on y.
+ * bhcp_pint_levels: passes 0..dim-1 on the native layout (lin = batch).
+ * bhcp_pint_levels_blocked: passes 0..dim-1 on an all-to-all receive buffer
+ *   of mode-major blocks (dim >= 2); level0 = global index of the slab's first
+ *   level (keeps the level pairing of the FFT identical to the 1-GPU solve). */
 int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
                    double* ghat_dev, void* stream);
 int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
                     const double* ghat_dev, int64_t k_begin, int64_t k_end,
-                    double* w_dev, int64_t w_ld, void* status_dev, void* stream);
+                    double* w_dev, int nslabs, const int64_t* slab_bounds,
+                    void* status_dev, void* stream);
+int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev,
+                         const int64_t* koff_dev, int64_t lin, double* y_dev,
+                         int64_t nlev, int pass, void* stream);
 int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
                      int64_t batch, void* stream);
-
-/* Level-slab inverse DST of the slab-decomposed solve (dim >= 2). in_dev is
- * the all-to-all receive buffer holding, for every mode slab, a block of W
- * rows; line (t, k1, r) of level t (r enumerating the axes after k1) starts
- * at koff[k1] + t * kstride[k1] + r * m (element units; device int64 tables
- * of length m). out_dev receives `batch` contiguous level-major fields. */
 int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev,
-                             const int64_t* koff_dev, const int64_t* kstride_dev,
-                             double* out_dev, int64_t batch, void* stream);
+                             const int64_t* koff_dev, int64_t lin, double* out_dev,
+                             int64_t batch, int64_t level0, void* stream);
 
 /* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,

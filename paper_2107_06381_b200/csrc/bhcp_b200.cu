@@ -20,6 +20,8 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "../../include/bhcp_b200.h"
 #include "fft_engine.cuh"
@@ -92,6 +94,7 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 
 }  // namespace bhcp
 #include "fast_kernels.cuh"
+#include "gather_dst.cuh"
 namespace bhcp {
 
 template <int V> struct VT;
@@ -281,6 +284,8 @@ struct DstArgs {
   const double* in;
   double* out;
   long long nlines;      // rows kernel: number of lines (real or complex)
+  long long nseqs;       // rows kernel: number of FFT sequences
+  long long lpl;         // rows kernel, real data: lines per level (pairing, see fastk::pair_lines)
   long long ni, no;      // cols kernel: inner / outer line counts
   long long es, os;      // cols kernel: element / outer strides (elements)
   double f;              // sqrt(2/(m+1)) / 2
@@ -324,10 +329,11 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_dst_rows(DstArgs a) {
     double2 x = make_double2(0.0, 0.0);
     if (CPLX) {
       if (s < a.nlines) x = ld2(a.in + 2 * (s * m + e));
-    } else {
-      const long long l0 = 2 * s, l1 = 2 * s + 1;
-      if (l0 < a.nlines) x.x = a.in[line_base(a, l0) + e];
-      if (l1 < a.nlines) x.y = a.in[line_base(a, l1) + e];
+    } else if (s < a.nseqs) {
+      long long l0, l1;
+      fastk::pair_lines(s, a.nlines, a.lpl, l0, l1);
+      if (l0 >= 0) x.x = a.in[line_base(a, l0) + e];
+      if (l1 >= 0) x.y = a.in[line_base(a, l1) + e];
     }
     dst_put(a.p, smem, a.ld, q, m, e, x);
   }
@@ -367,10 +373,11 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_dst_rows(DstArgs a) {
     const double2 c = dst_coef(a, smem, q, e + 1);
     if (CPLX) {
       if (s < a.nlines) reinterpret_cast<double2*>(a.out)[s * m + e] = c;
-    } else {
-      const long long l0 = 2 * s, l1 = 2 * s + 1;
-      if (l0 < a.nlines) a.out[l0 * m + e] = c.x;
-      if (l1 < a.nlines) a.out[l1 * m + e] = c.y;
+    } else if (s < a.nseqs) {
+      long long l0, l1;
+      fastk::pair_lines(s, a.nlines, a.lpl, l0, l1);
+      if (l0 >= 0) a.out[l0 * m + e] = c.x;
+      if (l1 >= 0) a.out[l1 * m + e] = c.y;
     }
   }
 }
@@ -469,7 +476,7 @@ struct ModesArgs {
   double cscale;         // 1 / (divisor * n) applied to ghat
   long long k_begin, k_count;
   double* W;
-  long long w_ld;
+  fastk::WLayout wl;
   StatusDev* st;
 };
 
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_modes(ModesArgs a) {
     const double wr = c * Z.x, wi = c * Z.y;
     sre = fma(wr, wr, sre);
     sim = fma(wi, wi, sim);
-    a.W[(long long)t * a.w_ld + kl] = wr;
+    a.W[a.wl.addr(kl, t)] = wr;
   }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
@@ -578,6 +585,8 @@ struct bhcp_space_plan {
   long long nx;          // m^dim interior unknowns
   double* mu1_dev;       // m doubles
   FftPlanHost dst;       // FFT of length 2(m+1)
+  int2* tiles_dev;       // 2D: upper-triangle 4x4 mode tiles (a, b), a <= b
+  long long ntiles;
 };
 
 struct bhcp_time_plan {
@@ -648,21 +657,43 @@ void set_all_attributes() {
   allow_smem(fastk::k_dst_cols_fast<LL, 1>);
   BHCP_FATTR(512) BHCP_FATTR(1024) BHCP_FATTR(2048) BHCP_FATTR(8192)
 #undef BHCP_FATTR
-  allow_smem(fastk::k_modes_fast<513>);
+  allow_smem(gdst::k_dst_gather<512, 0>);
+  allow_smem(gdst::k_dst_gather<512, 1>);
+  allow_smem(gdst::k_dst_gather<1024, 0>);
+  allow_smem(gdst::k_dst_gather<1024, 1>);
+  allow_smem(gdst::k_dst_gather<2048, 0>);
+  allow_smem(gdst::k_dst_gather<2048, 1>);
+  allow_smem(gdst::k_dst_gather<8192, 0>);
+  allow_smem(gdst::k_dst_gather<8192, 1>);
+  allow_smem(fastk::k_modes_fast<513, false>);
+  allow_smem(fastk::k_modes_fast<513, true>);
 }
 
 // --- specialised fast paths (fast_kernels.cuh) ---------------------------------
+int g_num_sms = 148;
+
+// CTAs of `kernel` that fit on the device at once (persistent-grid size).
+template <typename K>
+long long resident_ctas(K kernel, int threads, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return (long long)per_sm * g_num_sms;
+}
 struct Blocked;
 template <int L, class B>
 void rows_fast(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
-               cudaStream_t s, const B& blk) {
+               cudaStream_t s, const B& blk, long long lpl) {
   using namespace fastk;
   FastDstArgs a{};
-  a.in = in; a.out = out; a.nlines = nlines; a.tw = sp->dst.d.tw; a.m = sp->m;
+  a.in = in; a.out = out; a.nlines = nlines; a.tw = sp->dst.d.tw; a.m = sp->m; a.lpl = lpl;
   a.koff = blk.koff; a.kstride = blk.kstride; a.lines_per_level = blk.lines_per_level; a.inner_div = blk.inner_div;
   a.f = sqrt(2.0 / (L / 2)) * 0.5;
-  const long long seqs = cplx ? nlines : (nlines + 1) / 2;
-  const long long grid = (seqs + RowsShape<L>::S - 1) / RowsShape<L>::S;
+  const long long seqs = cplx ? nlines : real_row_seqs(nlines, lpl);
+  a.nseqs = seqs;
+  long long grid = (seqs + RowsShape<L>::S - 1) / RowsShape<L>::S;
+  grid = std::min<long long>(grid, cplx ? resident_ctas(k_dst_rows_fast<L, 1>, RowsShape<L>::T, rows_smem<L>())
+                                        : resident_ctas(k_dst_rows_fast<L, 0>, RowsShape<L>::T, rows_smem<L>()));
   if (cplx) k_dst_rows_fast<L, 1><<<(unsigned)grid, RowsShape<L>::T, rows_smem<L>(), s>>>(a);
   else k_dst_rows_fast<L, 0><<<(unsigned)grid, RowsShape<L>::T, rows_smem<L>(), s>>>(a);
 }
@@ -675,7 +706,9 @@ void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cpl
   a.in = in; a.out = out; a.ni = ni; a.no = no; a.es = ni; a.os = (long long)sp->m * ni; a.tw = sp->dst.d.tw;
   a.f = sqrt(2.0 / (L / 2)) * 0.5;
   const int lines_per_cta = cplx ? ColsShape<L>::S : 2 * ColsShape<L>::S;
-  const long long grid = ((ni + lines_per_cta - 1) / lines_per_cta) * no;
+  long long grid = ((ni + lines_per_cta - 1) / lines_per_cta) * no;
+  grid = std::min<long long>(grid, cplx ? resident_ctas(k_dst_cols_fast<L, 1>, ColsShape<L>::T, cols_smem<L>())
+                                        : resident_ctas(k_dst_cols_fast<L, 0>, ColsShape<L>::T, cols_smem<L>()));
   if (cplx) k_dst_cols_fast<L, 1><<<(unsigned)grid, ColsShape<L>::T, cols_smem<L>(), s>>>(a);
   else k_dst_cols_fast<L, 0><<<(unsigned)grid, ColsShape<L>::T, cols_smem<L>(), s>>>(a);
 }
@@ -695,26 +728,27 @@ struct Blocked {
 };
 
 int launch_rows(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long nlines,
-                int epi, const double2* shifts, StatusDev* st, cudaStream_t s, const Blocked& blk = Blocked()) {
+                int epi, const double2* shifts, StatusDev* st, cudaStream_t s, const Blocked& blk = Blocked(),
+                long long lpl = 1) {
   const FftPlanHost& P = sp->dst;
   if (!epi && !g_disable_fast && fast_dst_length(2 * (sp->m + 1)) && nlines > 0) {
     switch (2 * (sp->m + 1)) {
-      case 512: rows_fast<512>(sp, in, out, cplx, nlines, s, blk); break;
-      case 1024: rows_fast<1024>(sp, in, out, cplx, nlines, s, blk); break;
-      case 2048: rows_fast<2048>(sp, in, out, cplx, nlines, s, blk); break;
-      case 8192: rows_fast<8192>(sp, in, out, cplx, nlines, s, blk); break;
+      case 512: rows_fast<512>(sp, in, out, cplx, nlines, s, blk, lpl); break;
+      case 1024: rows_fast<1024>(sp, in, out, cplx, nlines, s, blk, lpl); break;
+      case 2048: rows_fast<2048>(sp, in, out, cplx, nlines, s, blk, lpl); break;
+      case 8192: rows_fast<8192>(sp, in, out, cplx, nlines, s, blk, lpl); break;
     }
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_rows_fast launch");
     return BHCP_OK;
   }
   const int nseq_max = P.max_seqs(kSmemBudget);
   if (nseq_max < 1) return fail(BHCP_ERR_INVALID, "DST length does not fit the FFT engine");
-  const long long seqs = cplx ? nlines : (nlines + 1) / 2;
+  const long long seqs = cplx ? nlines : fastk::real_row_seqs(nlines, lpl);
   const int nseq = (int)(seqs < nseq_max ? seqs : nseq_max);
   if (seqs == 0) return BHCP_OK;
   DstArgs a{};
   a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.m = sp->m; a.dim = sp->dim;
-  a.in = in; a.out = out; a.nlines = nlines;
+  a.in = in; a.out = out; a.nlines = nlines; a.nseqs = seqs; a.lpl = lpl;
   a.f = sqrt(2.0 / (sp->m + 1)) * 0.5;
   a.shifts = shifts; a.mu1 = sp->mu1_dev; a.st = st;
   a.koff = blk.koff; a.kstride = blk.kstride; a.lines_per_level = blk.lines_per_level; a.inner_div = blk.inner_div;
@@ -783,7 +817,8 @@ long long ipow(long long b, int e) {
 int sine_passes(const bhcp_space_plan* sp, const double* in, double* out, int cplx, long long batch,
                 cudaStream_t s) {
   const int d = sp->dim, m = sp->m;
-  int rc = launch_rows(sp, in, out, cplx, batch * ipow(m, d - 1), 0, nullptr, nullptr, s);
+  int rc = launch_rows(sp, in, out, cplx, batch * ipow(m, d - 1), 0, nullptr, nullptr, s, Blocked(),
+                       ipow(m, d - 1));
   if (rc) return rc;
   for (int depth = 1; depth < d; ++depth) {
     rc = launch_cols(sp, out, out, cplx, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0,
@@ -847,7 +882,8 @@ int launch_time(const bhcp_time_plan* tp, int mode, const double* in, int in_cpl
 }
 
 int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
-                 long long k_begin, long long k_end, double* W, long long w_ld, StatusDev* st, cudaStream_t s) {
+                 long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
+                 cudaStream_t s) {
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
@@ -855,10 +891,22 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
     using namespace fastk;
     FastModesArgs f{};
     f.shifts = tp->tables + 2 * tp->n; f.gaminv = tp->tables + tp->n; f.mu1 = sp->mu1_dev; f.ghat = ghat;
-    f.cscale = cscale; f.k_begin = k_begin; f.k_count = kc; f.W = W; f.w_ld = w_ld; f.m = sp->m; f.dim = sp->dim;
-    f.tw = P.d.tw; f.st = st;
-    const long long grid = (kc + ModesPlan<513>::S - 1) / ModesPlan<513>::S;
-    k_modes_fast<513><<<(unsigned)grid, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+    f.cscale = cscale; f.k_begin = k_begin; f.k_count = kc; f.W = W; f.m = sp->m; f.dim = sp->dim;
+    f.tw = P.d.tw; f.st = st; f.wl = wl;
+    {
+      const char* k = getenv("BHCP_EXPERIMENT_SKIP");
+      f.skip = k ? atoi(k) : 0;
+    }
+    // symmetric 4x4 tiles need the whole mode range with global column indices
+    const bool sym = sp->dim == 2 && k_begin == 0 && k_end == sp->nx && sp->tiles_dev && wl.nmodes == sp->nx;
+    if (sym) {
+      f.tiles = sp->tiles_dev;
+      f.ntiles = sp->ntiles;
+      k_modes_fast<513, true><<<(unsigned)sp->ntiles, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+    } else {
+      const long long work = (kc + ModesPlan<513>::S - 1) / ModesPlan<513>::S;
+      k_modes_fast<513, false><<<(unsigned)work, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+    }
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_fast launch");
     return BHCP_OK;
   }
@@ -869,7 +917,7 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
   ModesArgs a{};
   a.p = P.d; a.ld = P.ld; a.nseq = nseq; a.n = tp->n; a.m = sp->m; a.dim = sp->dim;
   a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev;
-  a.ghat = ghat; a.cscale = cscale; a.k_begin = k_begin; a.k_count = kc; a.W = W; a.w_ld = w_ld; a.st = st;
+  a.ghat = ghat; a.cscale = cscale; a.k_begin = k_begin; a.k_count = kc; a.W = W; a.wl = wl; a.st = st;
   const long long grid = (kc + nseq - 1) / nseq;
   const size_t sm = smem_bytes(P, nseq);
 #define BHCP_MODES(VV) \
@@ -878,6 +926,100 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
 #undef BHCP_MODES
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes launch");
   return BHCP_OK;
+}
+
+// W layout of the single-GPU fused solve: level-major in 1D, one mode-major slab otherwise.
+fastk::WLayout native_layout(const bhcp_space_plan* sp, long long k_count, int n) {
+  fastk::WLayout wl{};
+  if (sp->dim == 1) {
+    wl.mode_major = 0;
+    wl.w_ld = k_count;
+  } else {
+    wl.mode_major = 1;
+    wl.nsl = 1;
+    wl.sl_c[0] = 0;
+    wl.sl_c[1] = n;
+  }
+  wl.nmodes = k_count;
+  return wl;
+}
+
+// --- level passes ----------------------------------------------------------------
+__global__ void k_unpack_modes(const double* __restrict__ in, const long long* __restrict__ koff, long long Lin,
+                               long long plane, long long nx, long long nlev, double* __restrict__ out) {
+  const long long total = nx * nlev;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / nx, k = i - t * nx;
+    const long long k1 = k / plane, rem = k - k1 * plane;
+    const long long base = koff ? koff[k1] : k1 * plane * Lin;
+    out[i] = in[base + rem * Lin + t];
+  }
+}
+
+template <int L, int MODE>
+int gather_launch(const bhcp_space_plan* sp, gdst::Args a, cudaStream_t s) {
+  using namespace gdst;
+  const long long tiles = ((a.ni + 2 * Plan<L>::S - 1) / (2 * Plan<L>::S)) * a.no;
+  if (tiles == 0) return BHCP_OK;
+  const size_t sm = gdst::smem_bytes<L>();
+  long long grid = std::min<long long>(tiles, resident_ctas(k_dst_gather<L, MODE>, Plan<L>::T, sm));
+  k_dst_gather<L, MODE><<<(unsigned)grid, Plan<L>::T, sm, s>>>(a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_gather launch");
+  return BHCP_OK;
+}
+
+template <int MODE>
+int gather_dispatch(const bhcp_space_plan* sp, const gdst::Args& a, cudaStream_t s) {
+  switch (2 * (sp->m + 1)) {
+    case 512: return gather_launch<512, MODE>(sp, a, s);
+    case 1024: return gather_launch<1024, MODE>(sp, a, s);
+    case 2048: return gather_launch<2048, MODE>(sp, a, s);
+    case 8192: return gather_launch<8192, MODE>(sp, a, s);
+  }
+  return fail(BHCP_ERR_INVALID, "no gather kernel for this length");
+}
+
+// One level pass of the fused solve on `nlev` levels. pass 0: W (mode-major,
+// line starts koff[k1] or k1*plane*Lin) -> y (level-major) with the DST along
+// the last axis; pass p >= 1: DST along axis -(p+1) in place on y.
+int level_pass(const bhcp_space_plan* sp, const double* in, const long long* koff, long long Lin, double* y,
+               long long nlev, int pass, cudaStream_t s, long long level0 = 0) {
+  const int d = sp->dim, m = sp->m;
+  const bool fast = !g_disable_fast && fast_dst_length(2 * (sp->m + 1));
+  if (pass == 0 && d == 1) {
+    // 1D: W is level-major -> contiguous rows
+    return launch_rows(sp, in, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
+  }
+  if (!fast) {
+    if (pass == 0) {
+      const long long total = nlev * sp->nx;
+      k_unpack_modes<<<(unsigned)std::min<long long>((total + 255) / 256, 65535), 256, 0, s>>>(
+          in, koff, Lin, ipow(m, d - 1), sp->nx, nlev, y);
+      if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_unpack_modes");
+      return launch_rows(sp, y, y, 0, nlev * ipow(m, d - 1), 0, nullptr, nullptr, s, Blocked(), ipow(m, d - 1));
+    }
+    return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
+  }
+  gdst::Args a{};
+  a.tw = sp->dst.d.tw;
+  a.f = sqrt(2.0 / (m + 1)) * 0.5;
+  a.m = m;
+  if (pass == 0) {
+    a.in = in; a.out = y;
+    a.ni = nlev; a.no = ipow(m, d - 1);
+    a.P = ipow(m, d - 1);
+    a.idiv = ipow(m, d - 2);
+    a.Lin = Lin;
+    a.koff = koff;
+    a.ibase = 0;
+    a.ishift = (int)(level0 & 1);
+    return gather_dispatch<0>(sp, a, s);
+  }
+  a.in = y; a.out = y;
+  a.ni = ipow(m, pass); a.no = nlev * ipow(m, d - 1 - pass);
+  a.es = ipow(m, pass); a.os = ipow(m, pass + 1);
+  return gather_dispatch<1>(sp, a, s);
 }
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -905,6 +1047,7 @@ bool ensure_device_constants(int device, std::string* err) {
     return false;
   }
   cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, device);
   {
     const char* e = getenv("BHCP_DISABLE_FAST");
     g_disable_fast = (e && e[0] == '1');
@@ -942,6 +1085,19 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
     free_fft_plan(&sp->dst); delete sp; return cuda_fail("cudaMalloc mu1");
   }
   cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
+  sp->tiles_dev = nullptr;
+  sp->ntiles = 0;
+  if (dim == 2) {
+    const int mt = (sp->m + 3) / 4;
+    std::vector<int2> tiles;
+    for (int a = 0; a < mt; ++a)
+      for (int b = a; b < mt; ++b) tiles.push_back(make_int2(a, b));
+    sp->ntiles = (long long)tiles.size();
+    if (cudaMalloc(&sp->tiles_dev, sizeof(int2) * tiles.size()) != cudaSuccess) {
+      free_fft_plan(&sp->dst); cudaFree(sp->mu1_dev); delete sp; return cuda_fail("cudaMalloc tiles");
+    }
+    cudaMemcpy(sp->tiles_dev, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice);
+  }
   *out = sp;
   return BHCP_OK;
 }
@@ -951,6 +1107,7 @@ void bhcp_space_plan_destroy(bhcp_space_plan* sp) {
   DeviceGuard g(sp->device);
   free_fft_plan(&sp->dst);
   cudaFree(sp->mu1_dev);
+  if (sp->tiles_dev) cudaFree(sp->tiles_dev);
   delete sp;
 }
 
@@ -1021,7 +1178,7 @@ int bhcp_sine_axis(const bhcp_space_plan* sp, const void* in, void* out, int is_
   const int cplx = is_complex ? 1 : 0;
   if (axis == 0)
     return launch_rows(sp, (const double*)in, (double*)out, cplx, batch * ipow(m, d - 1), 0, nullptr, nullptr,
-                       as_stream(stream));
+                       as_stream(stream), Blocked(), ipow(m, d - 1));
   return launch_cols(sp, (const double*)in, (double*)out, cplx, ipow(m, axis), batch * ipow(m, d - 1 - axis), axis,
                      0, nullptr, nullptr, as_stream(stream));
 }
@@ -1074,19 +1231,44 @@ int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
 }
 
 int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat_dev, int64_t k_begin,
-                    int64_t k_end, double* w_dev, int64_t w_ld, void* status_dev, void* stream) {
+                    int64_t k_end, double* w_dev, int nslabs, const int64_t* slab_bounds, void* status_dev,
+                    void* stream) {
   if (!sp || !tp || !ghat_dev || !w_dev || !status_dev) return fail(BHCP_ERR_INVALID, "bad argument");
   if (k_begin < 0 || k_end > sp->nx || k_begin > k_end) return fail(BHCP_ERR_INVALID, "bad mode range");
+  if (nslabs < 0 || nslabs > 8) return fail(BHCP_ERR_INVALID, "nslabs must be in [0, 8]");
   DeviceGuard g(sp->device);
-  return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, w_dev, w_ld, (StatusDev*)status_dev,
+  fastk::WLayout wl = native_layout(sp, k_end - k_begin, tp->n);
+  if (nslabs > 0) {
+    if (!slab_bounds || slab_bounds[0] != 0 || slab_bounds[nslabs] != tp->n)
+      return fail(BHCP_ERR_INVALID, "slab bounds must cover [0, n_levels)");
+    wl.mode_major = 1;
+    wl.nsl = nslabs;
+    for (int i = 0; i <= nslabs; ++i) {
+      if (i > 0 && slab_bounds[i] < slab_bounds[i - 1]) return fail(BHCP_ERR_INVALID, "slab bounds not sorted");
+      wl.sl_c[i] = (int)slab_bounds[i];
+    }
+  }
+  return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, w_dev, wl, (StatusDev*)status_dev,
                       as_stream(stream));
+}
+
+int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, int64_t lin,
+                         double* y_dev, int64_t nlev, int pass, void* stream) {
+  if (!sp || !in_dev || !y_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (pass < 0 || pass >= sp->dim) return fail(BHCP_ERR_INVALID, "pass out of range");
+  DeviceGuard g(sp->device);
+  return level_pass(sp, in_dev, (const long long*)koff_dev, lin, y_dev, nlev, pass, as_stream(stream));
 }
 
 int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t batch,
                      void* stream) {
   if (!sp || !in_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   DeviceGuard g(sp->device);
-  return sine_passes(sp, in_dev, out_dev, 0, batch, as_stream(stream));
+  for (int p = 0; p < sp->dim; ++p) {
+    int rc = level_pass(sp, in_dev, nullptr, batch, out_dev, batch, p, as_stream(stream));
+    if (rc) return rc;
+  }
+  return BHCP_OK;
 }
 
 int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* g_dev, double divisor,
@@ -1104,28 +1286,22 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   int rc = sine_passes(sp, g_dev, ghat, 0, 1, s);
   if (rc) return rc;
   const double cscale = 1.0 / (divisor * (double)tp->n);
-  rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, sp->nx, st, s);
+  rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, native_layout(sp, sp->nx, tp->n), st, s);
   if (rc) return rc;
-  return sine_passes(sp, W, y_dev, 0, tp->n, s);
+  for (int p = 0; p < sp->dim; ++p) {
+    rc = level_pass(sp, W, nullptr, tp->n, y_dev, tp->n, p, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
 }
 
-int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev,
-                             const int64_t* kstride_dev, double* out_dev, int64_t batch, void* stream) {
-  if (!sp || !in_dev || !koff_dev || !kstride_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, int64_t lin,
+                             double* out_dev, int64_t batch, int64_t level0, void* stream) {
+  if (!sp || !in_dev || !koff_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
   DeviceGuard g(sp->device);
-  cudaStream_t s = as_stream(stream);
-  const int d = sp->dim, m = sp->m;
-  Blocked blk;
-  blk.koff = (const long long*)koff_dev;
-  blk.kstride = (const long long*)kstride_dev;
-  blk.lines_per_level = ipow(m, d - 1);
-  blk.inner_div = ipow(m, d - 2);
-  int rc = launch_rows(sp, in_dev, out_dev, 0, batch * ipow(m, d - 1), 0, nullptr, nullptr, s, blk);
-  if (rc) return rc;
-  for (int depth = 1; depth < d; ++depth) {
-    rc = launch_cols(sp, out_dev, out_dev, 0, ipow(m, depth), batch * ipow(m, d - 1 - depth), depth, 0, nullptr,
-                     nullptr, s);
+  for (int p = 0; p < sp->dim; ++p) {
+    int rc = level_pass(sp, in_dev, (const long long*)koff_dev, lin, out_dev, batch, p, as_stream(stream), level0);
     if (rc) return rc;
   }
   return BHCP_OK;

@@ -2,12 +2,14 @@
 //
 // k_dst_rows_fast / k_dst_cols_fast: orthonormal DST-I (space.py:163-177) of
 //   length N-1 through an odd-extension FFT of length L = 2N, for
-//   N in {256, 512, 1024, 4096}; first stage reads global memory, last stage
-//   writes the coefficients straight back (one shared-memory round trip per
-//   middle stage only).
-// k_modes_fast: pass A of the fused solve for n = 513 time levels:
+//   N in {256, 512, 1024, 4096}; the first stage reads global memory, the last
+//   stage writes the coefficients straight back.
+// k_modes_fast: pass A of the fused solve for n = 513 levels:
 //   generator = 1/(s_j + mu_k) computed in registers, sink = Gamma^-1, Re,
-//   norms and the coalesced store of W[t, k].
+//   residue norms and the coalesced store of W[t, k]. In 2D the CTA works on
+//   a 4x4 tile (k1, k2) of the upper triangle k1 <= k2 and also stores the
+//   mirrored tile: mu(k1,k2) = mu1[k1] + mu1[k2] is bit-identical to
+//   mu(k2,k1), so the time transform of one mode serves both.
 // Included by bhcp_b200.cu (single translation unit).
 #pragma once
 #include "static_fft.cuh"
@@ -17,6 +19,37 @@ namespace fastk {
 
 using namespace sfft;
 
+// fp64 reciprocal: hardware approximation + two Newton steps (<= 1 ulp).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Layout of W written by the modes kernels.
+//   mode_major = 0: level-major, W[t * w_ld + k]               (1D)
+//   mode_major = 1: mode-major per level slab s:               (2D / 3D)
+//     W[nmodes * c[s] + k * (c[s+1] - c[s]) + (t - c[s])]
+//     one slab on one GPU; one slab per destination rank in the slab-
+//     decomposed solve, so each all-to-all chunk is contiguous.
+struct WLayout {
+  int mode_major;
+  int nsl;
+  int sl_c[9];
+  long long nmodes;
+  long long w_ld;
+  __host__ __device__ __forceinline__ long long addr(long long k, int t) const {
+    if (!mode_major) return (long long)t * w_ld + k;
+    int s = 0;
+    while (s + 1 < nsl && t >= sl_c[s + 1]) ++s;
+    const long long Ls = sl_c[s + 1] - sl_c[s];
+    return nmodes * sl_c[s] + k * Ls + (t - sl_c[s]);
+  }
+};
+
 // radix plans for the odd-extension DST lengths (L = 2N)
 template <int L> struct DstPlan;
 template <> struct DstPlan<512> { template <int S, int T, class Lay> using F = Fft<512, S, T, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
@@ -24,23 +57,24 @@ template <> struct DstPlan<1024> { template <int S, int T, class Lay> using F = 
 template <> struct DstPlan<2048> { template <int S, int T, class Lay> using F = Fft<2048, S, T, Lay, 16, 16, 8>; static constexpr int R1 = 16; };
 template <> struct DstPlan<8192> { template <int S, int T, class Lay> using F = Fft<8192, S, T, Lay, 16, 16, 8, 4>; static constexpr int R1 = 16; };
 
-// CTA shapes: sequences per CTA (S) and threads (T), rows / cols kernels
+// CTA shapes: sequences per CTA (S), threads (T), min CTAs per SM
 template <int L> struct RowsShape;
-template <> struct RowsShape<512> { static constexpr int S = 8, T = 256; };
-template <> struct RowsShape<1024> { static constexpr int S = 4, T = 256; };
-template <> struct RowsShape<2048> { static constexpr int S = 2, T = 256; };
-template <> struct RowsShape<8192> { static constexpr int S = 1, T = 512; };
+template <> struct RowsShape<512> { static constexpr int S = 8, T = 256, MINB = 2; };
+template <> struct RowsShape<1024> { static constexpr int S = 4, T = 256, MINB = 2; };
+template <> struct RowsShape<2048> { static constexpr int S = 2, T = 256, MINB = 2; };
+template <> struct RowsShape<8192> { static constexpr int S = 1, T = 512, MINB = 1; };
 template <int L> struct ColsShape;
-template <> struct ColsShape<512> { static constexpr int S = 8, T = 256; };
-template <> struct ColsShape<1024> { static constexpr int S = 4, T = 256; };
-template <> struct ColsShape<2048> { static constexpr int S = 4, T = 512; };
-template <> struct ColsShape<8192> { static constexpr int S = 1, T = 512; };
+template <> struct ColsShape<512> { static constexpr int S = 8, T = 256, MINB = 2; };
+template <> struct ColsShape<1024> { static constexpr int S = 4, T = 256, MINB = 2; };
+template <> struct ColsShape<2048> { static constexpr int S = 4, T = 512, MINB = 1; };
+template <> struct ColsShape<8192> { static constexpr int S = 1, T = 512, MINB = 1; };
 
 struct FastDstArgs {
   const double* in;
   double* out;
-  long long nseqs;   // rows: number of FFT sequences (complex lines or real pairs)
+  long long nseqs;   // rows: number of FFT sequences
   long long nlines;  // rows: number of lines
+  long long lpl;     // rows, real data: lines per level (>1: pair lines inside a level)
   long long ni, no, es, os;  // cols geometry
   const double2* tw;
   double f;          // sqrt(2/N)/2
@@ -60,12 +94,35 @@ __device__ __forceinline__ long long fast_line_base(const FastDstArgs& a, long l
   return __ldg(a.koff + k1) + t * __ldg(a.kstride + k1) + r2 * a.m;
 }
 
+// Real-data rows: FFT sequence s carries lines (l0, l1). With lpl > 1 the two
+// lines are taken inside one level (lines (t, 2u), (t, 2u+1)), so the result
+// of a level never depends on which other levels share the launch (slab
+// decomposition stays bit-identical); with lpl == 1 (1D) consecutive levels
+// are paired. l1 = -1 when the partner line does not exist.
+__host__ __device__ __forceinline__ void pair_lines(long long s, long long nlines, long long lpl, long long& l0,
+                                                    long long& l1) {
+  if (lpl > 1) {
+    const long long ppl = (lpl + 1) / 2;
+    const long long t = s / ppl, u = s - t * ppl;
+    l0 = t * lpl + 2 * u;
+    l1 = (2 * u + 1 < lpl) ? l0 + 1 : -1;
+  } else {
+    l0 = 2 * s;
+    l1 = 2 * s + 1;
+  }
+  if (l0 >= nlines) l0 = -1;
+  if (l1 >= nlines) l1 = -1;
+}
+__host__ __device__ __forceinline__ long long real_row_seqs(long long nlines, long long lpl) {
+  return lpl > 1 ? (nlines / lpl) * ((lpl + 1) / 2) : (nlines + 1) / 2;
+}
+
 // ---------------------------------------------------------------- rows
 template <int L, int CPLX>
 struct RowsGen {
   const double* in;
-  long long s0, nlines;
-  const long long* base;  // shared: start of each line of the CTA (2 per sequence)
+  long long s0, nseqs;
+  const long long* base;  // shared: input start of each line of the CTA (2 per sequence), -1 = none
   __device__ __forceinline__ double2 operator()(int q, int idx) const {
     constexpr int N = L / 2, m = N - 1;
     if (idx == 0 || idx == N) return make_double2(0.0, 0.0);
@@ -74,11 +131,11 @@ struct RowsGen {
     const long long s = s0 + q;
     double2 x = make_double2(0.0, 0.0);
     if (CPLX) {
-      if (s < nlines) x = __ldg(reinterpret_cast<const double2*>(in) + s * m + e);
+      if (s < nseqs) x = __ldg(reinterpret_cast<const double2*>(in) + s * m + e);
     } else {
-      const long long l0 = 2 * s;
-      if (l0 < nlines) x.x = __ldg(in + base[2 * q] + e);
-      if (l0 + 1 < nlines) x.y = __ldg(in + base[2 * q + 1] + e);
+      const long long b0 = base[2 * q], b1 = base[2 * q + 1];
+      if (b0 >= 0) x.x = __ldg(in + b0 + e);
+      if (b1 >= 0) x.y = __ldg(in + b1 + e);
     }
     return neg ? make_double2(-x.x, -x.y) : x;
   }
@@ -87,7 +144,8 @@ struct RowsGen {
 template <int L, int CPLX>
 struct RowsSink {
   double* out;
-  long long s0, nlines;
+  long long s0, nseqs;
+  const long long* obase;  // shared: output start of each line (2 per sequence), -1 = none
   double f;
   __device__ __forceinline__ void operator()(int q, int idx, double2 X) const {
     constexpr int N = L / 2, m = N - 1;
@@ -96,30 +154,55 @@ struct RowsSink {
     const int e = idx - 1;
     const double2 c = make_double2(-f * X.y, f * X.x);
     if (CPLX) {
-      if (s < nlines) reinterpret_cast<double2*>(out)[s * m + e] = c;
+      if (s < nseqs) reinterpret_cast<double2*>(out)[s * m + e] = c;
     } else {
-      const long long l0 = 2 * s;
-      if (l0 < nlines) out[l0 * m + e] = c.x;
-      if (l0 + 1 < nlines) out[(l0 + 1) * m + e] = c.y;
+      const long long b0 = obase[2 * q], b1 = obase[2 * q + 1];
+      if (b0 >= 0) out[b0 + e] = c.x;
+      if (b1 >= 0) out[b1 + e] = c.y;
     }
   }
 };
 
+// twiddle table: global (L1-cached); set TwSmem<L>::on to stage it in shared memory
+template <int L> struct TwSmem { static constexpr bool on = false; static constexpr int n = on ? L : 0; };
+
+template <int L>
+__device__ __forceinline__ const double2* stage_twiddles(const double2* tw_g, double2* tw_s) {
+  if constexpr (TwSmem<L>::on) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) tw_s[i] = __ldg(tw_g + i);
+    return tw_s;
+  } else {
+    return tw_g;
+  }
+}
+
+// Persistent: each CTA loops over tiles of S sequences (grid = resident CTAs).
 template <int L, int CPLX>
-__global__ void __launch_bounds__(RowsShape<L>::T) k_dst_rows_fast(FastDstArgs a) {
+__global__ void __launch_bounds__(RowsShape<L>::T, RowsShape<L>::MINB) k_dst_rows_fast(FastDstArgs a) {
   constexpr int S = RowsShape<L>::S, T = RowsShape<L>::T;
   using Lay = SeqMajorPad<L, DstPlan<L>::R1>;
   extern __shared__ double2 smem[];
-  __shared__ long long s_base[2 * S];
-  const long long s0 = (long long)blockIdx.x * S;
-  if (!CPLX && threadIdx.x < 2 * S) {
-    const long long l = 2 * s0 + threadIdx.x;
-    s_base[threadIdx.x] = l < a.nlines ? fast_line_base(a, l) : 0;
+  __shared__ long long s_base[2 * S], s_obase[2 * S];
+  double2* buf = smem;
+  const double2* tw = stage_twiddles<L>(a.tw, smem + Lay::words(S));
+  const long long ntiles = (a.nseqs + S - 1) / S;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long s0 = tile * S;
+    __syncthreads();  // previous tile done with buf / s_base
+    if (!CPLX && threadIdx.x < S) {
+      long long l0, l1;
+      pair_lines(s0 + threadIdx.x, a.nlines, a.lpl, l0, l1);
+      if (s0 + threadIdx.x >= a.nseqs) l0 = l1 = -1;
+      s_base[2 * threadIdx.x] = l0 >= 0 ? fast_line_base(a, l0) : -1;
+      s_base[2 * threadIdx.x + 1] = l1 >= 0 ? fast_line_base(a, l1) : -1;
+      s_obase[2 * threadIdx.x] = l0 >= 0 ? l0 * a.m : -1;
+      s_obase[2 * threadIdx.x + 1] = l1 >= 0 ? l1 * a.m : -1;
+    }
+    __syncthreads();
+    RowsGen<L, CPLX> gen{a.in, s0, a.nseqs, s_base};
+    RowsSink<L, CPLX> sink{a.out, s0, a.nseqs, s_obase, a.f};
+    DstPlan<L>::template F<S, T, Lay>::run(buf, tw, gen, sink);
   }
-  __syncthreads();
-  RowsGen<L, CPLX> gen{a.in, s0, a.nlines, s_base};
-  RowsSink<L, CPLX> sink{a.out, s0, a.nlines, a.f};
-  DstPlan<L>::template F<S, T, Lay>::run(smem, a.tw, gen, sink);
 }
 
 // ---------------------------------------------------------------- cols
@@ -167,25 +250,31 @@ struct ColsSink {
 };
 
 template <int L, int CPLX>
-__global__ void __launch_bounds__(ColsShape<L>::T) k_dst_cols_fast(FastDstArgs a) {
+__global__ void __launch_bounds__(ColsShape<L>::T, ColsShape<L>::MINB) k_dst_cols_fast(FastDstArgs a) {
   constexpr int S = ColsShape<L>::S, T = ColsShape<L>::T;
-  using Lay = Interleaved<S>;
+  using Lay = Interleaved<S, DstPlan<L>::R1>;
   extern __shared__ double2 smem[];
   constexpr int lines_per_cta = CPLX ? S : 2 * S;
+  double2* buf = smem;
+  const double2* tw = stage_twiddles<L>(a.tw, smem + Lay::words(L));
   const long long ntile = (a.ni + lines_per_cta - 1) / lines_per_cta;
-  const long long o = blockIdx.x / ntile;
-  const long long i0 = (blockIdx.x - o * ntile) * lines_per_cta;
-  const long long off = (CPLX ? 2 : 1) * (o * a.os);
-  ColsGen<L, CPLX> gen{a.in + off, i0, a.ni, a.es};
-  ColsSink<L, CPLX> sink{a.out + off, i0, a.ni, a.es, a.f};
-  DstPlan<L>::template F<S, T, Lay>::run(smem, a.tw, gen, sink);
+  const long long total = ntile * a.no;
+  for (long long tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    const long long o = tile / ntile;
+    const long long i0 = (tile - o * ntile) * lines_per_cta;
+    const long long off = (CPLX ? 2 : 1) * (o * a.os);
+    __syncthreads();
+    ColsGen<L, CPLX> gen{a.in + off, i0, a.ni, a.es};
+    ColsSink<L, CPLX> sink{a.out + off, i0, a.ni, a.es, a.f};
+    DstPlan<L>::template F<S, T, Lay>::run(buf, tw, gen, sink);
+  }
 }
 
 // ---------------------------------------------------------------- modes
 template <int N> struct ModesPlan;
 template <> struct ModesPlan<513> {
-  static constexpr int S = 8, T = 256;
-  template <class Lay> using F = Fft<513, S, T, Lay, 19, 9, 3>;
+  static constexpr int S = 16, T = 512, MINB = 1;
+  using WF = WarpFft<513, 19, 9, 3>;
 };
 
 struct FastModesArgs {
@@ -196,71 +285,105 @@ struct FastModesArgs {
   double cscale;
   long long k_begin, k_count;
   double* W;
-  long long w_ld;
   int m, dim;
   const double2* tw;
   StatusDev* st;
+  const int2* tiles;  // SYM: upper-triangle 4x4 tile coordinates (a, b), a <= b
+  long long ntiles;
+  int skip;           // experiment: 1 = no W stores, 2 = no FFT
+  WLayout wl;
 };
 
-template <int S>
-struct ModesGen {
-  const double2* shifts;
-  const double* smu;  // shared: per-sequence mu
-  const bool* valid;
-  StatusDev* st;
-  __device__ __forceinline__ double2 operator()(int q, int j) const {
-    const double2 s = __ldg(shifts + j);
-    if (!valid[q]) return make_double2(0.0, 0.0);
-    const double dr = s.x + smu[q], di = s.y;
-    const double den2 = dr * dr + di * di;
-    if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(st, j);
-    const double inv = 1.0 / den2;
-    return make_double2(dr * inv, -di * inv);
-  }
-};
-
-template <int S>
-struct ModesSink {
-  const double2* gaminv;
-  const double* sc;  // shared: per-sequence ghat * cscale
-  const bool* valid;
-  double* W;
-  long long w_ld, kl0;
-  double sre, sim;
-  __device__ __forceinline__ void operator()(int q, int t, double2 X) {
-    if (!valid[q]) return;
-    const double2 g = __ldg(gaminv + t);
-    const double c = sc[q];
-    const double wr = c * (X.x * g.x - X.y * g.y);
-    const double wi = c * (X.x * g.y + X.y * g.x);
-    sre = fma(wr, wr, sre);
-    sim = fma(wi, wi, sim);
-    W[(long long)t * w_ld + kl0 + q] = wr;
-  }
-};
-
-template <int N>
-__global__ void __launch_bounds__(ModesPlan<N>::T) k_modes_fast(FastModesArgs a) {
+// Warp-per-mode pass A: the CTA takes S = 16 modes (a 4x4 upper-triangle tile
+// in 2D, SYM, or 16 consecutive modes); warp q transforms mode q in its own
+// shared-memory region with warp-synchronous stages, then the CTA writes
+// W[t, k] (and the mirrored columns) with coalesced stores.
+template <int N, bool SYM>
+__global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_fast(FastModesArgs a) {
   constexpr int S = ModesPlan<N>::S, T = ModesPlan<N>::T;
-  using Lay = Interleaved<S>;
+  static_assert(T == 32 * S, "one warp per mode");
+  constexpr int LDW = N;  // per-warp region (odd length: conflict-light)
   extern __shared__ double2 smem[];
-  __shared__ double s_mu[S], s_c[S], red[2 * (T / 32)];
+  __shared__ double s_mu[S], s_c[S], s_cm[S], red[2 * (T / 32)];
+  __shared__ long long s_dst[S], s_mir[S];
   __shared__ bool s_valid[S];
-  const long long kl0 = (long long)blockIdx.x * S;
+  __shared__ double2 s_gi[N], s_sh[N];
+  for (int i = threadIdx.x; i < N; i += T) {
+    s_gi[i] = __ldg(a.gaminv + i);
+    s_sh[i] = __ldg(a.shifts + i);
+  }
   if (threadIdx.x < S) {
     const int q = threadIdx.x;
-    const long long kl = kl0 + q;
-    const bool v = kl < a.k_count;
+    bool v;
+    long long kd, km = -1;
+    if (SYM) {
+      const int2 tb = a.tiles[blockIdx.x];
+      const int k1 = 4 * tb.x + (q >> 2), k2 = 4 * tb.y + (q & 3);
+      v = (k1 < a.m) && (k2 < a.m) && (tb.x != tb.y || k1 <= k2);
+      kd = (long long)k1 * a.m + k2;
+      if (v && k1 != k2) km = (long long)k2 * a.m + k1;
+      if (!v) kd = 0;
+    } else {
+      const long long kl = (long long)blockIdx.x * S + q;
+      v = kl < a.k_count;
+      kd = a.k_begin + (v ? kl : 0);
+    }
     s_valid[q] = v;
-    const long long k = a.k_begin + (v ? kl : 0);
-    s_mu[q] = mode_mu(a.mu1, a.m, a.dim, k);
-    s_c[q] = v ? a.ghat[k] * a.cscale : 0.0;
+    s_mu[q] = mode_mu(a.mu1, a.m, a.dim, kd);
+    s_c[q] = v ? a.ghat[kd] * a.cscale : 0.0;
+    s_cm[q] = (km >= 0) ? a.ghat[km] * a.cscale : 0.0;
+    s_dst[q] = v ? (SYM ? kd : kd - a.k_begin) : -1;
+    s_mir[q] = km;
   }
   __syncthreads();
-  ModesGen<S> gen{a.shifts, s_mu, s_valid, a.st};
-  ModesSink<S> sink{a.gaminv, s_c, s_valid, a.W, a.w_ld, kl0, 0.0, 0.0};
-  ModesPlan<N>::template F<Lay>::run(smem, a.tw, gen, sink);
-  double sre = sink.sre, sim = sink.sim;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* buf = smem + warp * LDW;
+  {
+    const double mu = s_mu[warp];
+    const bool valid = s_valid[warp];
+    StatusDev* st = a.st;
+    const double2* shifts = s_sh;
+    auto gen = [&](int j) -> double2 {
+      const double2 s = shifts[j];
+      if (!valid) return make_double2(0.0, 0.0);
+      const double dr = s.x + mu, di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(st, j);
+      const double inv = fast_rcp(den2);
+      return make_double2(dr * inv, -di * inv);
+    };
+    if (a.skip != 2) ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
+  }
+  __syncthreads();
+  // store phase: W is mode-major per destination level slab:
+  // element (mode k, level t) of slab s at boff[s] + k * (c[s+1]-c[s]) + t - c[s],
+  // k = column index (SYM: global mode, else local to k_begin). Threads run
+  // along t, so each mode's time series is written contiguously.
+  double sre = 0.0, sim = 0.0;
+  for (int i = threadIdx.x; i < S * N; i += T) {
+    const int q = i / N, t = i - q * N;
+    const long long cd = s_dst[q];
+    if (cd < 0) continue;
+    const double2 x = smem[q * LDW + t];
+    const double2 g = s_gi[t];
+    const double zr = x.x * g.x - x.y * g.y;
+    const double zi = x.x * g.y + x.y * g.x;
+    const double c = s_c[q];
+    const double wr = c * zr, wi = c * zi;
+    sre = fma(wr, wr, sre);
+    sim = fma(wi, wi, sim);
+    if (a.skip != 1) a.W[a.wl.addr(cd, t)] = wr;
+    if (SYM) {
+      const long long cm = s_mir[q];
+      if (cm >= 0) {
+        const double c2 = s_cm[q];
+        const double vr = c2 * zr, vi = c2 * zi;
+        sre = fma(vr, vr, sre);
+        sim = fma(vi, vi, sim);
+        if (a.skip != 1) a.W[a.wl.addr(cm, t)] = vr;
+      }
+    }
+  }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
     atomicAdd(&a.st->sum_re2, sre);
@@ -270,9 +393,11 @@ __global__ void __launch_bounds__(ModesPlan<N>::T) k_modes_fast(FastModesArgs a)
 
 // smem bytes for each kernel
 template <int L> constexpr size_t rows_smem() {
-  return sizeof(double2) * SeqMajorPad<L, DstPlan<L>::R1>::LD * RowsShape<L>::S;
+  return sizeof(double2) * (SeqMajorPad<L, DstPlan<L>::R1>::words(RowsShape<L>::S) + TwSmem<L>::n);
 }
-template <int L> constexpr size_t cols_smem() { return sizeof(double2) * L * ColsShape<L>::S; }
+template <int L> constexpr size_t cols_smem() {
+  return sizeof(double2) * (Interleaved<ColsShape<L>::S, DstPlan<L>::R1>::words(L) + TwSmem<L>::n);
+}
 template <int N> constexpr size_t modes_smem() { return sizeof(double2) * N * ModesPlan<N>::S; }
 
 }  // namespace fastk

@@ -123,10 +123,12 @@ template <> struct Cod<9> {
 };
 
 // ------------------------------------------------------------------ layouts
-// Interleaved: element idx of sequence q at idx*S + q (thread-fastest = q).
-template <int S> struct Interleaved {
-  static constexpr int words(int L) { return L * S; }
-  static __device__ __forceinline__ int addr(int q, int idx) { return idx * S + q; }
+// Interleaved: element idx of sequence q at idx*S + q + idx/P (thread-fastest
+// = q); the pad slot every P indices breaks the stride-R*S pattern of the
+// first-stage stores (P = first radix).
+template <int S, int P = 1 << 30> struct Interleaved {
+  static constexpr int words(int L) { return L * S + L / P + 1; }
+  static __device__ __forceinline__ int addr(int q, int idx) { return idx * S + q + idx / P; }
   // butterfly b -> (q, j): q fastest
   static __device__ __forceinline__ void split(int b, int nb, int& q, int& j) { q = b % S; j = b / S; }
 };
@@ -139,7 +141,20 @@ template <int L, int P> struct SeqMajorPad {
 };
 
 // ------------------------------------------------------------------ stages
-template <int... Rs> struct RadixList {};
+// Multiply v[r] by w^r, r = 1..R-1, from the single table value w = w_L^(k*TWS)
+// (running product, depth R-2 <= 7 for the radices used after stage 1, so
+// the twiddle error stays within a few ulp) -- one table load per butterfly
+// instead of R-1.
+template <int R>
+__device__ __forceinline__ void apply_twiddles(double2 (&v)[R], double2 w) {
+  double2 p = w;
+  v[1] = cmul(v[1], p);
+#pragma unroll
+  for (int r = 2; r < R; ++r) {
+    p = cmul(p, w);
+    v[r] = cmul(v[r], p);
+  }
+}
 
 template <int L, int S, int T, class Lay, int R, int Ns>
 struct Stage {
@@ -161,11 +176,7 @@ struct Stage {
         qq[i] = q; jj[i] = j;
 #pragma unroll
         for (int r = 0; r < R; ++r) v[i][r] = buf[Lay::addr(q, j + r * (L / R))];
-        if (Ns > 1) {
-          const int k = j % Ns;
-#pragma unroll
-          for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], __ldg(tw + r * k * TWS));
-        }
+        if (Ns > 1) apply_twiddles<R>(v[i], tw[(j % Ns) * TWS]);
         Cod<R>::run(v[i]);
       }
     }
@@ -184,7 +195,8 @@ struct Stage {
     __syncthreads();
   }
 
-  // first stage (Ns == 1): inputs from gen(q, idx) instead of smem
+  // first stage (Ns == 1): inputs from gen(q, idx) instead of smem.
+  // The caller must have synchronised if buf still holds a previous transform.
   template <class Gen>
   static __device__ __forceinline__ void first(double2* buf, Gen& gen) {
     static_assert(Ns == 1, "first stage");
@@ -218,10 +230,7 @@ struct Stage {
         double2 v[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) v[r] = buf[Lay::addr(q, j + r * (L / R))];
-        if (Ns > 1) {
-#pragma unroll
-          for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(tw + r * j * TWS));
-        }
+        if (Ns > 1) apply_twiddles<R>(v, tw[j * TWS]);
         Cod<R>::run(v);
         // k = j (j < Ns), outputs at j + r*Ns
 #pragma unroll
@@ -252,6 +261,98 @@ struct Fft {
     static_assert(sizeof...(Rest) >= 1, "need at least two stages");
     Stage<L, S, T, Lay, R1, 1>::first(buf, gen);
     Runner<L, S, T, Lay, R1, Rest...>::tail(buf, tw, sink);
+  }
+  // stages 2..k only (after the caller ran Stage<..., R1, 1>::first itself)
+  template <class Sink>
+  static __device__ __forceinline__ void tail(double2* buf, const double2* tw, Sink& sink) {
+    Runner<L, S, T, Lay, R1, Rest...>::tail(buf, tw, sink);
+  }
+};
+
+template <class F> struct FftTail {
+  template <class Sink>
+  static __device__ __forceinline__ void run(double2* buf, const double2* tw, Sink& sink) { F::tail(buf, tw, sink); }
+};
+
+}  // namespace sfft
+}  // namespace bhcp
+
+namespace bhcp {
+namespace sfft {
+
+// ------------------------------------------------------------------ warp FFT
+// One warp owns one length-L sequence in its own shared-memory region and runs
+// the Stockham stages with __syncwarp() only: warps of a CTA progress
+// independently (no CTA-wide barrier inside the transform), which is what
+// hides the latency of the FP64 / shared-memory chains at 16 warps per SM.
+// Stage s in place: every lane computes its ceil(L/R / 32) butterflies into
+// registers, the warp synchronises, then stores.
+template <int L, int R, int Ns>
+struct WStage {
+  static constexpr int NB = L / R;
+  static constexpr int PER = (NB + 31) / 32;
+  static constexpr int TWS = L / (Ns * R);
+
+  template <class Gen>
+  static __device__ __forceinline__ void first(double2* buf, int lane, Gen& gen) {
+    static_assert(Ns == 1, "first stage");
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = lane + 32 * i;
+      if (b < NB) {
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[r] = gen(b + r * NB);
+        Cod<R>::run(v);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[b * R + r] = v[r];
+      }
+    }
+    __syncwarp();
+  }
+
+  static __device__ __forceinline__ void mid(double2* buf, int lane, const double2* __restrict__ tw) {
+    double2 v[PER][R];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = lane + 32 * i;
+      if (b < NB) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = buf[b + r * NB];
+        if (Ns > 1) apply_twiddles<R>(v[i], __ldg(tw + (b % Ns) * TWS));
+        Cod<R>::run(v[i]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = lane + 32 * i;
+      if (b < NB) {
+        const int k = b % Ns;
+        const int base = (b - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[i][r];
+      }
+    }
+    __syncwarp();
+  }
+};
+
+template <int L, int Ns, int R, int... Rest>
+struct WRunner {
+  static __device__ __forceinline__ void tail(double2* buf, int lane, const double2* tw) {
+    WStage<L, R, Ns>::mid(buf, lane, tw);
+    if constexpr (sizeof...(Rest) > 0) WRunner<L, Ns * R, Rest...>::tail(buf, lane, tw);
+  }
+};
+
+// Full transform, natural-order result left in buf (per-warp region).
+template <int L, int R1, int... Rest>
+struct WarpFft {
+  template <class Gen>
+  static __device__ __forceinline__ void run(double2* buf, int lane, const double2* tw, Gen& gen) {
+    WStage<L, R1, 1>::first(buf, lane, gen);
+    if constexpr (sizeof...(Rest) > 0) WRunner<L, R1, Rest...>::tail(buf, lane, tw);
   }
 };
 

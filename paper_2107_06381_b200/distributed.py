@@ -52,7 +52,11 @@ class SlabLayout:
         if self.dim < 2:
             raise ValueError("slab decomposition needs dim >= 2 (1D runs stay on one GPU)")
         self.k1 = partition(self.m, self.world)
-        self.lev = partition(self.n, self.world)
+        # level slabs start at even levels: the level passes pack levels
+        # (2u, 2u+1) into one complex FFT, so no pair straddles two ranks and
+        # every rank count gives the single-GPU result bit for bit
+        pairs = partition((self.n + 1) // 2, self.world)
+        self.lev = [(min(2 * a, self.n), min(2 * b, self.n)) for a, b in pairs]
         self.plane = self.m ** (self.dim - 1)   # modes per k1 value
 
     @property
@@ -78,22 +82,26 @@ class SlabLayout:
     def recv_splits(self, r: int) -> List[int]:
         return [self.levels(r) * self.slab_modes(p) for p in range(self.world)]
 
-    def block_tables(self, r: int) -> Tuple[np.ndarray, np.ndarray]:
-        """koff/kstride of bhcp_pint_levels_blocked for receiver r: the line of
-        level t (local), outer mode k1 and inner index r2 starts at
-        koff[k1] + t * kstride[k1] + r2 * m in the receive buffer."""
+    def slab_bounds(self) -> np.ndarray:
+        """Level-slab boundaries (the W chunking of bhcp_pint_modes)."""
+        return np.array([c for c, _ in self.lev] + [self.n], dtype=np.int64)
+
+    def block_tables(self, r: int) -> Tuple[np.ndarray, int]:
+        """koff and level stride of bhcp_pint_levels_blocked for receiver r.
+
+        The receive buffer holds, for every sender p, the mode-major block
+        (S_p modes x L_r levels); mode (k1, rest) of level t (local) is at
+        koff[k1] + rest * L_r + t."""
+        Lr = self.levels(r)
         koff = np.empty(self.m, dtype=np.int64)
-        kstride = np.empty(self.m, dtype=np.int64)
         offset = 0
         recv = self.recv_splits(r)
         for p in range(self.world):
             a, b = self.k1[p]
-            sp = self.slab_modes(p)
             for k1 in range(a, b):
-                koff[k1] = offset + (k1 - a) * self.plane
-                kstride[k1] = sp
+                koff[k1] = offset + (k1 - a) * self.plane * Lr
             offset += recv[p]
-        return koff, kstride
+        return koff, Lr
 
 
 # ---------------------------------------------------------------- orchestration
@@ -101,21 +109,20 @@ class SlabLayout:
 def sharded_solve(ops, comm, layout: SlabLayout, rank: int, events=None):
     """Run one slab-decomposed solve on this rank; returns (y_local, (c, d)).
 
-    ops.modes(k_begin, k_end)          -> W_r, contiguous (n, S_r) float64
-    ops.levels_blocked(recv, koff, kstride, L) -> y (L, n_space)
+    ops.modes(layout, rank)            -> W_r, mode-major per destination slab (flat)
+    ops.levels_blocked(recv, koff, lin, L, level0) -> y (L, n_space)
     comm.all_to_all(send, send_splits, recv_splits) -> recv buffer (flat)
     """
-    kb, ke = layout.mode_range(rank)
     if events:
         events[0].record()
-    W = ops.modes(kb, ke)
+    W = ops.modes(layout, rank)
     if events:
         events[1].record()
     recv = comm.all_to_all(W.reshape(-1), layout.send_splits(rank), layout.recv_splits(rank))
     if events:
         events[2].record()
-    koff, kstride = ops.tables(layout, rank)
-    y = ops.levels_blocked(recv, koff, kstride, layout.levels(rank))
+    koff, lin = ops.tables(layout, rank)
+    y = ops.levels_blocked(recv, koff, lin, layout.levels(rank), layout.lev[rank][0])
     if events:
         events[3].record()
     return y, layout.lev[rank]
@@ -193,31 +200,34 @@ class DeviceOps:
         self._lib.check(self.lib.bhcp_pint_ghat(self.plan.sp.handle, p.ptr(self.g), 1.0 / (self.divisor * self.n),
                                                 p.ptr(self.ghat), p.stream_handle()), "ghat")
 
-    def modes(self, kb: int, ke: int):
+    def modes(self, layout: SlabLayout, rank: int):
         torch, p = self.torch, self.plans
+        kb, ke = layout.mode_range(rank)
         S = ke - kb
-        if self._W is None or self._W.shape != (self.n, S):
-            self._W = torch.empty((self.n, S), dtype=torch.float64, device=self.g.device)
+        if self._W is None or self._W.numel() != S * self.n:
+            self._W = torch.empty(S * self.n, dtype=torch.float64, device=self.g.device)
+        bounds = layout.slab_bounds()
         self.prepare()
         self._lib.check(self.lib.bhcp_pint_modes(self.plan.sp.handle, self.plan.tp.handle, p.ptr(self.ghat), kb, ke,
-                                                 p.ptr(self._W), S, p.ptr(self.status), p.stream_handle()), "modes")
+                                                 p.ptr(self._W), layout.world,
+                                                 bounds.ctypes.data_as(ctypes.c_void_p), p.ptr(self.status),
+                                                 p.stream_handle()), "modes")
         return self._W
 
     def tables(self, layout: SlabLayout, rank: int):
         key = (layout.world, rank)
         if key not in self._tables:
-            koff, kstride = layout.block_tables(rank)
-            dev = self.g.device
-            self._tables[key] = (self.torch.from_numpy(koff).to(dev), self.torch.from_numpy(kstride).to(dev))
+            koff, lin = layout.block_tables(rank)
+            self._tables[key] = (self.torch.from_numpy(koff).to(self.g.device), lin)
         return self._tables[key]
 
-    def levels_blocked(self, recv, koff, kstride, L: int):
+    def levels_blocked(self, recv, koff, lin: int, L: int, level0: int = 0):
         torch, p = self.torch, self.plans
         if self._y is None or self._y.shape != (L, self.nx):
             self._y = torch.empty((L, self.nx), dtype=torch.float64, device=self.g.device)
         if L > 0:
-            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), p.ptr(koff),
-                                                              p.ptr(kstride), p.ptr(self._y), L, p.stream_handle()),
+            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), p.ptr(koff), lin,
+                                                              p.ptr(self._y), L, level0, p.stream_handle()),
                             "levels_blocked")
         return self._y
 

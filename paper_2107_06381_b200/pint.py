@@ -113,7 +113,7 @@ class PintPlan:
                    "bhcp_pint_ghat")
         if events:
             events[1].record()
-        _lib.check(lib.bhcp_pint_modes(self.sp.handle, self.tp.handle, ghat, 0, nx, W, nx, status, stream),
+        _lib.check(lib.bhcp_pint_modes(self.sp.handle, self.tp.handle, ghat, 0, nx, W, 0, None, status, stream),
                    "bhcp_pint_modes")
         if events:
             events[2].record()

@@ -33,14 +33,14 @@ def test_partition_balanced_and_uneven():
 def test_layout_tables_address_every_line_once(dim, m, n, world):
     L = D.SlabLayout(dim, m, n, world)
     for r in range(world):
-        koff, kstride = L.block_tables(r)
+        koff, lin = L.block_tables(r)
+        assert lin == L.levels(r)
         total = sum(L.recv_splits(r))
         seen = np.zeros(total, dtype=int)
         for t in range(L.levels(r)):
             for k1 in range(m):
-                for r2 in range(m ** (dim - 2)):
-                    start = koff[k1] + t * kstride[k1] + r2 * m
-                    seen[start:start + m] += 1
+                for rest in range(m ** (dim - 1)):
+                    seen[koff[k1] + rest * lin + t] += 1
         assert (seen == 1).all()
     assert sum(sum(L.send_splits(r)) for r in range(world)) == n * m**dim
 
@@ -58,26 +58,28 @@ class NumpyOps:
         self.dim, self.m = w.dim, w.num_cells - 1
         self.sums = (0.0, 0.0)
 
-    def modes(self, kb, ke):
+    def modes(self, layout, rank):
+        """W_r mode-major per destination level slab (bhcp_pint_modes layout)."""
         import torch
-        W, sre, sim = O.fused_pass_a(*self.args, kb, ke)
+        kb, ke = layout.mode_range(rank)
+        W, sre, sim = O.fused_pass_a(*self.args, kb, ke)   # (n, S) level-major
         self.sums = (sre, sim)
-        return torch.from_numpy(W)
+        chunks = [np.ascontiguousarray(W[c:d].T).ravel() for c, d in layout.lev]
+        return torch.from_numpy(np.concatenate(chunks))
 
     def tables(self, layout, rank):
         return layout.block_tables(rank)
 
-    def levels_blocked(self, recv, koff, kstride, L):
+    def levels_blocked(self, recv, koff, lin, L, level0=0):
         import torch
         recv = recv.numpy()
         m, d = self.m, self.dim
+        plane = m ** (d - 1)
         F = np.zeros((L, m**d))
-        for t in range(L):
-            for k1 in range(m):
-                for r2 in range(m ** (d - 2)):
-                    s = koff[k1] + t * kstride[k1] + r2 * m
-                    base = k1 * m ** (d - 1) + r2 * m
-                    F[t, base:base + m] = recv[s:s + m]
+        for k1 in range(m):
+            for rest in range(plane):
+                s = koff[k1] + rest * lin
+                F[:, k1 * plane + rest] = recv[s:s + L]
         return torch.from_numpy(O.fused_pass_b(F, d, m))
 
 
@@ -141,13 +143,16 @@ def emulate(system, world):
     plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
     ops = D.DeviceOps(plan, plans.to_device(system.data, torch.float64),
                       system.method.condition_divisor(tg.tau))
-    Ws = [ops.modes(*layout.mode_range(r)).clone() for r in range(world)]
+    Ws = [ops.modes(layout, r).clone() for r in range(world)]
     ys = []
     for q in range(world):
-        c, d = layout.lev[q]
-        recv = torch.cat([Wr[c:d].reshape(-1) for Wr in Ws])
-        koff, kstride = ops.tables(layout, q)
-        ys.append(ops.levels_blocked(recv, koff, kstride, d - c).clone())
+        chunks = []
+        for r in range(world):
+            off = sum(layout.send_splits(r)[:q])
+            chunks.append(Ws[r][off:off + layout.send_splits(r)[q]])
+        recv = torch.cat(chunks)
+        koff, lin = ops.tables(layout, q)
+        ys.append(ops.levels_blocked(recv, koff, lin, layout.levels(q), layout.lev[q][0]).clone())
     return torch.cat(ys).cpu().numpy()
 
 
