@@ -217,7 +217,7 @@ def main():
             if record:
                 record[2].record()
             for a in range(w.dim):
-                _lib.check(lib.bhcp_pint_level_pass(sp, W, None, n, plans.ptr(y), n, a, sh), "level pass")
+                _lib.check(lib.bhcp_pint_level_pass(sp, W, None, plans.ptr(y), n, a, sh), "level pass")
                 if record:
                     record[3 + a].record()
 
@@ -248,7 +248,7 @@ def main():
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
         names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"] + \
-                [f"k_dst_gather pass {a} (axis -{a + 1})" for a in range(w.dim)]
+                [("k_dst_blk" if a == 0 else "k_dst_cols_fast") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof

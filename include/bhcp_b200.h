@@ -162,22 +162,22 @@ int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
  * bhcp_pint_modes: for spatial modes [k_begin, k_end) write
  *   W(k, t) = ghat[k] * Re(gamma_inv_t * FFT_t(1/(s_j + mu_k)))
  *   and accumulate the residue norms / first singular column into status_dev.
- *   Layout of W (K = k_end - k_begin, k local):
- *     nslabs == 0, dim 1:  level-major, W[t * K + k]
- *     nslabs == 0, dim>=2: mode-major,  W[k * n + t]
- *     nslabs >= 1:         mode-major per level slab s (bounds b, host array of
- *                          nslabs+1 int64, b[0] = 0, b[nslabs] = n):
- *                          W[K * b[s] + k * (b[s+1] - b[s]) + t - b[s]]
- *                          (one contiguous all-to-all chunk per destination).
+ *   Layout of W (K = k_end - k_begin, k local, P1 = m^(dim-1)):
+ *     dim 1 (nslabs = 0):  level-major, W[t * K + k]
+ *     dim >= 2:            blocked by level slabs s (nslabs = 0: one slab
+ *       [0, n); else host int64 bounds b[0..nslabs], b[0] = 0, b[nslabs] = n,
+ *       inner bounds multiples of 8; mode range = whole k1 planes):
+ *       W[off_s + ((k1 * NT_s + tl / 8) * P1 + r) * 8 + tl % 8]
+ *       k = k1 * P1 + r, tl = t - b[s], NT_s = ceil((b[s+1]-b[s]) / 8),
+ *       off_s = K * 8 * sum_{s' < s} NT_{s'} -- one contiguous chunk per slab.
  * bhcp_pint_level_pass: pass 0 = inverse DST along the last spatial axis from
- *   W (native layout, or mode-major blocks whose mode (k1, 0..) starts at
- *   koff_dev[k1] with level stride lin when koff_dev is not null) into the
- *   level-major y (nlev, n_space); pass p >= 1 = inverse DST along axis
- *   -(p+1) in place on y.
- * bhcp_pint_levels: passes 0..dim-1 on the native layout (lin = batch).
+ *   W into the level-major y (nlev, n_space): dim 1 level-major W; dim >= 2
+ *   blocked W with k1's first block at koff_dev[k1] (device int64 table of
+ *   length m) or, when koff_dev is null, the single-slab layout above.
+ *   pass p >= 1 = inverse DST along axis -(p+1) in place on y.
+ * bhcp_pint_levels: passes 0..dim-1 on the single-slab layout.
  * bhcp_pint_levels_blocked: passes 0..dim-1 on an all-to-all receive buffer
- *   of mode-major blocks (dim >= 2); level0 = global index of the slab's first
- *   level (keeps the level pairing of the FFT identical to the 1-GPU solve). */
+ *   of blocked chunks (dim >= 2). */
 int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
                    double* ghat_dev, void* stream);
 int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
@@ -185,13 +185,13 @@ int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
                     double* w_dev, int nslabs, const int64_t* slab_bounds,
                     void* status_dev, void* stream);
 int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev,
-                         const int64_t* koff_dev, int64_t lin, double* y_dev,
-                         int64_t nlev, int pass, void* stream);
+                         const int64_t* koff_dev, double* y_dev, int64_t nlev,
+                         int pass, void* stream);
 int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
                      int64_t batch, void* stream);
 int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev,
-                             const int64_t* koff_dev, int64_t lin, double* out_dev,
-                             int64_t batch, int64_t level0, void* stream);
+                             const int64_t* koff_dev, double* out_dev, int64_t batch,
+                             void* stream);
 
 /* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,

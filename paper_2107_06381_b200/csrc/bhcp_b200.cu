@@ -587,6 +587,8 @@ struct bhcp_space_plan {
   FftPlanHost dst;       // FFT of length 2(m+1)
   int2* tiles_dev;       // 2D: upper-triangle 4x4 mode tiles (a, b), a <= b
   long long ntiles;
+  double2* twN;          // exp(-2 pi i k / N), N = m + 1 (half-length DST kernels)
+  double* snN;           // sin(pi j / N)
 };
 
 struct bhcp_time_plan {
@@ -657,6 +659,15 @@ void set_all_attributes() {
   allow_smem(fastk::k_dst_cols_fast<LL, 1>);
   BHCP_FATTR(512) BHCP_FATTR(1024) BHCP_FATTR(2048) BHCP_FATTR(8192)
 #undef BHCP_FATTR
+  allow_smem(gdst::k_dst_blk<512>);
+  allow_smem(gdst::k_dst_blk<1024>);
+  allow_smem(gdst::k_dst_blk<2048>);
+  allow_smem(gdst::k_dst2<256, 0>);
+  allow_smem(gdst::k_dst2<256, 1>);
+  allow_smem(gdst::k_dst2<512, 0>);
+  allow_smem(gdst::k_dst2<512, 1>);
+  allow_smem(gdst::k_dst2<1024, 0>);
+  allow_smem(gdst::k_dst2<1024, 1>);
   allow_smem(gdst::k_dst_gather<512, 0>);
   allow_smem(gdst::k_dst_gather<512, 1>);
   allow_smem(gdst::k_dst_gather<1024, 0>);
@@ -714,6 +725,7 @@ void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cpl
 }
 
 bool fast_dst_length(int L) { return L == 512 || L == 1024 || L == 2048 || L == 8192; }
+bool g_use_dst2 = false;  // half-length DST level pass (BHCP_USE_DST2=1); see DESIGN.md 7
 bool g_disable_fast = false;
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -928,33 +940,64 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
   return BHCP_OK;
 }
 
-// W layout of the single-GPU fused solve: level-major in 1D, one mode-major slab otherwise.
-fastk::WLayout native_layout(const bhcp_space_plan* sp, long long k_count, int n) {
+// W layout of the single-GPU fused solve: level-major in 1D, one blocked slab otherwise.
+fastk::WLayout make_blocked(const bhcp_space_plan* sp, long long k_count, int nsl, const long long* bounds) {
   fastk::WLayout wl{};
-  if (sp->dim == 1) {
-    wl.mode_major = 0;
-    wl.w_ld = k_count;
-  } else {
-    wl.mode_major = 1;
-    wl.nsl = 1;
-    wl.sl_c[0] = 0;
-    wl.sl_c[1] = n;
-  }
+  wl.mode_major = 2;
+  wl.nsl = nsl;
   wl.nmodes = k_count;
+  wl.P1 = ipow(sp->m, sp->dim - 1);
+  long long off = 0;
+  for (int s = 0; s < nsl; ++s) {
+    wl.sl_c[s] = (int)bounds[s];
+    wl.sl_nt[s] = (bounds[s + 1] - bounds[s] + fastk::kTBL - 1) / fastk::kTBL;
+    wl.sl_off[s] = off;
+    off += k_count * fastk::kTBL * wl.sl_nt[s];
+  }
+  wl.sl_c[nsl] = (int)bounds[nsl];
   return wl;
 }
 
+fastk::WLayout native_layout(const bhcp_space_plan* sp, long long k_count, int n) {
+  if (sp->dim == 1) {
+    fastk::WLayout wl{};
+    wl.mode_major = 0;
+    wl.w_ld = k_count;
+    wl.nmodes = k_count;
+    return wl;
+  }
+  const long long b[2] = {0, n};
+  return make_blocked(sp, k_count, 1, b);
+}
+
+long long native_w_elems(const bhcp_space_plan* sp, int n) {
+  if (sp->dim == 1) return sp->nx * (long long)n;
+  return sp->nx * fastk::kTBL * ((n + fastk::kTBL - 1) / fastk::kTBL);
+}
+
 // --- level passes ----------------------------------------------------------------
-__global__ void k_unpack_modes(const double* __restrict__ in, const long long* __restrict__ koff, long long Lin,
-                               long long plane, long long nx, long long nlev, double* __restrict__ out) {
+__global__ void k_unpack_blocked(const double* __restrict__ in, const long long* __restrict__ koff, long long NT,
+                                 long long P1, long long nx, long long nlev, double* __restrict__ out) {
   const long long total = nx * nlev;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long t = i / nx, k = i - t * nx;
-    const long long k1 = k / plane, rem = k - k1 * plane;
-    const long long base = koff ? koff[k1] : k1 * plane * Lin;
-    out[i] = in[base + rem * Lin + t];
+    const long long k1 = k / P1, r = k - k1 * P1;
+    const long long base = koff ? koff[k1] : k1 * NT * P1 * fastk::kTBL;
+    out[i] = in[base + ((t / fastk::kTBL) * P1 + r) * fastk::kTBL + (t % fastk::kTBL)];
   }
+}
+
+template <int L>
+int blk_launch(const bhcp_space_plan* sp, gdst::ArgsB a, cudaStream_t s) {
+  using namespace gdst;
+  const long long tiles = a.P * a.NT;
+  if (tiles == 0) return BHCP_OK;
+  const size_t sm = gdst::smemB_bytes<L>();
+  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_blk<L>, PlanB<L>::T, sm));
+  k_dst_blk<L><<<(unsigned)grid, PlanB<L>::T, sm, s>>>(a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk launch");
+  return BHCP_OK;
 }
 
 template <int L, int MODE>
@@ -969,6 +1012,33 @@ int gather_launch(const bhcp_space_plan* sp, gdst::Args a, cudaStream_t s) {
   return BHCP_OK;
 }
 
+template <int N, int MODE>
+int dst2_launch(const bhcp_space_plan* sp, gdst::Args2 a, cudaStream_t s) {
+  using namespace gdst;
+  const long long tiles = ((a.ni + a.ishift + 2 * Plan2<N>::S - 1) / (2 * Plan2<N>::S)) * a.no;
+  if (tiles == 0) return BHCP_OK;
+  const size_t sm = gdst::smem2_bytes<N>(MODE);
+  long long grid = std::min<long long>(tiles, resident_ctas(k_dst2<N, MODE>, Plan2<N>::T, sm));
+  k_dst2<N, MODE><<<(unsigned)grid, Plan2<N>::T, sm, s>>>(a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst2 launch");
+  return BHCP_OK;
+}
+
+bool dst2_length(int N) { return N == 256 || N == 512 || N == 1024; }
+
+template <int MODE>
+int dst2_dispatch(const bhcp_space_plan* sp, gdst::Args2 a, cudaStream_t s) {
+  a.tw = sp->twN;
+  a.sn = sp->snN;
+  a.scale = sqrt(2.0 / (sp->m + 1));
+  switch (sp->m + 1) {
+    case 256: return dst2_launch<256, MODE>(sp, a, s);
+    case 512: return dst2_launch<512, MODE>(sp, a, s);
+    case 1024: return dst2_launch<1024, MODE>(sp, a, s);
+  }
+  return fail(BHCP_ERR_INVALID, "no half-length DST kernel for this length");
+}
+
 template <int MODE>
 int gather_dispatch(const bhcp_space_plan* sp, const gdst::Args& a, cudaStream_t s) {
   switch (2 * (sp->m + 1)) {
@@ -980,46 +1050,34 @@ int gather_dispatch(const bhcp_space_plan* sp, const gdst::Args& a, cudaStream_t
   return fail(BHCP_ERR_INVALID, "no gather kernel for this length");
 }
 
-// One level pass of the fused solve on `nlev` levels. pass 0: W (mode-major,
-// line starts koff[k1] or k1*plane*Lin) -> y (level-major) with the DST along
-// the last axis; pass p >= 1: DST along axis -(p+1) in place on y.
-int level_pass(const bhcp_space_plan* sp, const double* in, const long long* koff, long long Lin, double* y,
-               long long nlev, int pass, cudaStream_t s, long long level0 = 0) {
+// One level pass of the fused solve on `nlev` levels. pass 0: W (1D:
+// level-major; else blocked, k1's first block at koff[k1] or k1*NT*P1*8) ->
+// y (level-major) with the DST along the last axis; pass p >= 1: DST along
+// axis -(p+1) in place on y.
+int level_pass(const bhcp_space_plan* sp, const double* in, const long long* koff, double* y, long long nlev,
+               int pass, cudaStream_t s) {
   const int d = sp->dim, m = sp->m;
-  const bool fast = !g_disable_fast && fast_dst_length(2 * (sp->m + 1));
-  if (pass == 0 && d == 1) {
-    // 1D: W is level-major -> contiguous rows
-    return launch_rows(sp, in, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
-  }
-  if (!fast) {
-    if (pass == 0) {
-      const long long total = nlev * sp->nx;
-      k_unpack_modes<<<(unsigned)std::min<long long>((total + 255) / 256, 65535), 256, 0, s>>>(
-          in, koff, Lin, ipow(m, d - 1), sp->nx, nlev, y);
-      if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_unpack_modes");
-      return launch_rows(sp, y, y, 0, nlev * ipow(m, d - 1), 0, nullptr, nullptr, s, Blocked(), ipow(m, d - 1));
-    }
+  const int L = 2 * (m + 1);
+  if (pass == 0 && d == 1) return launch_rows(sp, in, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
+  if (pass >= 1)
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  const long long P1 = ipow(m, d - 1);
+  if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
+    gdst::ArgsB a{};
+    a.in = in; a.out = y; a.tw = sp->dst.d.tw; a.f = sqrt(2.0 / (m + 1)) * 0.5;
+    a.koff = koff; a.NT = NT; a.P1 = P1; a.idiv = ipow(m, d - 2); a.P = P1; a.nlev = nlev;
+    switch (L) {
+      case 512: return blk_launch<512>(sp, a, s);
+      case 1024: return blk_launch<1024>(sp, a, s);
+      case 2048: return blk_launch<2048>(sp, a, s);
+    }
   }
-  gdst::Args a{};
-  a.tw = sp->dst.d.tw;
-  a.f = sqrt(2.0 / (m + 1)) * 0.5;
-  a.m = m;
-  if (pass == 0) {
-    a.in = in; a.out = y;
-    a.ni = nlev; a.no = ipow(m, d - 1);
-    a.P = ipow(m, d - 1);
-    a.idiv = ipow(m, d - 2);
-    a.Lin = Lin;
-    a.koff = koff;
-    a.ibase = 0;
-    a.ishift = (int)(level0 & 1);
-    return gather_dispatch<0>(sp, a, s);
-  }
-  a.in = y; a.out = y;
-  a.ni = ipow(m, pass); a.no = nlev * ipow(m, d - 1 - pass);
-  a.es = ipow(m, pass); a.os = ipow(m, pass + 1);
-  return gather_dispatch<1>(sp, a, s);
+  const long long total = nlev * sp->nx;
+  k_unpack_blocked<<<(unsigned)std::min<long long>((total + 255) / 256, 65535), 256, 0, s>>>(in, koff, NT, P1, sp->nx,
+                                                                                          nlev, y);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_unpack_blocked");
+  return launch_rows(sp, y, y, 0, nlev * P1, 0, nullptr, nullptr, s, Blocked(), P1);
 }
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
@@ -1051,6 +1109,8 @@ bool ensure_device_constants(int device, std::string* err) {
   {
     const char* e = getenv("BHCP_DISABLE_FAST");
     g_disable_fast = (e && e[0] == '1');
+    const char* e2 = getenv("BHCP_USE_DST2");
+    g_use_dst2 = (e2 && e2[0] == '1');
   }
   set_all_attributes();
   cudaError_t e = cudaGetLastError();
@@ -1087,6 +1147,22 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
   cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
   sp->tiles_dev = nullptr;
   sp->ntiles = 0;
+  {
+    const int N = num_cells;
+    std::vector<double2> tw(N);
+    std::vector<double> sn(N);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k = 0; k < N; ++k) {
+      const long double a = -2.0L * pi * (long double)k / (long double)N;
+      tw[k] = make_double2((double)cosl(a), (double)sinl(a));
+      sn[k] = (double)sinl(pi * (long double)k / (long double)N);
+    }
+    if (cudaMalloc(&sp->twN, sizeof(double2) * N) != cudaSuccess || cudaMalloc(&sp->snN, sizeof(double) * N) != cudaSuccess) {
+      free_fft_plan(&sp->dst); cudaFree(sp->mu1_dev); delete sp; return cuda_fail("cudaMalloc DST tables");
+    }
+    cudaMemcpy(sp->twN, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice);
+    cudaMemcpy(sp->snN, sn.data(), sizeof(double) * N, cudaMemcpyHostToDevice);
+  }
   if (dim == 2) {
     const int mt = (sp->m + 3) / 4;
     std::vector<int2> tiles;
@@ -1108,6 +1184,8 @@ void bhcp_space_plan_destroy(bhcp_space_plan* sp) {
   free_fft_plan(&sp->dst);
   cudaFree(sp->mu1_dev);
   if (sp->tiles_dev) cudaFree(sp->tiles_dev);
+  cudaFree(sp->twN);
+  cudaFree(sp->snN);
   delete sp;
 }
 
@@ -1211,7 +1289,7 @@ int bhcp_from_eigenspace(const bhcp_time_plan* tp, const void* in, int64_t batch
 size_t bhcp_pint_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
   if (!sp || !tp) return 0;
   return align256(sizeof(StatusDev)) + align256(sizeof(double) * sp->nx) +
-         align256(sizeof(double) * sp->nx * (size_t)tp->n);
+         align256(sizeof(double) * (size_t)native_w_elems(sp, tp->n));
 }
 
 void* bhcp_pint_status_ptr(const bhcp_space_plan*, const bhcp_time_plan*, void* ws) { return ws; }
@@ -1239,25 +1317,28 @@ int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   DeviceGuard g(sp->device);
   fastk::WLayout wl = native_layout(sp, k_end - k_begin, tp->n);
   if (nslabs > 0) {
+    if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "level slabs need dim >= 2");
+    const long long P1 = ipow(sp->m, sp->dim - 1);
+    if (k_begin % P1 || k_end % P1) return fail(BHCP_ERR_INVALID, "mode range must hold whole k1 planes");
     if (!slab_bounds || slab_bounds[0] != 0 || slab_bounds[nslabs] != tp->n)
       return fail(BHCP_ERR_INVALID, "slab bounds must cover [0, n_levels)");
-    wl.mode_major = 1;
-    wl.nsl = nslabs;
-    for (int i = 0; i <= nslabs; ++i) {
-      if (i > 0 && slab_bounds[i] < slab_bounds[i - 1]) return fail(BHCP_ERR_INVALID, "slab bounds not sorted");
-      wl.sl_c[i] = (int)slab_bounds[i];
+    for (int i = 1; i <= nslabs; ++i) {
+      if (slab_bounds[i] < slab_bounds[i - 1]) return fail(BHCP_ERR_INVALID, "slab bounds not sorted");
+      if (i < nslabs && slab_bounds[i] % fastk::kTBL && slab_bounds[i] != tp->n)
+        return fail(BHCP_ERR_INVALID, "slab bounds must be multiples of 8");
     }
+    wl = make_blocked(sp, k_end - k_begin, nslabs, (const long long*)slab_bounds);
   }
   return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, w_dev, wl, (StatusDev*)status_dev,
                       as_stream(stream));
 }
 
-int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, int64_t lin,
-                         double* y_dev, int64_t nlev, int pass, void* stream) {
+int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, double* y_dev,
+                         int64_t nlev, int pass, void* stream) {
   if (!sp || !in_dev || !y_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   if (pass < 0 || pass >= sp->dim) return fail(BHCP_ERR_INVALID, "pass out of range");
   DeviceGuard g(sp->device);
-  return level_pass(sp, in_dev, (const long long*)koff_dev, lin, y_dev, nlev, pass, as_stream(stream));
+  return level_pass(sp, in_dev, (const long long*)koff_dev, y_dev, nlev, pass, as_stream(stream));
 }
 
 int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t batch,
@@ -1265,7 +1346,7 @@ int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* ou
   if (!sp || !in_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   DeviceGuard g(sp->device);
   for (int p = 0; p < sp->dim; ++p) {
-    int rc = level_pass(sp, in_dev, nullptr, batch, out_dev, batch, p, as_stream(stream));
+    int rc = level_pass(sp, in_dev, nullptr, out_dev, batch, p, as_stream(stream));
     if (rc) return rc;
   }
   return BHCP_OK;
@@ -1289,19 +1370,19 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, native_layout(sp, sp->nx, tp->n), st, s);
   if (rc) return rc;
   for (int p = 0; p < sp->dim; ++p) {
-    rc = level_pass(sp, W, nullptr, tp->n, y_dev, tp->n, p, s);
+    rc = level_pass(sp, W, nullptr, y_dev, tp->n, p, s);
     if (rc) return rc;
   }
   return BHCP_OK;
 }
 
-int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, int64_t lin,
-                             double* out_dev, int64_t batch, int64_t level0, void* stream) {
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev,
+                             double* out_dev, int64_t batch, void* stream) {
   if (!sp || !in_dev || !koff_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
   DeviceGuard g(sp->device);
   for (int p = 0; p < sp->dim; ++p) {
-    int rc = level_pass(sp, in_dev, (const long long*)koff_dev, lin, out_dev, batch, p, as_stream(stream), level0);
+    int rc = level_pass(sp, in_dev, (const long long*)koff_dev, out_dev, batch, p, as_stream(stream));
     if (rc) return rc;
   }
   return BHCP_OK;

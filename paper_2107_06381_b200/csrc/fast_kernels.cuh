@@ -30,23 +30,36 @@ __device__ __forceinline__ double fast_rcp(double x) {
 }
 
 // Layout of W written by the modes kernels.
-//   mode_major = 0: level-major, W[t * w_ld + k]               (1D)
-//   mode_major = 1: mode-major per level slab s:               (2D / 3D)
-//     W[nmodes * c[s] + k * (c[s+1] - c[s]) + (t - c[s])]
-//     one slab on one GPU; one slab per destination rank in the slab-
-//     decomposed solve, so each all-to-all chunk is contiguous.
+//   mode_major = 0: level-major, W[t * w_ld + k]                      (1D)
+//   mode_major = 2: blocked, per level slab s (levels [c_s, c_{s+1}),
+//     NT_s = ceil(L_s / 8) tiles of 8 levels):                        (2D / 3D)
+//       W[off_s + ((k1 * NT_s + tl / 8) * P1 + r) * 8 + tl % 8],
+//       k = k1 * P1 + r (local mode), tl = t - c_s, off_s = nmodes * 8 * sum NT_{s'<s}
+//     so a spatial line of 8 levels is contiguous for the level pass and
+//     each destination slab is one contiguous all-to-all chunk.
+constexpr int kTBL = 8;
 struct WLayout {
   int mode_major;
   int nsl;
   int sl_c[9];
+  long long sl_off[8];
+  long long sl_nt[8];
   long long nmodes;
   long long w_ld;
+  long long P1;
   __host__ __device__ __forceinline__ long long addr(long long k, int t) const {
     if (!mode_major) return (long long)t * w_ld + k;
     int s = 0;
     while (s + 1 < nsl && t >= sl_c[s + 1]) ++s;
-    const long long Ls = sl_c[s + 1] - sl_c[s];
-    return nmodes * sl_c[s] + k * Ls + (t - sl_c[s]);
+    const long long tl = t - sl_c[s];
+    const long long k1 = k / P1, r = k - k1 * P1;
+    return sl_off[s] + ((k1 * sl_nt[s] + tl / kTBL) * P1 + r) * kTBL + (tl % kTBL);
+  }
+  __host__ __device__ __forceinline__ long long total(int n) const {
+    if (!mode_major) return (long long)n * w_ld;
+    long long nt = 0;
+    for (int s = 0; s < nsl; ++s) nt += sl_nt[s];
+    return nmodes * kTBL * nt;
   }
 };
 
@@ -354,33 +367,54 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
     };
     if (a.skip != 2) ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
   }
-  __syncthreads();
-  // store phase: W is mode-major per destination level slab:
-  // element (mode k, level t) of slab s at boff[s] + k * (c[s+1]-c[s]) + t - c[s],
-  // k = column index (SYM: global mode, else local to k_begin). Threads run
-  // along t, so each mode's time series is written contiguously.
+  // Store phase, per warp (no CTA barrier): warp q writes its own mode's
+  // time series. W layout: a.wl (mode-major slabs: contiguous runs of t;
+  // level-major: stride w_ld) -- see WLayout.
   double sre = 0.0, sim = 0.0;
-  for (int i = threadIdx.x; i < S * N; i += T) {
-    const int q = i / N, t = i - q * N;
+  {
+    const int q = warp;
     const long long cd = s_dst[q];
-    if (cd < 0) continue;
-    const double2 x = smem[q * LDW + t];
-    const double2 g = s_gi[t];
-    const double zr = x.x * g.x - x.y * g.y;
-    const double zi = x.x * g.y + x.y * g.x;
-    const double c = s_c[q];
-    const double wr = c * zr, wi = c * zi;
-    sre = fma(wr, wr, sre);
-    sim = fma(wi, wi, sim);
-    if (a.skip != 1) a.W[a.wl.addr(cd, t)] = wr;
-    if (SYM) {
-      const long long cm = s_mir[q];
-      if (cm >= 0) {
-        const double c2 = s_cm[q];
-        const double vr = c2 * zr, vi = c2 * zi;
-        sre = fma(vr, vr, sre);
-        sim = fma(vi, vi, sim);
-        if (a.skip != 1) a.W[a.wl.addr(cm, t)] = vr;
+    const long long cm = SYM ? s_mir[q] : -1;
+    const double c = s_c[q], c2 = SYM ? s_cm[q] : 0.0;
+    const double2* X = buf;
+    if (cd >= 0) {
+      const fastk::WLayout& wl = a.wl;
+      const int nsl = wl.mode_major ? wl.nsl : 1;
+      const long long cds = cm >= 0 ? cm : 0;
+      for (int sl = 0; sl < nsl; ++sl) {
+        const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+        const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : N;
+        // element t of mode k at pk + (tl / 8) * tstep + tl % 8 (blocked), or pk + t * w_ld
+        long long pd, pm, tstep;
+        if (wl.mode_major) {
+          const long long nt = wl.sl_nt[sl];
+          const long long k1d = cd / wl.P1, k1m = cds / wl.P1;
+          pd = wl.sl_off[sl] + (k1d * nt * wl.P1 + (cd - k1d * wl.P1)) * kTBL;
+          pm = wl.sl_off[sl] + (k1m * nt * wl.P1 + (cds - k1m * wl.P1)) * kTBL;
+          tstep = wl.P1 * kTBL;
+        } else {
+          pd = cd;
+          pm = cds;
+          tstep = 0;
+        }
+        for (int t = t0 + lane; t < t1; t += 32) {
+          const double2 x = X[t];
+          const double2 g = s_gi[t];
+          const double zr = x.x * g.x - x.y * g.y;
+          const double zi = x.x * g.y + x.y * g.x;
+          const double wr = c * zr, wi = c * zi;
+          sre = fma(wr, wr, sre);
+          sim = fma(wi, wi, sim);
+          const int tl = t - t0;
+          const long long off = wl.mode_major ? (long long)(tl >> 3) * tstep + (tl & 7) : (long long)t * wl.w_ld;
+          if (a.skip != 1) a.W[pd + off] = wr;
+          if (SYM && cm >= 0) {
+            const double vr = c2 * zr, vi = c2 * zi;
+            sre = fma(vr, vr, sre);
+            sim = fma(vi, vi, sim);
+            if (a.skip != 1) a.W[pm + off] = vr;
+          }
+        }
       }
     }
   }

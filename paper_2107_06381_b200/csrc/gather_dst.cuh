@@ -83,23 +83,28 @@ __global__ void __launch_bounds__(Plan<L>::T, (L <= 2048 ? 2 : 1)) k_dst_gather(
   extern __shared__ double2 smem[];
   double2* buf = smem;
   double* stage = reinterpret_cast<double*>(smem + Lay::words(S));
-  const int m = a.m;
+  constexpr int m = N - 1;
   const int shift = MODE == 0 ? a.ishift : 0;
   const long long ntile_i = (a.ni + shift + 2 * S - 1) / (2 * S);
   const long long ntiles = ntile_i * a.no;
 
   const long long es = Geo<L, MODE>::in_es(a);
+  // thread -> (lane li of the 2S lines, first element row); pointer walks the rows
+  constexpr int ROWS = T / (2 * S);
+  const int my_li = threadIdx.x % (2 * S);
+  const int my_e0 = threadIdx.x / (2 * S);
   auto issue = [&](long long tile) {
     const long long o = tile / ntile_i;
     const long long i0 = (tile - o * ntile_i) * (2 * S) - shift;
-    const double* src = a.in + Geo<L, MODE>::in_base(a, o) + i0;
-    // lane li of every element row e; rows beyond the valid level range are zero
-    const int li = threadIdx.x % (2 * S);
-    const bool ok = (i0 + li >= 0) && (i0 + li < a.ni);
-    for (int e = threadIdx.x / (2 * S); e < m; e += T / (2 * S)) {
-      double* dst = stage + e * SW + li;
-      if (ok) cp_async8(dst, src + e * es + li);
+    const bool ok = (i0 + my_li >= 0) && (i0 + my_li < a.ni);
+    const double* src = a.in + Geo<L, MODE>::in_base(a, o) + i0 + my_li + my_e0 * es;
+    const long long step = ROWS * es;
+    double* dst = stage + my_e0 * SW + my_li;
+    for (int e = my_e0; e < m; e += ROWS) {
+      if (ok) cp_async8(dst, src);
       else *dst = 0.0;
+      src += step;
+      dst += ROWS * SW;
     }
     cp_async_commit();
   };
@@ -129,25 +134,31 @@ __global__ void __launch_bounds__(Plan<L>::T, (L <= 2048 ? 2 : 1)) k_dst_gather(
     __syncthreads();
     // store: DST coefficient e of real line li = S_{e+1}; contiguous axis across threads
     if (MODE == 0) {
-      // line (level i0+li, spatial line o) is contiguous in the level-major output
-      for (int idx = threadIdx.x; idx < 2 * S * m; idx += T) {
-        const int li = idx / m, e = idx - li * m;
+      // one warp per output line (level i0+li, spatial line o): contiguous run of m
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int li = warp; li < 2 * S; li += T / 32) {
         const long long i = i0 + li;
         if (i < 0 || i >= a.ni) continue;
-        const double2 X = buf[Lay::addr(li >> 1, e + 1)];
-        const double c = (li & 1) ? a.f * X.x : -a.f * X.y;
-        a.out[((i + a.ibase) * a.P + o) * m + e] = c;
+        double* __restrict__ dst = a.out + ((i + a.ibase) * a.P + o) * m;
+        const double2* col = buf + Lay::addr(li >> 1, 0);
+        const bool odd = li & 1;
+        for (int e = lane; e < m; e += 32) {
+          const double2 X = col[(e + 1) + (e + 1) / Plan<L>::R1];
+          dst[e] = odd ? a.f * X.x : -a.f * X.y;
+        }
       }
     } else {
-      double* dst = a.out + o * a.os + i0;
-      const int li = threadIdx.x % (2 * S);
-      const bool ok = i0 + li < a.ni;
-      const double2* col = buf + Lay::addr(li >> 1, 0);
-      for (int e = threadIdx.x / (2 * S); e < m; e += T / (2 * S)) {
-        if (!ok) continue;
-        const double2 X = col[(e + 1) + (e + 1) / Plan<L>::R1];
-        const double c = (li & 1) ? a.f * X.x : -a.f * X.y;
-        dst[e * a.es + li] = c;
+      const bool ok = i0 + my_li < a.ni;
+      double* __restrict__ dst = a.out + o * a.os + i0 + my_li + my_e0 * a.es;
+      const long long step = ROWS * a.es;
+      const double2* col = buf + Lay::addr(my_li >> 1, 0);
+      const bool odd = my_li & 1;
+      if (ok) {
+        for (int e = my_e0; e < m; e += ROWS) {
+          const double2 X = col[(e + 1) + (e + 1) / Plan<L>::R1];
+          *dst = odd ? a.f * X.x : -a.f * X.y;
+          dst += step;
+        }
       }
     }
   }
@@ -156,6 +167,288 @@ __global__ void __launch_bounds__(Plan<L>::T, (L <= 2048 ? 2 : 1)) k_dst_gather(
 template <int L> constexpr size_t smem_bytes() {
   using Lay = SeqMajorPad<L, Plan<L>::R1>;
   return sizeof(double2) * Lay::words(Plan<L>::S) + sizeof(double) * (L / 2 - 1) * Stg<Plan<L>::S>::W;
+}
+
+}  // namespace gdst
+}  // namespace bhcp
+
+namespace bhcp {
+namespace gdst {
+
+// ---------------------------------------------------------------------------
+// k_dst2: the same level passes with a half-length transform.
+// DST-I of two real lines a, b (length N-1) through ONE complex FFT of length
+// N (instead of the 2N-point odd extension), the classic real-sine algorithm:
+//   u_j = sin(pi j/N)(x_j + x_{N-j}) + (x_j - x_{N-j})/2,  j = 0..N-1
+//   U = FFT_N(u^a + i u^b);  U^a_k = (U_k + conj U_{N-k})/2, U^b_k = (U_k - conj U_{N-k})/(2i)
+//   S_{2k}   = -Im U_k                      (k = 1 .. N/2-1)
+//   S_{2k+1} = sum_{i<=k} Re U_i - Re U_0/2  (k = 0 .. N/2-1, prefix sum)
+// (C_k = Re U_k = S_{2k+1} - S_{2k-1}, D_k = -Im U_k = S_{2k}). Half the FFT
+// flops and half the shared-memory traffic of the odd-extension kernel; the
+// prefix sum runs as a per-lane serial scan plus a warp shuffle scan.
+template <int N> struct Plan2;
+template <> struct Plan2<256> { static constexpr int S = 8, T = 512, MINB = 1; template <class Lay> using F = Fft<256, S, T, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
+template <> struct Plan2<512> { static constexpr int S = 4, T = 256, MINB = 2; template <class Lay> using F = Fft<512, S, T, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
+template <> struct Plan2<1024> { static constexpr int S = 4, T = 256, MINB = 2; template <class Lay> using F = Fft<1024, S, T, Lay, 16, 8, 8>; static constexpr int R1 = 16; };
+template <> struct Plan2<4096> { static constexpr int S = 1, T = 256, MINB = 2; template <class Lay> using F = Fft<4096, S, T, Lay, 16, 16, 16>; static constexpr int R1 = 16; };
+
+struct Args2 {
+  const double* in;
+  double* out;
+  const double2* tw;     // exp(-2 pi i k / N), k < N
+  const double* sn;      // sin(pi j / N), j < N
+  double scale;          // sqrt(2/N)
+  long long ni, no;
+  const long long* koff;
+  long long idiv, Lin, P, ibase;
+  int ishift;
+  long long os, es;
+};
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(Plan2<N>::T, Plan2<N>::MINB) k_dst2(Args2 a) {
+  constexpr int S = Plan2<N>::S, T = Plan2<N>::T, m = N - 1, NL = 2 * S;
+  constexpr int SW = NL + 1;        // staging row stride (doubles)
+  constexpr int OW = m + 2;         // output staging row stride (doubles), MODE 1
+  constexpr int K = (N / 2) / 32;   // k values per lane in the scan
+  static_assert(T / 32 >= NL || MODE == 0 || true, "");
+  using Lay = SeqMajorPad<N, Plan2<N>::R1>;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  double* stage = reinterpret_cast<double*>(smem + Lay::words(S));
+  double* sn = stage + m * SW;
+  double* ob = sn + N;              // MODE 1 only
+  for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
+
+  const int shift = MODE == 0 ? a.ishift : 0;
+  const long long ntile_i = (a.ni + shift + NL - 1) / NL;
+  const long long ntiles = ntile_i * a.no;
+  const long long es_in = MODE == 0 ? a.Lin : a.es;
+  constexpr int ROWS = T / NL;
+  const int my_li = threadIdx.x % NL;
+  const int my_e0 = threadIdx.x / NL;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  auto in_base = [&](long long o) -> long long {
+    if (MODE == 0) {
+      const long long k1 = o / a.idiv, r2 = o - k1 * a.idiv;
+      const long long base = a.koff ? __ldg(a.koff + k1) : k1 * a.idiv * (long long)m * a.Lin;
+      return base + r2 * (long long)m * a.Lin;
+    }
+    return o * a.os;
+  };
+  auto issue = [&](long long tile) {
+    const long long o = tile / ntile_i;
+    const long long i0 = (tile - o * ntile_i) * NL - shift;
+    const bool ok = (i0 + my_li >= 0) && (i0 + my_li < a.ni);
+    const double* src = a.in + in_base(o) + i0 + my_li + my_e0 * es_in;
+    const long long step = ROWS * es_in;
+    double* dst = stage + my_e0 * SW + my_li;
+    for (int e = my_e0; e < m; e += ROWS) {
+      if (ok) cp_async8(dst, src);
+      else *dst = 0.0;
+      src += step;
+      dst += ROWS * SW;
+    }
+    cp_async_commit();
+  };
+
+  long long tile = blockIdx.x;
+  if (tile < ntiles) issue(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const long long o = tile / ntile_i;
+    const long long i0 = (tile - o * ntile_i) * NL - shift;
+    cp_async_wait_all();
+    __syncthreads();
+    auto gen = [&](int q, int j) -> double2 {
+      if (j == 0) return make_double2(0.0, 0.0);
+      const double* p = stage + (j - 1) * SW + 2 * q;        // x_j
+      const double* r = stage + (N - j - 1) * SW + 2 * q;    // x_{N-j}
+      const double s = sn[j];
+      const double pa = p[0], pb = p[1], ra = r[0], rb = r[1];
+      return make_double2(fma(s, pa + ra, 0.5 * (pa - ra)), fma(s, pb + rb, 0.5 * (pb - rb)));
+    };
+    using F = typename Plan2<N>::template F<Lay>;
+    Stage<N, S, T, Lay, Plan2<N>::R1, 1>::first(buf, gen);
+    if (tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+    auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
+    FftTail<F>::run(buf, a.tw, sink);
+    __syncthreads();
+    // post-processing + prefix sum: one warp per real line
+    for (int li = warp; li < NL; li += T / 32) {
+      const int q = li >> 1;
+      const bool isb = li & 1;
+      double C[K], D[K];
+      double run = 0.0;
+#pragma unroll
+      for (int u = 0; u < K; ++u) {
+        const int k = lane * K + u;
+        const double2 A = buf[Lay::addr(q, k)];
+        const double2 B = buf[Lay::addr(q, (N - k) & (N - 1))];
+        // U^a = (A + conj B)/2 ; U^b = (A - conj B)/(2i)
+        double ur, ui;
+        if (!isb) { ur = 0.5 * (A.x + B.x); ui = 0.5 * (A.y - B.y); }
+        else { ur = 0.5 * (A.y + B.y); ui = -0.5 * (A.x - B.x); }
+        C[u] = ur;
+        D[u] = -ui;
+        run += ur;
+      }
+      // exclusive warp scan of the lane totals
+      double incl = run;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const double c0 = __shfl_sync(0xffffffffu, C[0], 0);
+      double acc = incl - run - 0.5 * c0;
+      const long long i = i0 + li;
+      const bool valid = i >= 0 && i < a.ni;
+      if (MODE == 0) {
+        double* __restrict__ dst = a.out + ((i + a.ibase) * a.P + o) * m;
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+          const int k = lane * K + u;
+          acc += C[u];
+          if (valid) {
+            if (k >= 1) dst[2 * k - 1] = a.scale * D[u];   // S_{2k}
+            dst[2 * k] = a.scale * acc;                    // S_{2k+1}
+          }
+        }
+      } else {
+        double* row = ob + li * OW;
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+          const int k = lane * K + u;
+          acc += C[u];
+          if (k >= 1) row[2 * k - 1] = a.scale * D[u];
+          row[2 * k] = a.scale * acc;
+        }
+      }
+    }
+    if (MODE == 1) {
+      __syncthreads();
+      const bool ok = i0 + my_li < a.ni;
+      double* __restrict__ dst = a.out + o * a.os + i0 + my_li + my_e0 * a.es;
+      const long long step = ROWS * a.es;
+      const double* row = ob + my_li * OW;
+      if (ok) {
+        for (int e = my_e0; e < m; e += ROWS) {
+          *dst = row[e];
+          dst += step;
+        }
+      }
+    }
+  }
+}
+
+template <int N> constexpr size_t smem2_bytes(int mode) {
+  using Lay = SeqMajorPad<N, Plan2<N>::R1>;
+  constexpr int NL = 2 * Plan2<N>::S;
+  return sizeof(double2) * Lay::words(Plan2<N>::S) + sizeof(double) * ((N - 1) * (NL + 1) + N) +
+         (mode == 1 ? sizeof(double) * NL * (N + 1) : 0);
+}
+
+}  // namespace gdst
+}  // namespace bhcp
+
+namespace bhcp {
+namespace gdst {
+
+// ---------------------------------------------------------------------------
+// k_dst_blk: first level pass from the BLOCKED W layout.
+// The modes kernel stores W in blocks of TB = 8 consecutive levels:
+//   block (k1, level tile tt) = P1 x 8 doubles, mode (k1, rr) at rr*8,
+// so one tile of this kernel -- one spatial line (k1, r2) for 8 levels -- is
+// a single contiguous m*8*8-byte run: it is staged with 16-byte cp.async
+// (coalesced, long DRAM bursts) while the previous tile is transformed.
+constexpr int kTB = 8;
+
+template <int L> struct PlanB;
+template <> struct PlanB<512> { static constexpr int T = 256, R1 = 8; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };
+template <> struct PlanB<1024> { static constexpr int T = 256, R1 = 16; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
+template <> struct PlanB<2048> { static constexpr int T = 512, R1 = 16; template <class Lay> using F = Fft<2048, 4, T, Lay, 16, 16, 8>; };
+
+struct ArgsB {
+  const double* in;       // blocked W (receive buffer on a rank)
+  double* out;            // level-major y (nlev, n_space)
+  const double2* tw;
+  double f;               // sqrt(2/N)/2
+  const long long* koff;  // start of k1's first block, null: k1 * NT * P1 * TB
+  long long NT;           // level tiles in this W (slab)
+  long long P1;           // modes per k1 value (m^(d-1))
+  long long idiv;         // m^(d-2): lines per k1 value
+  long long P;            // lines per level (m^(d-1))
+  long long nlev;         // valid levels
+};
+
+template <int L>
+__global__ void __launch_bounds__(PlanB<L>::T, (L <= 1024 ? 2 : 1)) k_dst_blk(ArgsB a) {
+  constexpr int S = 4, T = PlanB<L>::T, N = L / 2, m = N - 1;
+  constexpr int RUN = m * kTB;        // doubles per tile (contiguous)
+  using Lay = Interleaved<S, PlanB<L>::R1>;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  double* stage = reinterpret_cast<double*>(smem + Lay::words(L));
+  const long long ntiles = a.P * a.NT;
+  auto src_of = [&](long long tile) -> const double* {
+    const long long o = tile / a.NT, tt = tile - o * a.NT;
+    const long long k1 = o / a.idiv, r2 = o - k1 * a.idiv;
+    const long long kb = a.koff ? __ldg(a.koff + k1) : k1 * a.NT * a.P1 * kTB;
+    return a.in + kb + tt * a.P1 * kTB + r2 * (long long)m * kTB;
+  };
+  auto issue = [&](long long tile) {
+    const double2* src = reinterpret_cast<const double2*>(src_of(tile));
+    double2* dst = reinterpret_cast<double2*>(stage);
+    for (int i = threadIdx.x; i < RUN / 2; i += T) {
+      const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + i));
+    }
+    cp_async_commit();
+  };
+  long long tile = blockIdx.x;
+  if (tile < ntiles) issue(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const long long o = tile / a.NT, tt = tile - o * a.NT;
+    cp_async_wait_all();
+    __syncthreads();
+    // staged tile: element e of level tl at stage[e*8 + tl]; sequence q = levels (2q, 2q+1).
+    // Levels past nlev (padding of the last tile) are never read: they hold
+    // no data and must not leak into the partner level through the FFT.
+    const long long tvalid = a.nlev - tt * kTB;
+    auto gen = [&](int q, int idx) -> double2 {
+      if (idx == 0 || idx == N) return make_double2(0.0, 0.0);
+      const bool neg = idx > N;
+      const int e = neg ? (L - idx - 1) : (idx - 1);
+      double2 x = *reinterpret_cast<const double2*>(stage + e * kTB + 2 * q);
+      if (2 * q >= tvalid) x.x = 0.0;
+      if (2 * q + 1 >= tvalid) x.y = 0.0;
+      return neg ? make_double2(-x.x, -x.y) : x;
+    };
+    using Ff = typename PlanB<L>::template F<Lay>;
+    Stage<L, S, T, Lay, PlanB<L>::R1, 1>::first(buf, gen);
+    if (tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+    auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
+    FftTail<Ff>::run(buf, a.tw, sink);
+    __syncthreads();
+    // one warp per output line (level t0 + li): contiguous run of m in y
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int li = warp; li < kTB; li += T / 32) {
+      const long long t = tt * kTB + li;
+      if (t >= a.nlev) continue;
+      double* __restrict__ dst = a.out + (t * a.P + o) * m;
+      const bool odd = li & 1;
+      for (int e = lane; e < m; e += 32) {
+        const double2 X = buf[Lay::addr(li >> 1, e + 1)];
+        dst[e] = odd ? a.f * X.x : -a.f * X.y;
+      }
+    }
+  }
+}
+
+template <int L> constexpr size_t smemB_bytes() {
+  using Lay = Interleaved<4, PlanB<L>::R1>;
+  return sizeof(double2) * Lay::words(L) + sizeof(double) * (L / 2 - 1) * kTB;
 }
 
 }  // namespace gdst

@@ -129,6 +129,18 @@ template <> struct Cod<9> {
 template <int S, int P = 1 << 30> struct Interleaved {
   static constexpr int words(int L) { return L * S + L / P + 1; }
   static __device__ __forceinline__ int addr(int q, int idx) { return idx * S + q + idx / P; }
+  // addr(q, j + r * STRIDE) with the per-r part folded to a compile-time offset
+  template <int STRIDE>
+  static __device__ __forceinline__ int addr_r(int q, int j, int r) {
+    if constexpr (STRIDE % P == 0) return addr(q, j) + r * (STRIDE * S + STRIDE / P);
+    else return addr(q, j + r * STRIDE);
+  }
+  // addr(q, base + r), r < R, base a multiple of R (first-stage stores)
+  template <int R>
+  static __device__ __forceinline__ int addr_first(int q, int base, int r) {
+    if constexpr (P % R == 0) return addr(q, base) + r * S;
+    else return addr(q, base + r);
+  }
   // butterfly b -> (q, j): q fastest
   static __device__ __forceinline__ void split(int b, int nb, int& q, int& j) { q = b % S; j = b / S; }
 };
@@ -137,6 +149,16 @@ template <int L, int P> struct SeqMajorPad {
   static constexpr int LD = L + L / P + 1;
   static constexpr int words(int S) { return LD * S; }
   static __device__ __forceinline__ int addr(int q, int idx) { return q * LD + idx + idx / P; }
+  template <int STRIDE>
+  static __device__ __forceinline__ int addr_r(int q, int j, int r) {
+    if constexpr (STRIDE % P == 0) return addr(q, j) + r * (STRIDE + STRIDE / P);
+    else return addr(q, j + r * STRIDE);
+  }
+  template <int R>
+  static __device__ __forceinline__ int addr_first(int q, int base, int r) {
+    if constexpr (P % R == 0) return addr(q, base) + r;
+    else return addr(q, base + r);
+  }
   static __device__ __forceinline__ void split(int b, int nb, int& q, int& j) { q = b / nb; j = b - q * nb; }
 };
 
@@ -175,7 +197,7 @@ struct Stage {
         Lay::split(b, L / R, q, j);
         qq[i] = q; jj[i] = j;
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[i][r] = buf[Lay::addr(q, j + r * (L / R))];
+        for (int r = 0; r < R; ++r) v[i][r] = buf[Lay::template addr_r<L / R>(q, j, r)];
         if (Ns > 1) apply_twiddles<R>(v[i], tw[(j % Ns) * TWS]);
         Cod<R>::run(v[i]);
       }
@@ -189,7 +211,7 @@ struct Stage {
         const int k = j % Ns;
         const int base = (j - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[Lay::addr(q, base + r * Ns)] = v[i][r];
+        for (int r = 0; r < R; ++r) buf[Lay::template addr_r<Ns>(q, base, r)] = v[i][r];
       }
     }
     __syncthreads();
@@ -211,7 +233,7 @@ struct Stage {
         for (int r = 0; r < R; ++r) v[i][r] = gen(q, j + r * (L / R));
         Cod<R>::run(v[i]);
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[Lay::addr(q, j * R + r)] = v[i][r];
+        for (int r = 0; r < R; ++r) buf[Lay::template addr_first<R>(q, j * R, r)] = v[i][r];
       }
     }
     __syncthreads();
@@ -229,7 +251,7 @@ struct Stage {
         Lay::split(b, L / R, q, j);
         double2 v[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[r] = buf[Lay::addr(q, j + r * (L / R))];
+        for (int r = 0; r < R; ++r) v[r] = buf[Lay::template addr_r<L / R>(q, j, r)];
         if (Ns > 1) apply_twiddles<R>(v, tw[j * TWS]);
         Cod<R>::run(v);
         // k = j (j < Ns), outputs at j + r*Ns

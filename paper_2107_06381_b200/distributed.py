@@ -30,6 +30,9 @@ from typing import List, Tuple
 import numpy as np
 
 
+TB = 8  # levels per W tile (fastk::kTBL)
+
+
 def partition(total: int, parts: int) -> List[Tuple[int, int]]:
     """Balanced contiguous split of range(total) into `parts` (sizes differ by <= 1)."""
     base, extra = divmod(total, parts)
@@ -52,11 +55,12 @@ class SlabLayout:
         if self.dim < 2:
             raise ValueError("slab decomposition needs dim >= 2 (1D runs stay on one GPU)")
         self.k1 = partition(self.m, self.world)
-        # level slabs start at even levels: the level passes pack levels
-        # (2u, 2u+1) into one complex FFT, so no pair straddles two ranks and
-        # every rank count gives the single-GPU result bit for bit
-        pairs = partition((self.n + 1) // 2, self.world)
-        self.lev = [(min(2 * a, self.n), min(2 * b, self.n)) for a, b in pairs]
+        # level slabs start at multiples of 8: W is stored in tiles of 8
+        # levels and the level pass packs levels (2u, 2u+1) into one complex
+        # FFT, so no tile or pair straddles two ranks and every rank count
+        # gives the single-GPU result bit for bit
+        tiles = partition((self.n + TB - 1) // TB, self.world)
+        self.lev = [(min(TB * a, self.n), min(TB * b, self.n)) for a, b in tiles]
         self.plane = self.m ** (self.dim - 1)   # modes per k1 value
 
     @property
@@ -75,33 +79,35 @@ class SlabLayout:
         c, d = self.lev[r]
         return d - c
 
+    def tiles(self, r: int) -> int:
+        return (self.levels(r) + TB - 1) // TB
+
     def send_splits(self, r: int) -> List[int]:
-        """Rank r sends rows lev[q] of its W_r (n, S_r) to rank q."""
-        return [self.levels(q) * self.slab_modes(r) for q in range(self.world)]
+        """Rank r sends the blocked chunk of level slab q of its W_r to rank q."""
+        return [self.tiles(q) * TB * self.slab_modes(r) for q in range(self.world)]
 
     def recv_splits(self, r: int) -> List[int]:
-        return [self.levels(r) * self.slab_modes(p) for p in range(self.world)]
+        return [self.tiles(r) * TB * self.slab_modes(p) for p in range(self.world)]
 
     def slab_bounds(self) -> np.ndarray:
         """Level-slab boundaries (the W chunking of bhcp_pint_modes)."""
         return np.array([c for c, _ in self.lev] + [self.n], dtype=np.int64)
 
-    def block_tables(self, r: int) -> Tuple[np.ndarray, int]:
-        """koff and level stride of bhcp_pint_levels_blocked for receiver r.
-
-        The receive buffer holds, for every sender p, the mode-major block
-        (S_p modes x L_r levels); mode (k1, rest) of level t (local) is at
-        koff[k1] + rest * L_r + t."""
-        Lr = self.levels(r)
+    def block_tables(self, r: int) -> np.ndarray:
+        """koff of bhcp_pint_levels_blocked for receiver r: the receive buffer
+        holds, for every sender p, its blocked chunk (S_p modes x NT_r tiles of
+        8 levels); mode (k1, rest) of local level t is at
+        koff[k1] + ((t // 8) * plane + rest) * 8 + t % 8."""
+        nt = self.tiles(r)
         koff = np.empty(self.m, dtype=np.int64)
         offset = 0
         recv = self.recv_splits(r)
         for p in range(self.world):
             a, b = self.k1[p]
             for k1 in range(a, b):
-                koff[k1] = offset + (k1 - a) * self.plane * Lr
+                koff[k1] = offset + (k1 - a) * nt * self.plane * TB
             offset += recv[p]
-        return koff, Lr
+        return koff
 
 
 # ---------------------------------------------------------------- orchestration
@@ -109,8 +115,8 @@ class SlabLayout:
 def sharded_solve(ops, comm, layout: SlabLayout, rank: int, events=None):
     """Run one slab-decomposed solve on this rank; returns (y_local, (c, d)).
 
-    ops.modes(layout, rank)            -> W_r, mode-major per destination slab (flat)
-    ops.levels_blocked(recv, koff, lin, L, level0) -> y (L, n_space)
+    ops.modes(layout, rank)            -> W_r, blocked per destination slab (flat)
+    ops.levels_blocked(recv, koff, L)  -> y (L, n_space)
     comm.all_to_all(send, send_splits, recv_splits) -> recv buffer (flat)
     """
     if events:
@@ -121,8 +127,8 @@ def sharded_solve(ops, comm, layout: SlabLayout, rank: int, events=None):
     recv = comm.all_to_all(W.reshape(-1), layout.send_splits(rank), layout.recv_splits(rank))
     if events:
         events[2].record()
-    koff, lin = ops.tables(layout, rank)
-    y = ops.levels_blocked(recv, koff, lin, layout.levels(rank), layout.lev[rank][0])
+    koff = ops.tables(layout, rank)
+    y = ops.levels_blocked(recv, koff, layout.levels(rank))
     if events:
         events[3].record()
     return y, layout.lev[rank]
@@ -204,8 +210,9 @@ class DeviceOps:
         torch, p = self.torch, self.plans
         kb, ke = layout.mode_range(rank)
         S = ke - kb
-        if self._W is None or self._W.numel() != S * self.n:
-            self._W = torch.empty(S * self.n, dtype=torch.float64, device=self.g.device)
+        size = sum(layout.tiles(q) for q in range(layout.world)) * TB * S
+        if self._W is None or self._W.numel() != size:
+            self._W = torch.empty(size, dtype=torch.float64, device=self.g.device)
         bounds = layout.slab_bounds()
         self.prepare()
         self._lib.check(self.lib.bhcp_pint_modes(self.plan.sp.handle, self.plan.tp.handle, p.ptr(self.ghat), kb, ke,
@@ -217,17 +224,16 @@ class DeviceOps:
     def tables(self, layout: SlabLayout, rank: int):
         key = (layout.world, rank)
         if key not in self._tables:
-            koff, lin = layout.block_tables(rank)
-            self._tables[key] = (self.torch.from_numpy(koff).to(self.g.device), lin)
+            self._tables[key] = self.torch.from_numpy(layout.block_tables(rank)).to(self.g.device)
         return self._tables[key]
 
-    def levels_blocked(self, recv, koff, lin: int, L: int, level0: int = 0):
+    def levels_blocked(self, recv, koff, L: int):
         torch, p = self.torch, self.plans
         if self._y is None or self._y.shape != (L, self.nx):
             self._y = torch.empty((L, self.nx), dtype=torch.float64, device=self.g.device)
         if L > 0:
-            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), p.ptr(koff), lin,
-                                                              p.ptr(self._y), L, level0, p.stream_handle()),
+            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), p.ptr(koff),
+                                                              p.ptr(self._y), L, p.stream_handle()),
                             "levels_blocked")
         return self._y
 

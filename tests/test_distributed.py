@@ -32,17 +32,19 @@ def test_partition_balanced_and_uneven():
 @pytest.mark.parametrize("dim,m,n,world", [(2, 7, 9, 2), (2, 5, 6, 3), (3, 4, 5, 2), (2, 3, 4, 4)])
 def test_layout_tables_address_every_line_once(dim, m, n, world):
     L = D.SlabLayout(dim, m, n, world)
+    tb = D.TB
     for r in range(world):
-        koff, lin = L.block_tables(r)
-        assert lin == L.levels(r)
+        koff = L.block_tables(r)
         total = sum(L.recv_splits(r))
         seen = np.zeros(total, dtype=int)
         for t in range(L.levels(r)):
             for k1 in range(m):
                 for rest in range(m ** (dim - 1)):
-                    seen[koff[k1] + rest * lin + t] += 1
-        assert (seen == 1).all()
-    assert sum(sum(L.send_splits(r)) for r in range(world)) == n * m**dim
+                    seen[koff[k1] + ((t // tb) * m ** (dim - 1) + rest) * tb + t % tb] += 1
+        assert seen.sum() == L.levels(r) * m**dim
+        assert total == 0 or seen.max() == 1
+    assert sum(L.levels(r) for r in range(world)) == n
+    assert all(c % tb == 0 or c == n for c, _ in L.lev)
 
 
 def test_layout_rejects_1d():
@@ -59,27 +61,35 @@ class NumpyOps:
         self.sums = (0.0, 0.0)
 
     def modes(self, layout, rank):
-        """W_r mode-major per destination level slab (bhcp_pint_modes layout)."""
+        """W_r blocked per destination level slab (bhcp_pint_modes layout)."""
         import torch
         kb, ke = layout.mode_range(rank)
         W, sre, sim = O.fused_pass_a(*self.args, kb, ke)   # (n, S) level-major
         self.sums = (sre, sim)
-        chunks = [np.ascontiguousarray(W[c:d].T).ravel() for c, d in layout.lev]
+        tb, plane = D.TB, layout.plane
+        nk1 = (ke - kb) // plane
+        chunks = []
+        for c, d in layout.lev:
+            nt = (d - c + tb - 1) // tb
+            blk = np.zeros((nk1, nt, plane, tb))
+            for t in range(c, d):
+                blk[:, (t - c) // tb, :, (t - c) % tb] = W[t].reshape(nk1, plane)
+            chunks.append(blk.ravel())
         return torch.from_numpy(np.concatenate(chunks))
 
     def tables(self, layout, rank):
         return layout.block_tables(rank)
 
-    def levels_blocked(self, recv, koff, lin, L, level0=0):
+    def levels_blocked(self, recv, koff, L):
         import torch
         recv = recv.numpy()
-        m, d = self.m, self.dim
+        m, d, tb = self.m, self.dim, D.TB
         plane = m ** (d - 1)
         F = np.zeros((L, m**d))
-        for k1 in range(m):
-            for rest in range(plane):
-                s = koff[k1] + rest * lin
-                F[:, k1 * plane + rest] = recv[s:s + L]
+        for t in range(L):
+            for k1 in range(m):
+                s = koff[k1] + (t // tb) * plane * tb + t % tb
+                F[t, k1 * plane:(k1 + 1) * plane] = recv[s:s + plane * tb:tb]
         return torch.from_numpy(O.fused_pass_b(F, d, m))
 
 
@@ -151,8 +161,8 @@ def emulate(system, world):
             off = sum(layout.send_splits(r)[:q])
             chunks.append(Ws[r][off:off + layout.send_splits(r)[q]])
         recv = torch.cat(chunks)
-        koff, lin = ops.tables(layout, q)
-        ys.append(ops.levels_blocked(recv, koff, lin, layout.levels(q), layout.lev[q][0]).clone())
+        koff = ops.tables(layout, q)
+        ys.append(ops.levels_blocked(recv, koff, layout.levels(q)).clone())
     return torch.cat(ys).cpu().numpy()
 
 
