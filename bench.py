@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=CONFIG_NAME)
-    p.add_argument("--cpu-fraction", type=float, default=0.1,
+    p.add_argument("--cpu-fraction", type=float, default=1.0,
                    help="fraction of every per-unit operation in the CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -139,7 +139,7 @@ def run_reference(args, rank, world):
     w = workloads.make(args.config)
     kind, alpha = w.kinds[0], w.alphas[0]
     cores = os.cpu_count() or 1
-    frac = args.cpu_fraction
+    frac = min(args.cpu_fraction, 0.1)  # each reference step: a 10% sample (~0.6 s on 16 threads)
     for _ in range(args.warmup):
         cpu_sample(w, kind, alpha, frac / 4, cores)
     total_dof, total_s = 0.0, 0.0
@@ -255,10 +255,15 @@ def main():
         alg_bytes = [16.0 * nx, 8.0 * dof + 8.0 * nx] + [16.0 * dof] * w.dim
         hbm, peak_kind = peaks()
         achieved = alg_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
+        # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
         traffic = None
         tfile = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
         if tfile.exists():
-            traffic = json.loads(tfile.read_text()).get(names[dom].split()[0] if dom != 1 else "k_modes")
+            tmap = json.loads(tfile.read_text())
+            short = names[dom].split()[0]
+            for key, val in tmap.items():
+                if key.split("::")[-1] == short:
+                    traffic = val
         ms_per_step = total_ms / args.steps
         value = dof / (ms_per_step * 1e-3)
 

@@ -1,0 +1,78 @@
+"""Summarise ncu captures into profiles/ (run here, on the CPU box).
+
+usage: python tools/ncu_summary.py <full.ncu-rep> <launches.csv> <out_prefix>
+writes <out_prefix>_ncu_full.csv (selected raw metrics per captured kernel),
+<out_prefix>_launches.csv (copy) and <out_prefix>_summary.md, and updates
+profiles/ncu_traffic_c2.json (DRAM bytes per launch per kernel, used by bench.py).
+"""
+import csv
+import io
+import json
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units, data = rows[0], rows[1], rows[2:]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
+idx = {w: hdr.index(w) for w in want if w in hdr}
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+out_rows = []
+traffic = {}
+for r in data:
+    d = {}
+    for w, i in idx.items():
+        v, u = r[i], units[i]
+        if w.startswith("dram__bytes"):
+            v = float(v.replace(",", "")) * scale.get(u, 1)
+        d[w] = v
+    d["time_unit"] = units[idx["gpu__time_duration.sum"]]
+    out_rows.append(d)
+    name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
+    traffic.setdefault(name, d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])
+with open(f"{prefix}_ncu_full.csv", "w", newline="") as f:
+    w = csv.DictWriter(f, fieldnames=list(out_rows[0].keys()))
+    w.writeheader()
+    w.writerows(out_rows)
+shutil.copy(launches, f"{prefix}_launches.csv")
+# launch list shares
+lrows = list(csv.reader(open(launches)))
+h = next(i for i, r in enumerate(lrows) if "Kernel Name" in r)
+lh = lrows[h]
+ki, vi = lh.index("Kernel Name"), lh.index("Metric Value")
+agg = {}
+for r in lrows[h + 1:]:
+    if len(r) <= vi:
+        continue
+    name = r[ki].split("(")[0].replace("void ", "")
+    agg.setdefault(name, []).append(float(r[vi].replace(",", "")))
+tot = sum(sum(v) for v in agg.values())
+lines = [f"# ncu summary ({Path(prefix).name})", "", "## Launch list (gpu__time_duration.sum, cold-cache, serialised)", "",
+         "| kernel | launches | total us | share |", "|---|---|---|---|"]
+for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+    lines.append(f"| {name} | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/tot*100:.1f}% |")
+lines += ["", "## --set full capture (one launch each)", "",
+          "| kernel | time | DRAM read | DRAM write | DRAM % | SM % | L1 % | FP64 pipe % | IPC | warps % | regs |",
+          "|---|---|---|---|---|---|---|---|---|---|---|"]
+for d in out_rows:
+    lines.append(f"| {d['Kernel Name'][:48]} | {d['gpu__time_duration.sum']} {d['time_unit']} | "
+                 f"{d['dram__bytes_read.sum']/1e9:.3f} GB | {d['dram__bytes_write.sum']/1e9:.3f} GB | "
+                 f"{d.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed','')} | "
+                 f"{d.get('sm__throughput.avg.pct_of_peak_sustained_elapsed','')} | "
+                 f"{d.get('l1tex__throughput.avg.pct_of_peak_sustained_active','')} | "
+                 f"{d.get('sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active','')} | "
+                 f"{d.get('sm__inst_executed.avg.per_cycle_active','')} | "
+                 f"{d.get('sm__warps_active.avg.pct_of_peak_sustained_active','')} | "
+                 f"{d.get('launch__registers_per_thread','')} |")
+Path(f"{prefix}_summary.md").write_text("\n".join(lines) + "\n")
+tf = Path("profiles/ncu_traffic_c2.json")
+tf.write_text(json.dumps(traffic, indent=1) + "\n")
+print("\n".join(lines))
