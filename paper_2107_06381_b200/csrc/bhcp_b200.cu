@@ -659,6 +659,9 @@ void set_all_attributes() {
   allow_smem(fastk::k_dst_cols_fast<LL, 1>);
   BHCP_FATTR(512) BHCP_FATTR(1024) BHCP_FATTR(2048) BHCP_FATTR(8192)
 #undef BHCP_FATTR
+  allow_smem(gdst::k_dst_blk2<256>);
+  allow_smem(gdst::k_dst_blk2<512>);
+  allow_smem(gdst::k_dst_blk2<1024>);
   allow_smem(gdst::k_dst_blk<512>);
   allow_smem(gdst::k_dst_blk<1024>);
   allow_smem(gdst::k_dst_blk<2048>);
@@ -988,6 +991,19 @@ __global__ void k_unpack_blocked(const double* __restrict__ in, const long long*
   }
 }
 
+template <int N>
+int blk2_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
+  using namespace gdst;
+  const long long tiles = a.P * a.NT;
+  if (tiles == 0) return BHCP_OK;
+  const size_t sm = gdst::smemB2_bytes<N>();
+  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_blk2<N>, PlanB2<N>::T, sm));
+  k_dst_blk2<N><<<(unsigned)grid, PlanB2<N>::T, sm, s>>>(a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk2 launch");
+  return BHCP_OK;
+}
+bool g_blk_odd = false;  // BHCP_BLK_ODD=1: odd-extension first level pass (k_dst_blk)
+
 template <int L>
 int blk_launch(const bhcp_space_plan* sp, gdst::ArgsB a, cudaStream_t s) {
   using namespace gdst;
@@ -1063,6 +1079,16 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
   const long long P1 = ipow(m, d - 1);
+  if (!g_disable_fast && !g_blk_odd && (L == 512 || L == 1024 || L == 2048)) {
+    gdst::ArgsB2 b{};
+    b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
+    b.koff = koff; b.NT = NT; b.P1 = P1; b.idiv = ipow(m, d - 2); b.P = P1; b.nlev = nlev;
+    switch (L) {
+      case 512: return blk2_launch<256>(sp, b, s);
+      case 1024: return blk2_launch<512>(sp, b, s);
+      case 2048: return blk2_launch<1024>(sp, b, s);
+    }
+  }
   if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
     gdst::ArgsB a{};
     a.in = in; a.out = y; a.tw = sp->dst.d.tw; a.f = sqrt(2.0 / (m + 1)) * 0.5;
@@ -1111,6 +1137,8 @@ bool ensure_device_constants(int device, std::string* err) {
     g_disable_fast = (e && e[0] == '1');
     const char* e2 = getenv("BHCP_USE_DST2");
     g_use_dst2 = (e2 && e2[0] == '1');
+    const char* e3 = getenv("BHCP_BLK_ODD");
+    g_blk_odd = (e3 && e3[0] == '1');
   }
   set_all_attributes();
   cudaError_t e = cudaGetLastError();

@@ -78,7 +78,7 @@ template <> struct RowsShape<2048> { static constexpr int S = 2, T = 256, MINB =
 template <> struct RowsShape<8192> { static constexpr int S = 1, T = 512, MINB = 1; };
 template <int L> struct ColsShape;
 template <> struct ColsShape<512> { static constexpr int S = 8, T = 256, MINB = 2; };
-template <> struct ColsShape<1024> { static constexpr int S = 4, T = 256, MINB = 2; };
+template <> struct ColsShape<1024> { static constexpr int S = 8, T = 512, MINB = 1; };
 template <> struct ColsShape<2048> { static constexpr int S = 4, T = 512, MINB = 1; };
 template <> struct ColsShape<8192> { static constexpr int S = 1, T = 512, MINB = 1; };
 

@@ -1,0 +1,59 @@
+"""Time the fused device solve on every BASELINE config and check sampled
+levels against the closed-form oracle (usage: python tools/run_configs.py [c1 c3 ...])."""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+import paper_2107_06381_b200 as B
+from oracle import bhcp_oracle as O
+from paper_2107_06381_b200 import workloads
+
+names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+out = {}
+for name in names:
+    t0 = time.time()
+    w = workloads.make(name)
+    gen_s = time.time() - t0
+    grid = B.build_grid(w.dim, w.length, w.num_cells)
+    tg = B.TimeGrid(w.horizon, w.num_steps)
+    alphas = [w.alphas[0]] if name != "c5" else [w.alphas[0], w.alphas[32], w.alphas[-1]]
+    res = {}
+    for kind in w.kinds:
+        for alpha in alphas:
+            system = B.assemble(B.MethodKind(kind), alpha, grid, tg, w.g_delta)
+            plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
+            g = torch.from_numpy(w.g_delta).cuda()
+            div = system.method.condition_divisor(tg.tau)
+            y = plan.solve_device(g, div)
+            torch.cuda.synchronize()
+            plan.check_status()
+            reps = 3 if w.dof > 1e9 else 10
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                plan.solve_device(g, div, out=y)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            plan.check_status()
+            levels = np.unique(np.linspace(0, w.num_steps, 5).astype(int))
+            ref = O.spectral_oracle(kind, alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps, w.g_delta,
+                                    levels=levels)
+            yl = y[torch.from_numpy(levels).cuda()].cpu().numpy()
+            err = float(np.linalg.norm(yl - ref) / np.linalg.norm(ref))
+            tol = O.parity_tolerance(tg.n_levels, system.omega)
+            eh = workloads.l2_error(yl[0], w.z0, grid.h, w.dim)
+            eh_ref = workloads.l2_error(ref[0], w.z0, grid.h, w.dim)
+            res[f"{kind} alpha={alpha:.3g}"] = {"ms": ms, "GDOF_s": w.dof / ms / 1e6, "rel_l2_sampled_levels": err,
+                                               "tol": tol, "ok": bool(err <= tol), "e_h": eh, "e_h_oracle": eh_ref}
+            del y, plan
+            torch.cuda.empty_cache()
+    out[name] = {"dof": w.dof, "gen_s": gen_s, "results": res}
+    print(name, json.dumps(out[name]), flush=True)
+Path("gpurun_out").mkdir(exist_ok=True)
+Path("gpurun_out/configs.json").write_text(json.dumps(out, indent=1))
