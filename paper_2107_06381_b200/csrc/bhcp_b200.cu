@@ -560,6 +560,22 @@ __global__ void k_scale(const double* __restrict__ in, double s, long long n, do
     out[i] = in[i] * s;
 }
 
+// out[c * rows + r] = in[r * ld + c], r < rows, c < cols (32x32 tiles through shared memory)
+__global__ void k_transpose_ld(const double* __restrict__ in, long long ld, double* __restrict__ out, long long rows,
+                               long long cols) {
+  __shared__ double tile[32][33];
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = in[r * ld + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
 template <typename E>
 __global__ void k_transpose(const E* __restrict__ in, E* __restrict__ out, long long rows, long long cols) {
   __shared__ E tile[32][33];
@@ -589,12 +605,15 @@ struct bhcp_space_plan {
   long long ntiles;
   double2* twN;          // exp(-2 pi i k / N), N = m + 1 (half-length DST kernels)
   double* snN;           // sin(pi j / N)
+  int4* seg_tiles[9];    // symmetric segment tiles for the Bluestein modes kernel, by segment length S
+  long long seg_count[9];
 };
 
 struct bhcp_time_plan {
   int device, n;
   double2* tables;       // gamma | gamma_inv | shifts  (3n double2)
   FftPlanHost fft;       // FFT of length n
+  double2* blue;         // n = 2^p + 1 fast path: tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1)
 };
 
 namespace {
@@ -659,6 +678,12 @@ void set_all_attributes() {
   allow_smem(fastk::k_dst_cols_fast<LL, 1>);
   BHCP_FATTR(512) BHCP_FATTR(1024) BHCP_FATTR(2048) BHCP_FATTR(8192)
 #undef BHCP_FATTR
+  allow_smem(fastk::k_modes_blue<257, false>);
+  allow_smem(fastk::k_modes_blue<257, true>);
+  allow_smem(fastk::k_modes_blue<1025, false>);
+  allow_smem(fastk::k_modes_blue<1025, true>);
+  allow_smem(fastk::k_modes_blue<4097, false>);
+  allow_smem(fastk::k_modes_blue<4097, true>);
   allow_smem(gdst::k_dst_blk2<256>);
   allow_smem(gdst::k_dst_blk2<512>);
   allow_smem(gdst::k_dst_blk2<1024>);
@@ -896,12 +921,74 @@ int launch_time(const bhcp_time_plan* tp, int mode, const double* in, int in_cpl
   return BHCP_OK;
 }
 
+std::mutex g_tile_mutex;
+
+// Symmetric work list of the Bluestein modes kernel: 2D tiles (k1, k2a) cover
+// k2 in [k2a, k2a+S) with k2 >= k1; 3D tiles (k1, k2, k3a) with k1 <= k2 cover
+// k3 in [k3a, k3a+S). Each computed mode also writes its (k1 <-> k2) mirror.
+const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
+  auto* sp = const_cast<bhcp_space_plan*>(sp_c);
+  std::lock_guard<std::mutex> lk(g_tile_mutex);
+  if (!sp->seg_tiles[S]) {
+    std::vector<int4> t;
+    const int m = sp->m;
+    if (sp->dim == 2) {
+      for (int k1 = 0; k1 < m; ++k1)
+        for (int k2a = k1 - k1 % S; k2a < m; k2a += S) t.push_back(make_int4(k1, k2a, 0, 0));
+    } else {
+      for (int k1 = 0; k1 < m; ++k1)
+        for (int k2 = k1; k2 < m; ++k2)
+          for (int k3a = 0; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
+    }
+    if (cudaMalloc(&sp->seg_tiles[S], sizeof(int4) * t.size()) != cudaSuccess) return nullptr;
+    cudaMemcpy(sp->seg_tiles[S], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice);
+    sp->seg_count[S] = (long long)t.size();
+  }
+  *count = sp->seg_count[S];
+  return sp->seg_tiles[S];
+}
+
+template <int NL>
+int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
+               long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
+               cudaStream_t s) {
+  using namespace fastk;
+  using Pl = BluePlan<NL>;
+  BlueModesArgs a{};
+  a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev; a.ghat = ghat;
+  a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
+  a.st = st; a.wl = wl;
+  const int L = Pl::L;
+  a.bt.tw = tp->blue; a.bt.chirp = tp->blue + L; a.bt.bhat = tp->blue + L + NL; a.bt.wM = tp->blue + 2 * L + NL;
+  const size_t sm = blue_smem<NL>();
+  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  if (sym) {
+    long long cnt = 0;
+    a.tiles = seg_tiles(sp, Pl::S, &cnt);
+    if (!a.tiles) return cuda_fail("seg tiles");
+    a.ntiles = cnt;
+    k_modes_blue<NL, true><<<(unsigned)cnt, Pl::T, sm, s>>>(a);
+  } else {
+    const long long work = (a.k_count + Pl::S - 1) / Pl::S;
+    k_modes_blue<NL, false><<<(unsigned)work, Pl::T, sm, s>>>(a);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_blue launch");
+  return BHCP_OK;
+}
+
 int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
                  long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
                  cudaStream_t s) {
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
+  if (!g_disable_fast && tp->blue) {
+    switch (tp->n) {
+      case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+      case 1025: return blue_modes<1025>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+      case 4097: return blue_modes<4097>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+    }
+  }
   if (!g_disable_fast && tp->n == 513) {
     using namespace fastk;
     FastModesArgs f{};
@@ -962,19 +1049,12 @@ fastk::WLayout make_blocked(const bhcp_space_plan* sp, long long k_count, int ns
 }
 
 fastk::WLayout native_layout(const bhcp_space_plan* sp, long long k_count, int n) {
-  if (sp->dim == 1) {
-    fastk::WLayout wl{};
-    wl.mode_major = 0;
-    wl.w_ld = k_count;
-    wl.nmodes = k_count;
-    return wl;
-  }
+  // 1D: P1 = 1, i.e. mode-major with row stride NT*8 (each mode's time series contiguous)
   const long long b[2] = {0, n};
   return make_blocked(sp, k_count, 1, b);
 }
 
 long long native_w_elems(const bhcp_space_plan* sp, int n) {
-  if (sp->dim == 1) return sp->nx * (long long)n;
   return sp->nx * fastk::kTBL * ((n + fastk::kTBL - 1) / fastk::kTBL);
 }
 
@@ -1074,7 +1154,14 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
                int pass, cudaStream_t s) {
   const int d = sp->dim, m = sp->m;
   const int L = 2 * (m + 1);
-  if (pass == 0 && d == 1) return launch_rows(sp, in, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
+  if (pass == 0 && d == 1) {
+    // 1D: W mode-major (row stride NT*8) -> transpose to level-major y -> rows DST in place
+    const long long NT1 = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+    dim3 grid((unsigned)((nlev + 31) / 32), (unsigned)((m + 31) / 32));
+    k_transpose_ld<<<grid, dim3(32, 8), 0, s>>>(in, NT1 * fastk::kTBL, y, m, nlev);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_transpose_ld");
+    return launch_rows(sp, y, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
+  }
   if (pass >= 1)
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
@@ -1175,6 +1262,7 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
   cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
   sp->tiles_dev = nullptr;
   sp->ntiles = 0;
+  for (int i = 0; i < 9; ++i) { sp->seg_tiles[i] = nullptr; sp->seg_count[i] = 0; }
   {
     const int N = num_cells;
     std::vector<double2> tw(N);
@@ -1214,6 +1302,8 @@ void bhcp_space_plan_destroy(bhcp_space_plan* sp) {
   if (sp->tiles_dev) cudaFree(sp->tiles_dev);
   cudaFree(sp->twN);
   cudaFree(sp->snN);
+  for (int i = 0; i < 9; ++i)
+    if (sp->seg_tiles[i]) cudaFree(sp->seg_tiles[i]);
   delete sp;
 }
 
@@ -1234,6 +1324,17 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
   cudaMemcpy(tp->tables, gamma_host, nb, cudaMemcpyHostToDevice);
   cudaMemcpy(tp->tables + n_levels, gamma_inv_host, nb, cudaMemcpyHostToDevice);
   cudaMemcpy(tp->tables + 2 * n_levels, shifts_host, nb, cudaMemcpyHostToDevice);
+  tp->blue = nullptr;
+  if (n_levels == 257 || n_levels == 1025 || n_levels == 4097) {
+    std::vector<double2> tabs;
+    if (!build_blue_tables(n_levels, &tabs, &err)) {
+      free_fft_plan(&tp->fft); cudaFree(tp->tables); delete tp; return fail(BHCP_ERR_INVALID, err);
+    }
+    if (cudaMalloc(&tp->blue, sizeof(double2) * tabs.size()) != cudaSuccess) {
+      free_fft_plan(&tp->fft); cudaFree(tp->tables); delete tp; return cuda_fail("cudaMalloc blue tables");
+    }
+    cudaMemcpy(tp->blue, tabs.data(), sizeof(double2) * tabs.size(), cudaMemcpyHostToDevice);
+  }
   *out = tp;
   return BHCP_OK;
 }
@@ -1243,6 +1344,7 @@ void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
   DeviceGuard g(tp->device);
   free_fft_plan(&tp->fft);
   cudaFree(tp->tables);
+  if (tp->blue) cudaFree(tp->blue);
   delete tp;
 }
 

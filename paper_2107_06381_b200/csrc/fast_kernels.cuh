@@ -436,3 +436,190 @@ template <int N> constexpr size_t modes_smem() { return sizeof(double2) * N * Mo
 
 }  // namespace fastk
 }  // namespace bhcp
+
+namespace bhcp {
+namespace fastk {
+
+// ---------------------------------------------------------------------------
+// k_modes_blue<n>: pass A for n = 2^p + 1 time levels (BASELINE n = 257,
+// 1025, 4097). With M = n - 1 = 2^p the DFT
+//   X_t = sum_{j<M} v_j w^{jt} + v_M w^{Mt},  w = exp(-2 pi i / n),
+// has its first sum as a chirp-z transform whose linear convolution spans
+// exactly 2M = 2^(p+1) points (inputs j < M, lags -(M-1)..M), so Bluestein
+// runs on power-of-two FFTs of length L = 2M instead of the smooth length
+// >= 2n-1 a general Bluestein needs:
+//   X_t = c_t * IFFT_L( FFT_L(v c) * FFT_L(b) )_t + v_M w^{Mt},
+//   c_j = exp(-i pi j^2 / n), b_d = conj(c_d) for d in [-(M-1), M].
+// Tables (host, long double): chirp c (n), bhat = FFT_L(b)/L (L), w^{Mt} (n),
+// twiddles of length L.
+struct BlueTables {
+  const double2* tw;     // exp(-2 pi i k / L)
+  const double2* chirp;  // c_j, j < n
+  const double2* bhat;   // FFT_L(b) / L
+  const double2* wM;     // w^{M t}, t < n
+};
+
+template <int NL> struct BluePlan;
+template <> struct BluePlan<257> { static constexpr int L = 512, S = 8, T = 256, R1 = 8; template <class Lay> using F = Fft<512, S, T, Lay, 8, 8, 8>; };
+template <> struct BluePlan<1025> { static constexpr int L = 2048, S = 2, T = 256, R1 = 16; template <class Lay> using F = Fft<2048, S, T, Lay, 16, 16, 8>; };
+template <> struct BluePlan<4097> { static constexpr int L = 8192, S = 1, T = 512, R1 = 16; template <class Lay> using F = Fft<8192, S, T, Lay, 16, 16, 8, 4>; };
+
+struct BlueModesArgs {
+  const double2* shifts;
+  const double2* gaminv;
+  const double* mu1;
+  const double* ghat;
+  double cscale;
+  long long k_begin, k_count;
+  double* W;
+  int m, dim;
+  StatusDev* st;
+  BlueTables bt;
+  WLayout wl;
+  const int4* tiles;   // SYM: (k1, k2-or-segment start, k3 segment start)
+  long long ntiles;
+};
+
+// Second FFT of the Bluestein pair: all stages read shared memory.
+template <int L, int S, int T, class Lay, int R1, int... Rest>
+struct FftAllSmem {
+  template <class Sink>
+  static __device__ __forceinline__ void run(double2* buf, const double2* tw, Sink& sink) {
+    Runner<L, S, T, Lay, 1, R1, Rest...>::tail(buf, tw, sink);
+  }
+};
+template <class F> struct AllSmemOf;
+template <int L, int S, int T, class Lay, int R1, int... Rest>
+struct AllSmemOf<Fft<L, S, T, Lay, R1, Rest...>> { using type = FftAllSmem<L, S, T, Lay, R1, Rest...>; };
+
+template <int NL, bool SYM>
+__global__ void __launch_bounds__(BluePlan<NL>::T, 1) k_modes_blue(BlueModesArgs a) {
+  using P = BluePlan<NL>;
+  constexpr int L = P::L, S = P::S, T = P::T, M = NL - 1;
+  using Lay = SeqMajorPad<L, P::R1>;
+  using F1 = typename P::template F<Lay>;
+  using F2 = typename AllSmemOf<F1>::type;
+  extern __shared__ double2 smem[];
+  __shared__ double s_mu[S], s_c[S], s_cm[S], red[2 * (T / 32)];
+  __shared__ long long s_dst[S], s_mir[S];
+  __shared__ bool s_valid[S];
+  __shared__ double2 s_vM[S];
+  double2* buf = smem;
+  if (threadIdx.x < S) {
+    const int q = threadIdx.x;
+    bool v;
+    long long kd, km = -1;
+    if (SYM) {
+      const int4 tb = a.tiles[blockIdx.x];
+      if (a.dim == 2) {
+        const int k1 = tb.x, k2 = tb.y + q;
+        v = k2 < a.m && k2 >= k1;
+        kd = (long long)k1 * a.m + k2;
+        if (v && k2 != k1) km = (long long)k2 * a.m + k1;
+      } else {
+        const int k1 = tb.x, k2 = tb.y, k3 = tb.z + q;
+        v = k3 < a.m;
+        kd = ((long long)k1 * a.m + k2) * a.m + k3;
+        if (v && k1 != k2) km = ((long long)k2 * a.m + k1) * a.m + k3;
+      }
+      if (!v) kd = 0;
+    } else {
+      const long long kl = (long long)blockIdx.x * S + q;
+      v = kl < a.k_count;
+      kd = a.k_begin + (v ? kl : 0);
+    }
+    s_valid[q] = v;
+    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    s_mu[q] = mu;
+    s_c[q] = v ? a.ghat[kd] * a.cscale : 0.0;
+    s_cm[q] = (km >= 0) ? a.ghat[km] * a.cscale : 0.0;
+    s_dst[q] = v ? (SYM ? kd : kd - a.k_begin) : -1;
+    s_mir[q] = km;
+    // last input v_M = 1/(s_M + mu)
+    const double2 s = __ldg(a.shifts + M);
+    const double dr = s.x + mu, di = s.y;
+    const double den2 = dr * dr + di * di;
+    if (v && den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, M);
+    const double inv = fast_rcp(den2);
+    s_vM[q] = v ? make_double2(dr * inv, -di * inv) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // FFT 1: a_j = v_j c_j (j < M), zero padded to L
+  auto gen = [&](int q, int j) -> double2 {
+    if (j >= M || !s_valid[q]) return make_double2(0.0, 0.0);
+    const double2 s = __ldg(a.shifts + j);
+    const double dr = s.x + s_mu[q], di = s.y;
+    const double den2 = dr * dr + di * di;
+    if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, j);
+    const double inv = fast_rcp(den2);
+    return cmul(make_double2(dr * inv, -di * inv), __ldg(a.bt.chirp + j));
+  };
+  auto sink1 = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = cconj(cmul(X, __ldg(a.bt.bhat + idx))); };
+  F1::run(buf, a.bt.tw, gen, sink1);
+  __syncthreads();
+  // FFT 2 (conjugated inverse): conv_t = conj(X_t); X_t of the DFT = c_t conv_t + v_M w^{Mt}
+  auto sink2 = [&](int q, int idx, double2 X) {
+    if (idx > M) return;
+    const double2 conv = cconj(X);
+    const double2 Y = cadd(cmul(conv, __ldg(a.bt.chirp + idx)), cmul(s_vM[q], __ldg(a.bt.wM + idx)));
+    buf[Lay::addr(q, idx)] = cmul(Y, __ldg(a.gaminv + idx));
+  };
+  F2::run(buf, a.bt.tw, sink2);
+  __syncthreads();
+  // store: warps loop over the S modes; lanes run along t
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double sre = 0.0, sim = 0.0;
+  for (int q = warp; q < S; q += T / 32) {
+    const long long cd = s_dst[q];
+    if (cd < 0) continue;
+    const long long cm = SYM ? s_mir[q] : -1;
+    const double c = s_c[q], c2 = SYM ? s_cm[q] : 0.0;
+    const WLayout& wl = a.wl;
+    const int nsl = wl.mode_major ? wl.nsl : 1;
+    const long long cds = cm >= 0 ? cm : 0;
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
+      long long pd, pm, tstep;
+      if (wl.mode_major) {
+        const long long nt = wl.sl_nt[sl];
+        const long long k1d = cd / wl.P1, k1m = cds / wl.P1;
+        pd = wl.sl_off[sl] + (k1d * nt * wl.P1 + (cd - k1d * wl.P1)) * kTBL;
+        pm = wl.sl_off[sl] + (k1m * nt * wl.P1 + (cds - k1m * wl.P1)) * kTBL;
+        tstep = wl.P1 * kTBL;
+      } else {
+        pd = cd;
+        pm = cds;
+        tstep = 0;
+      }
+      for (int t = t0 + lane; t < t1; t += 32) {
+        const double2 z = buf[Lay::addr(q, t)];
+        const double wr = c * z.x, wi = c * z.y;
+        sre = fma(wr, wr, sre);
+        sim = fma(wi, wi, sim);
+        const int tl = t - t0;
+        const long long off = wl.mode_major ? (long long)(tl >> 3) * tstep + (tl & 7) : (long long)t * wl.w_ld;
+        a.W[pd + off] = wr;
+        if (SYM && cm >= 0) {
+          const double vr = c2 * z.x, vi = c2 * z.y;
+          sre = fma(vr, vr, sre);
+          sim = fma(vi, vi, sim);
+          a.W[pm + off] = vr;
+        }
+      }
+    }
+  }
+  block_sum2(sre, sim, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.st->sum_re2, sre);
+    atomicAdd(&a.st->sum_im2, sim);
+  }
+}
+
+template <int NL> constexpr size_t blue_smem() {
+  using P = BluePlan<NL>;
+  return sizeof(double2) * SeqMajorPad<P::L, P::R1>::words(P::S);
+}
+
+}  // namespace fastk
+}  // namespace bhcp

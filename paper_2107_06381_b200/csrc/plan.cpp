@@ -176,6 +176,38 @@ bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
   return true;
 }
 
+// Power-of-two Bluestein tables for n = 2^p + 1 (see fastk::k_modes_blue):
+// tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1).
+bool build_blue_tables(int n, std::vector<double2>* out, std::string* err) {
+  const int M = n - 1, L = 2 * M;
+  if (M < 2 || (M & (M - 1))) { *err = "n - 1 must be a power of two"; return false; }
+  out->assign(2 * L + 2 * n, make_double2(0.0, 0.0));
+  double2* tw = out->data();
+  double2* chirp = tw + L;
+  double2* bhat = chirp + n;
+  double2* wM = bhat + L;
+  for (int k = 0; k < L; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / (long double)L;
+    tw[k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  std::vector<cld> cl(n);
+  for (int j = 0; j < n; ++j) {
+    const long long e = ((long long)j * j) % (2LL * n);
+    const long double a = -kPi * (long double)e / (long double)n;
+    cl[j] = cld(cosl(a), sinl(a));
+    chirp[j] = to_d2(cl[j]);
+    const long long f = ((long long)M * j) % n;
+    const long double b = -2.0L * kPi * (long double)f / (long double)n;
+    wM[j] = make_double2((double)cosl(b), (double)sinl(b));
+  }
+  std::vector<cld> bb(L, cld(0, 0));
+  for (int d = 0; d <= M; ++d) bb[d] = std::conj(cl[d]);
+  for (int d = 1; d < M; ++d) bb[L - d] = std::conj(cl[d]);
+  host_dft(bb);
+  for (int k = 0; k < L; ++k) bhat[k] = to_d2(bb[k] / (long double)L);
+  return true;
+}
+
 void free_fft_plan(FftPlanHost* p) {
   if (p->mem) cudaFree(p->mem);
   p->mem = nullptr;

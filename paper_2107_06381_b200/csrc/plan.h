@@ -36,6 +36,9 @@ struct FftPlanHost {
 bool build_fft_plan(int L, FftPlanHost* out, std::string* err);
 void free_fft_plan(FftPlanHost* p);
 
+// tw (L) | chirp (n) | bhat (L) | wM (n) for the power-of-two Bluestein, n = 2^p + 1.
+bool build_blue_tables(int n, std::vector<double2>* out, std::string* err);
+
 // Upload the odd-radix codelet constants to the current device (idempotent).
 bool ensure_device_constants(int device, std::string* err);
 
