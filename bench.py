@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--cpu-fraction", type=float, default=1.0,
                    help="fraction of every per-unit operation in the CPU-baseline sample")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--quick", action="store_true", help="device timing only (no e2e / unfused / CPU legs)")
     return p.parse_args()
 
 
@@ -248,7 +249,7 @@ def main():
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
         names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"] + \
-                [("k_dst_blk" if a == 0 else "k_dst_cols_fast") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
+                [("k_dst_blk2" if a == 0 else "k_dst_cols_fast") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof
@@ -267,6 +268,10 @@ def main():
         ms_per_step = total_ms / args.steps
         value = dof / (ms_per_step * 1e-3)
 
+        if args.quick:
+            print(json.dumps({"config": args.config, "ms_per_step": ms_per_step, "value": value,
+                              "phases_ms": {nm: float(t) for nm, t in zip(names, phase_ms)}}), flush=True)
+            return
         # ---- e2e through the C-ABI with host buffers
         g_host = torch.from_numpy(w.g_delta).pin_memory()
         y_host = torch.empty((n, nx), dtype=torch.float64).pin_memory()

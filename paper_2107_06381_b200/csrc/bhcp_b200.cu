@@ -684,6 +684,12 @@ void set_all_attributes() {
   allow_smem(fastk::k_modes_blue<1025, true>);
   allow_smem(fastk::k_modes_blue<4097, false>);
   allow_smem(fastk::k_modes_blue<4097, true>);
+  allow_smem(gdst::k_lines2<256, 16, 0>);
+  allow_smem(gdst::k_lines2<256, 16, 1>);
+  allow_smem(gdst::k_lines2<512, 16, 0>);
+  allow_smem(gdst::k_lines2<512, 16, 1>);
+  allow_smem(gdst::k_lines2<1024, 8, 0>);
+  allow_smem(gdst::k_lines2<1024, 8, 1>);
   allow_smem(gdst::k_dst_blk2<256>);
   allow_smem(gdst::k_dst_blk2<512>);
   allow_smem(gdst::k_dst_blk2<1024>);
@@ -1083,6 +1089,30 @@ int blk2_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
   return BHCP_OK;
 }
 bool g_blk_odd = false;  // BHCP_BLK_ODD=1: odd-extension first level pass (k_dst_blk)
+bool g_level_lines2 = false;  // BHCP_LEVEL_LINES2=1: wide-tile k_lines2 level passes (slower on B200, kept for study)
+
+template <int N, int S, int MODE>
+int lines2_launch(const bhcp_space_plan* sp, gdst::ArgsL2 a, cudaStream_t s) {
+  using namespace gdst;
+  a.tw = sp->twN; a.sn = sp->snN; a.scale = sqrt(2.0 / N);
+  const long long tiles = ((a.ni + 2 * S - 1) / (2 * S)) * a.no;
+  if (tiles == 0) return BHCP_OK;
+  const size_t sm = gdst::smemL2_bytes<N, S>();
+  const long long grid = std::min<long long>(tiles, resident_ctas(k_lines2<N, S, MODE>, 32 * S, sm));
+  k_lines2<N, S, MODE><<<(unsigned)grid, 32 * S, sm, s>>>(a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_lines2 launch");
+  return BHCP_OK;
+}
+
+template <int MODE>
+int lines2_dispatch(const bhcp_space_plan* sp, const gdst::ArgsL2& a, cudaStream_t s) {
+  switch (sp->m + 1) {
+    case 256: return lines2_launch<256, 16, MODE>(sp, a, s);
+    case 512: return lines2_launch<512, 16, MODE>(sp, a, s);
+    case 1024: return lines2_launch<1024, 8, MODE>(sp, a, s);
+  }
+  return fail(BHCP_ERR_INVALID, "no k_lines2 for this length");
+}
 
 template <int L>
 int blk_launch(const bhcp_space_plan* sp, gdst::ArgsB a, cudaStream_t s) {
@@ -1162,10 +1192,21 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_transpose_ld");
     return launch_rows(sp, y, y, 0, nlev, 0, nullptr, nullptr, s, Blocked(), 1);
   }
-  if (pass >= 1)
-    return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
   const long long P1 = ipow(m, d - 1);
+  if (!g_disable_fast && g_level_lines2 && (m + 1 == 256 || m + 1 == 512 || m + 1 == 1024)) {
+    gdst::ArgsL2 a{};
+    if (pass == 0) {
+      a.in = in; a.out = y; a.ni = nlev; a.no = P1;
+      a.koff = koff; a.NT = NT; a.P1 = P1; a.idiv = ipow(m, d - 2); a.P = P1;
+      return lines2_dispatch<0>(sp, a, s);
+    }
+    a.in = y; a.out = y; a.ni = ipow(m, pass); a.no = nlev * ipow(m, d - 1 - pass);
+    a.es = ipow(m, pass); a.os = ipow(m, pass + 1);
+    return lines2_dispatch<1>(sp, a, s);
+  }
+  if (pass >= 1)
+    return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
   if (!g_disable_fast && !g_blk_odd && (L == 512 || L == 1024 || L == 2048)) {
     gdst::ArgsB2 b{};
     b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
@@ -1226,6 +1267,8 @@ bool ensure_device_constants(int device, std::string* err) {
     g_use_dst2 = (e2 && e2[0] == '1');
     const char* e3 = getenv("BHCP_BLK_ODD");
     g_blk_odd = (e3 && e3[0] == '1');
+    const char* e4 = getenv("BHCP_LEVEL_LINES2");
+    g_level_lines2 = (e4 && e4[0] == '1');
   }
   set_all_attributes();
   cudaError_t e = cudaGetLastError();

@@ -460,9 +460,9 @@ struct BlueTables {
 };
 
 template <int NL> struct BluePlan;
-template <> struct BluePlan<257> { static constexpr int L = 512, S = 8, T = 256, R1 = 8; template <class Lay> using F = Fft<512, S, T, Lay, 8, 8, 8>; };
-template <> struct BluePlan<1025> { static constexpr int L = 2048, S = 2, T = 256, R1 = 16; template <class Lay> using F = Fft<2048, S, T, Lay, 16, 16, 8>; };
-template <> struct BluePlan<4097> { static constexpr int L = 8192, S = 1, T = 512, R1 = 16; template <class Lay> using F = Fft<8192, S, T, Lay, 16, 16, 8, 4>; };
+template <> struct BluePlan<257> { static constexpr int L = 512, S = 8, T = 256, R1 = 8, MINB = 2; template <class Lay> using F = Fft<512, S, T, Lay, 8, 8, 8>; };
+template <> struct BluePlan<1025> { static constexpr int L = 2048, S = 2, T = 256, R1 = 16, MINB = 2; template <class Lay> using F = Fft<2048, S, T, Lay, 16, 16, 8>; };
+template <> struct BluePlan<4097> { static constexpr int L = 8192, S = 1, T = 512, R1 = 16, MINB = 1; template <class Lay> using F = Fft<8192, S, T, Lay, 16, 16, 8, 4>; };
 
 struct BlueModesArgs {
   const double2* shifts;
@@ -493,7 +493,7 @@ template <int L, int S, int T, class Lay, int R1, int... Rest>
 struct AllSmemOf<Fft<L, S, T, Lay, R1, Rest...>> { using type = FftAllSmem<L, S, T, Lay, R1, Rest...>; };
 
 template <int NL, bool SYM>
-__global__ void __launch_bounds__(BluePlan<NL>::T, 1) k_modes_blue(BlueModesArgs a) {
+__global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_blue(BlueModesArgs a) {
   using P = BluePlan<NL>;
   constexpr int L = P::L, S = P::S, T = P::T, M = NL - 1;
   using Lay = SeqMajorPad<L, P::R1>;

@@ -478,7 +478,7 @@ struct ArgsB2 {
 };
 
 template <int N>
-__global__ void __launch_bounds__(PlanB2<N>::T, 2) k_dst_blk2(ArgsB2 a) {
+__global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   constexpr int S = 4, T = PlanB2<N>::T, m = N - 1;
   constexpr int RUN = m * kTB;
   constexpr int KU = (N / 2) / 32;   // k values per lane (k = u*32 + lane)
@@ -559,6 +559,181 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 2) k_dst_blk2(ArgsB2 a) {
 template <int N> constexpr size_t smemB2_bytes() {
   using Lay = Interleaved<4, PlanB2<N>::R1>;
   return sizeof(double2) * Lay::words(N) + sizeof(double) * ((N - 1) * kTB + N);
+}
+
+}  // namespace gdst
+}  // namespace bhcp
+
+namespace bhcp {
+namespace gdst {
+
+// ---------------------------------------------------------------------------
+// k_lines2<N, S, MODE>: level-pass DST over 2S real lines per CTA with the
+// half-length real DST (one N-point complex FFT per two lines), wide tiles
+// and no CTA-wide barrier in the post-processing:
+//   * first FFT stage loads the lines straight from global memory, thread
+//     mapping sequence-fastest, so 2S consecutive lines give 16*S-byte runs;
+//   * warp q post-processes sequence q (both of its lines: U^a/U^b split and
+//     the prefix sums) and writes the DST coefficients back into its own
+//     shared-memory region;
+//   * one coalesced store phase.
+// MODE 0: input = blocked W (lines = levels of one spatial line, 8 levels per
+//         contiguous block), output = rows of the level-major y.
+// MODE 1: strided in place on y: element e of line (o, i) at o*os + e*es + i.
+template <int L, int LD>
+struct SeqMajorQ {  // sequence-major, odd stride LD, thread mapping sequence-fastest
+  static constexpr int words(int S) { return LD * S; }
+  static __device__ __forceinline__ int addr(int q, int idx) { return q * LD + idx; }
+  template <int STRIDE>
+  static __device__ __forceinline__ int addr_r(int q, int j, int r) { return q * LD + j + r * STRIDE; }
+  template <int R>
+  static __device__ __forceinline__ int addr_first(int q, int base, int r) { return q * LD + base + r; }
+  static __device__ __forceinline__ void split(int b, int nb, int& q, int& j);
+};
+
+template <int N, int S> struct PlanL2;
+template <> struct PlanL2<256, 16> { template <class Lay> using F = Fft<256, 16, 512, Lay, 4, 8, 8>; };
+template <> struct PlanL2<512, 16> { template <class Lay> using F = Fft<512, 16, 512, Lay, 8, 8, 8>; };
+template <> struct PlanL2<1024, 8> { template <class Lay> using F = Fft<1024, 8, 256, Lay, 16, 8, 8>; };
+
+template <int S> struct QSplit {
+  static __device__ __forceinline__ void split(int b, int nb, int& q, int& j) { q = b % S; j = b / S; }
+};
+template <int L, int LD, int S>
+struct SeqMajorQS : SeqMajorQ<L, LD> {
+  static __device__ __forceinline__ void split(int b, int nb, int& q, int& j) { q = b % S; j = b / S; }
+};
+
+struct ArgsL2 {
+  const double* in;
+  double* out;
+  const double2* tw;
+  const double* sn;
+  double scale;
+  long long ni, no;            // lines per outer index (levels for MODE 0), outer count
+  // MODE 0
+  const long long* koff;
+  long long NT, P1, idiv, P;
+  // MODE 1
+  long long os, es;
+};
+
+template <int N, int S, int MODE>
+__global__ void __launch_bounds__(32 * S, 1) k_lines2(ArgsL2 a) {
+  constexpr int T = 32 * S, m = N - 1, NL = 2 * S;
+  constexpr int LD = N + 1;  // odd stride (double2 units)
+  constexpr int KU = (N / 2) / 32;
+  using Lay = SeqMajorQS<N, LD, S>;
+  using Ff = typename PlanL2<N, S>::template F<Lay>;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  double* sn = reinterpret_cast<double*>(smem + Lay::words(S));
+  for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long ntile_i = (a.ni + NL - 1) / NL;
+  const long long ntiles = ntile_i * a.no;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long o = tile / ntile_i;
+    const long long i0 = (tile - o * ntile_i) * NL;
+    const long long valid = a.ni - i0;  // lines li < valid exist
+    long long base0 = 0;
+    if (MODE == 0) {
+      const long long k1 = o / a.idiv, r2 = o - k1 * a.idiv;
+      const long long kb = a.koff ? __ldg(a.koff + k1) : k1 * a.NT * a.P1 * kTB;
+      base0 = kb + r2 * (long long)m * kTB;  // + (tt*P1 + e)*8 + tl with level i = tt*8 + tl
+    } else {
+      base0 = o * a.os + i0;
+    }
+    __syncthreads();  // previous tile's store phase done with buf
+    auto gen = [&](int q, int j) -> double2 {
+      if (j == 0) return make_double2(0.0, 0.0);
+      double2 p = make_double2(0.0, 0.0), r = make_double2(0.0, 0.0);
+      const int li = 2 * q;
+      if (li < valid) {
+        if (MODE == 0) {
+          const long long i = i0 + li;  // even level: its pair lies in the same 8-level block
+          const long long blk = base0 + ((i >> 3) * a.P1) * kTB + (i & 7);
+          p = __ldg(reinterpret_cast<const double2*>(a.in + blk + (long long)(j - 1) * kTB));
+          r = __ldg(reinterpret_cast<const double2*>(a.in + blk + (long long)(N - j - 1) * kTB));
+        } else {
+          const double* src = a.in + base0 + li;
+          p.x = __ldg(src + (long long)(j - 1) * a.es);
+          r.x = __ldg(src + (long long)(N - j - 1) * a.es);
+          if (li + 1 < valid) {
+            p.y = __ldg(src + 1 + (long long)(j - 1) * a.es);
+            r.y = __ldg(src + 1 + (long long)(N - j - 1) * a.es);
+          }
+        }
+        if (MODE == 0 && li + 1 >= valid) { p.y = 0.0; r.y = 0.0; }
+      }
+      const double s = sn[j];
+      return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
+    };
+    auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
+    Ff::run(buf, a.tw, gen, sink);
+    __syncthreads();
+    // post-processing: warp q owns sequence q = lines (2q, 2q+1)
+    {
+      const int q = warp;
+      double Ca[KU], Da[KU], Cb[KU], Db[KU];
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = u * 32 + lane;
+        const double2 A = buf[Lay::addr(q, k)];
+        const double2 B = buf[Lay::addr(q, (N - k) & (N - 1))];
+        Ca[u] = 0.5 * (A.x + B.x);
+        Da[u] = -0.5 * (A.y - B.y);
+        Cb[u] = 0.5 * (A.y + B.y);
+        Db[u] = 0.5 * (A.x - B.x);
+      }
+      __syncwarp();
+      double* reg = reinterpret_cast<double*>(buf + Lay::addr(q, 0));  // 2*LD doubles
+      const double c0a = __shfl_sync(0xffffffffu, Ca[0], 0), c0b = __shfl_sync(0xffffffffu, Cb[0], 0);
+      double carry_a = 0.0, carry_b = 0.0;
+#pragma unroll
+      for (int u = 0; u < KU; ++u) {
+        const int k = u * 32 + lane;
+        double ia = Ca[u], ib = Cb[u];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const double va = __shfl_up_sync(0xffffffffu, ia, off);
+          const double vb = __shfl_up_sync(0xffffffffu, ib, off);
+          if (lane >= off) { ia += va; ib += vb; }
+        }
+        const double oa = carry_a + ia - 0.5 * c0a, ob = carry_b + ib - 0.5 * c0b;
+        carry_a += __shfl_sync(0xffffffffu, ia, 31);
+        carry_b += __shfl_sync(0xffffffffu, ib, 31);
+        // line a at reg[0 .. m), line b at reg[m .. 2m): coefficient e = 2k (odd S), 2k-1 (even S)
+        reg[2 * k] = a.scale * oa;
+        reg[m + 2 * k] = a.scale * ob;
+        if (k >= 1) {
+          reg[2 * k - 1] = a.scale * Da[u];
+          reg[m + 2 * k - 1] = a.scale * Db[u];
+        }
+      }
+    }
+    __syncthreads();
+    if (MODE == 0) {
+      // output rows: line li = level i0+li, contiguous in y
+      for (int li = warp; li < NL; li += T / 32) {
+        if (li >= valid) continue;
+        const double* reg = reinterpret_cast<const double*>(buf + Lay::addr(li >> 1, 0)) + (li & 1) * m;
+        double* __restrict__ dst = a.out + ((i0 + li) * a.P + o) * m;
+        for (int e = lane; e < m; e += 32) dst[e] = reg[e];
+      }
+    } else {
+      const int li = threadIdx.x % NL;
+      const double* reg = reinterpret_cast<const double*>(buf + Lay::addr(li >> 1, 0)) + (li & 1) * m;
+      double* __restrict__ dst = a.out + base0 + li;
+      if (li < valid) {
+        for (int e = threadIdx.x / NL; e < m; e += T / NL) dst[(long long)e * a.es] = reg[e];
+      }
+    }
+  }
+}
+
+template <int N, int S> constexpr size_t smemL2_bytes() {
+  return sizeof(double2) * (N + 1) * S + sizeof(double) * N;
 }
 
 }  // namespace gdst
