@@ -176,7 +176,10 @@ def main():
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
-    if world > 1:
+    # BHCP_FORCE_SHARDED=1 runs the slab-decomposed NCCL path even on one rank
+    # (exercises the multi-GPU code on a single-GPU box: all-to-all to itself)
+    sharded = world > 1 or os.environ.get("BHCP_FORCE_SHARDED") == "1"
+    if sharded:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2107_06381_b200 import _lib, plans, workloads
     from paper_2107_06381_b200 import distributed as D
@@ -194,7 +197,7 @@ def main():
     lib = _lib.lib()
     nx, n = w.n_space, w.n_levels
 
-    if world == 1:
+    if not sharded:
         plan = B.PintPlan(grid, n, tg.tau, system.omega)
         y = torch.empty((n, nx), dtype=torch.float64, device=dev)
         ws = plan.workspace()

@@ -328,6 +328,38 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     a2a_bytes = 8.0 * sum(s for q, s in enumerate(layout.send_splits(rank)) if q != rank)
     value = w.dof / (ms * 1e-3)
     hbm, kind = peaks()
+    # e2e: pinned host g -> device, sharded solve, this rank's level slab -> pinned host
+    g_host = torch.from_numpy(w.g_delta).pin_memory()
+    c0, c1 = layout.lev[rank]
+    y_host = torch.empty((c1 - c0, w.n_space), dtype=torch.float64).pin_memory()
+    g_dev = ops.g
+
+    def e2e_step():
+        g_dev.copy_(g_host, non_blocking=True)
+        y, _ = sharded_solve(ops, comm, layout, rank)
+        y_host.copy_(y, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    e2e_steps = max(3, min(args.steps, 10))
+    a0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    a1.record()
+    torch.cuda.synchronize()
+    e2e_ms = comm.all_reduce_max(a0.elapsed_time(a1)) / e2e_steps
+    check_global_status(comm, ops, plan.shifts)
+    # dominant per-rank phase vs HBM: pass A writes 8 B per local DOF, pass B moves 32 B per local DOF
+    local_dof_a = layout.slab_modes(rank) * layout.n
+    local_dof_b = layout.levels(rank) * layout.n_space
+    alg = [8.0 * local_dof_a, 0.0, 32.0 * local_dof_b]
+    dom = 0 if ph[0] >= ph[2] else 2
+    achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
+    launches = 6 + 2 * grid.dim  # status reset, ghat (dim passes + scale), modes, level passes (x2 kernels max)
     if rank != 0:
         return None
     return {
@@ -335,9 +367,17 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
         "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, slab-decomposed over {world} GPUs",
-                   "dof_per_solve": w.dof, "parallelism": f"mode slabs -> NCCL all-to-all -> level slabs, P={world}"},
+                   "dof_per_solve": w.dof, "parallelism": f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
+                   "l2": "working set larger than L2; no flush"},
+        "roofline": {"bound": "hbm", "kernel": ["pass A (k_modes_fast)", "", "pass B (level passes)"][dom],
+                     "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_source": kind},
         "phases_ms_rank0": {"pass_a_modes": ph[0], "all_to_all": ph[1], "pass_b_levels": ph[2]},
-        "nvlink": {"bytes_per_rank": a2a_bytes, "achieved_GBps": a2a_bytes / (ph[1] * 1e-3) / 1e9,
-                   "peak_GBps": 770.0, "frac": a2a_bytes / (ph[1] * 1e-3) / 1e9 / 770.0},
+        "nvlink": {"bytes_per_rank": a2a_bytes, "achieved_GBps": a2a_bytes / (ph[1] * 1e-3) / 1e9 if ph[1] > 0 else 0.0,
+                   "peak_GBps": 770.0,
+                   "frac": (a2a_bytes / (ph[1] * 1e-3) / 1e9 / 770.0) if ph[1] > 0 else 0.0},
+        "e2e": {"value": w.dof / (e2e_ms * 1e-3), "unit": unit, "h2d_bytes_per_step": 8 * w.n_space,
+                "d2h_bytes_per_step": 8 * (c1 - c0) * w.n_space, "ms_per_step": e2e_ms},
+        "gpu_launches": launches * args.steps,
         "clocks": clocks,
     }
