@@ -684,32 +684,9 @@ void set_all_attributes() {
   allow_smem(fastk::k_modes_blue<1025, true>);
   allow_smem(fastk::k_modes_blue<4097, false>);
   allow_smem(fastk::k_modes_blue<4097, true>);
-  allow_smem(gdst::k_lines2<256, 16, 0>);
-  allow_smem(gdst::k_lines2<256, 16, 1>);
-  allow_smem(gdst::k_lines2<512, 16, 0>);
-  allow_smem(gdst::k_lines2<512, 16, 1>);
-  allow_smem(gdst::k_lines2<1024, 8, 0>);
-  allow_smem(gdst::k_lines2<1024, 8, 1>);
   allow_smem(gdst::k_dst_blk2<256>);
   allow_smem(gdst::k_dst_blk2<512>);
   allow_smem(gdst::k_dst_blk2<1024>);
-  allow_smem(gdst::k_dst_blk<512>);
-  allow_smem(gdst::k_dst_blk<1024>);
-  allow_smem(gdst::k_dst_blk<2048>);
-  allow_smem(gdst::k_dst2<256, 0>);
-  allow_smem(gdst::k_dst2<256, 1>);
-  allow_smem(gdst::k_dst2<512, 0>);
-  allow_smem(gdst::k_dst2<512, 1>);
-  allow_smem(gdst::k_dst2<1024, 0>);
-  allow_smem(gdst::k_dst2<1024, 1>);
-  allow_smem(gdst::k_dst_gather<512, 0>);
-  allow_smem(gdst::k_dst_gather<512, 1>);
-  allow_smem(gdst::k_dst_gather<1024, 0>);
-  allow_smem(gdst::k_dst_gather<1024, 1>);
-  allow_smem(gdst::k_dst_gather<2048, 0>);
-  allow_smem(gdst::k_dst_gather<2048, 1>);
-  allow_smem(gdst::k_dst_gather<8192, 0>);
-  allow_smem(gdst::k_dst_gather<8192, 1>);
   allow_smem(fastk::k_modes_fast<513, false>);
   allow_smem(fastk::k_modes_fast<513, true>);
 }
@@ -759,7 +736,6 @@ void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cpl
 }
 
 bool fast_dst_length(int L) { return L == 512 || L == 1024 || L == 2048 || L == 8192; }
-bool g_use_dst2 = false;  // half-length DST level pass (BHCP_USE_DST2=1); see DESIGN.md 7
 bool g_disable_fast = false;
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -1001,10 +977,6 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
     f.shifts = tp->tables + 2 * tp->n; f.gaminv = tp->tables + tp->n; f.mu1 = sp->mu1_dev; f.ghat = ghat;
     f.cscale = cscale; f.k_begin = k_begin; f.k_count = kc; f.W = W; f.m = sp->m; f.dim = sp->dim;
     f.tw = P.d.tw; f.st = st; f.wl = wl;
-    {
-      const char* k = getenv("BHCP_EXPERIMENT_SKIP");
-      f.skip = k ? atoi(k) : 0;
-    }
     // symmetric 4x4 tiles need the whole mode range with global column indices
     const bool sym = sp->dim == 2 && k_begin == 0 && k_end == sp->nx && sp->tiles_dev && wl.nmodes == sp->nx;
     if (sym) {
@@ -1088,94 +1060,6 @@ int blk2_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk2 launch");
   return BHCP_OK;
 }
-bool g_blk_odd = false;  // BHCP_BLK_ODD=1: odd-extension first level pass (k_dst_blk)
-bool g_level_lines2 = false;  // BHCP_LEVEL_LINES2=1: wide-tile k_lines2 level passes (slower on B200, kept for study)
-
-template <int N, int S, int MODE>
-int lines2_launch(const bhcp_space_plan* sp, gdst::ArgsL2 a, cudaStream_t s) {
-  using namespace gdst;
-  a.tw = sp->twN; a.sn = sp->snN; a.scale = sqrt(2.0 / N);
-  const long long tiles = ((a.ni + 2 * S - 1) / (2 * S)) * a.no;
-  if (tiles == 0) return BHCP_OK;
-  const size_t sm = gdst::smemL2_bytes<N, S>();
-  const long long grid = std::min<long long>(tiles, resident_ctas(k_lines2<N, S, MODE>, 32 * S, sm));
-  k_lines2<N, S, MODE><<<(unsigned)grid, 32 * S, sm, s>>>(a);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_lines2 launch");
-  return BHCP_OK;
-}
-
-template <int MODE>
-int lines2_dispatch(const bhcp_space_plan* sp, const gdst::ArgsL2& a, cudaStream_t s) {
-  switch (sp->m + 1) {
-    case 256: return lines2_launch<256, 16, MODE>(sp, a, s);
-    case 512: return lines2_launch<512, 16, MODE>(sp, a, s);
-    case 1024: return lines2_launch<1024, 8, MODE>(sp, a, s);
-  }
-  return fail(BHCP_ERR_INVALID, "no k_lines2 for this length");
-}
-
-template <int L>
-int blk_launch(const bhcp_space_plan* sp, gdst::ArgsB a, cudaStream_t s) {
-  using namespace gdst;
-  const long long tiles = a.P * a.NT;
-  if (tiles == 0) return BHCP_OK;
-  const size_t sm = gdst::smemB_bytes<L>();
-  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_blk<L>, PlanB<L>::T, sm));
-  k_dst_blk<L><<<(unsigned)grid, PlanB<L>::T, sm, s>>>(a);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk launch");
-  return BHCP_OK;
-}
-
-template <int L, int MODE>
-int gather_launch(const bhcp_space_plan* sp, gdst::Args a, cudaStream_t s) {
-  using namespace gdst;
-  const long long tiles = ((a.ni + 2 * Plan<L>::S - 1) / (2 * Plan<L>::S)) * a.no;
-  if (tiles == 0) return BHCP_OK;
-  const size_t sm = gdst::smem_bytes<L>();
-  long long grid = std::min<long long>(tiles, resident_ctas(k_dst_gather<L, MODE>, Plan<L>::T, sm));
-  k_dst_gather<L, MODE><<<(unsigned)grid, Plan<L>::T, sm, s>>>(a);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_gather launch");
-  return BHCP_OK;
-}
-
-template <int N, int MODE>
-int dst2_launch(const bhcp_space_plan* sp, gdst::Args2 a, cudaStream_t s) {
-  using namespace gdst;
-  const long long tiles = ((a.ni + a.ishift + 2 * Plan2<N>::S - 1) / (2 * Plan2<N>::S)) * a.no;
-  if (tiles == 0) return BHCP_OK;
-  const size_t sm = gdst::smem2_bytes<N>(MODE);
-  long long grid = std::min<long long>(tiles, resident_ctas(k_dst2<N, MODE>, Plan2<N>::T, sm));
-  k_dst2<N, MODE><<<(unsigned)grid, Plan2<N>::T, sm, s>>>(a);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst2 launch");
-  return BHCP_OK;
-}
-
-bool dst2_length(int N) { return N == 256 || N == 512 || N == 1024; }
-
-template <int MODE>
-int dst2_dispatch(const bhcp_space_plan* sp, gdst::Args2 a, cudaStream_t s) {
-  a.tw = sp->twN;
-  a.sn = sp->snN;
-  a.scale = sqrt(2.0 / (sp->m + 1));
-  switch (sp->m + 1) {
-    case 256: return dst2_launch<256, MODE>(sp, a, s);
-    case 512: return dst2_launch<512, MODE>(sp, a, s);
-    case 1024: return dst2_launch<1024, MODE>(sp, a, s);
-  }
-  return fail(BHCP_ERR_INVALID, "no half-length DST kernel for this length");
-}
-
-template <int MODE>
-int gather_dispatch(const bhcp_space_plan* sp, const gdst::Args& a, cudaStream_t s) {
-  switch (2 * (sp->m + 1)) {
-    case 512: return gather_launch<512, MODE>(sp, a, s);
-    case 1024: return gather_launch<1024, MODE>(sp, a, s);
-    case 2048: return gather_launch<2048, MODE>(sp, a, s);
-    case 8192: return gather_launch<8192, MODE>(sp, a, s);
-  }
-  return fail(BHCP_ERR_INVALID, "no gather kernel for this length");
-}
-
 // One level pass of the fused solve on `nlev` levels. pass 0: W (1D:
 // level-major; else blocked, k1's first block at koff[k1] or k1*NT*P1*8) ->
 // y (level-major) with the DST along the last axis; pass p >= 1: DST along
@@ -1194,20 +1078,9 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
   }
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
   const long long P1 = ipow(m, d - 1);
-  if (!g_disable_fast && g_level_lines2 && (m + 1 == 256 || m + 1 == 512 || m + 1 == 1024)) {
-    gdst::ArgsL2 a{};
-    if (pass == 0) {
-      a.in = in; a.out = y; a.ni = nlev; a.no = P1;
-      a.koff = koff; a.NT = NT; a.P1 = P1; a.idiv = ipow(m, d - 2); a.P = P1;
-      return lines2_dispatch<0>(sp, a, s);
-    }
-    a.in = y; a.out = y; a.ni = ipow(m, pass); a.no = nlev * ipow(m, d - 1 - pass);
-    a.es = ipow(m, pass); a.os = ipow(m, pass + 1);
-    return lines2_dispatch<1>(sp, a, s);
-  }
   if (pass >= 1)
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
-  if (!g_disable_fast && !g_blk_odd && (L == 512 || L == 1024 || L == 2048)) {
+  if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
     gdst::ArgsB2 b{};
     b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
     b.koff = koff; b.NT = NT; b.P1 = P1; b.idiv = ipow(m, d - 2); b.P = P1; b.nlev = nlev;
@@ -1215,16 +1088,6 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
       case 512: return blk2_launch<256>(sp, b, s);
       case 1024: return blk2_launch<512>(sp, b, s);
       case 2048: return blk2_launch<1024>(sp, b, s);
-    }
-  }
-  if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
-    gdst::ArgsB a{};
-    a.in = in; a.out = y; a.tw = sp->dst.d.tw; a.f = sqrt(2.0 / (m + 1)) * 0.5;
-    a.koff = koff; a.NT = NT; a.P1 = P1; a.idiv = ipow(m, d - 2); a.P = P1; a.nlev = nlev;
-    switch (L) {
-      case 512: return blk_launch<512>(sp, a, s);
-      case 1024: return blk_launch<1024>(sp, a, s);
-      case 2048: return blk_launch<2048>(sp, a, s);
     }
   }
   const long long total = nlev * sp->nx;
@@ -1263,12 +1126,7 @@ bool ensure_device_constants(int device, std::string* err) {
   {
     const char* e = getenv("BHCP_DISABLE_FAST");
     g_disable_fast = (e && e[0] == '1');
-    const char* e2 = getenv("BHCP_USE_DST2");
-    g_use_dst2 = (e2 && e2[0] == '1');
-    const char* e3 = getenv("BHCP_BLK_ODD");
-    g_blk_odd = (e3 && e3[0] == '1');
-    const char* e4 = getenv("BHCP_LEVEL_LINES2");
-    g_level_lines2 = (e4 && e4[0] == '1');
+
   }
   set_all_attributes();
   cudaError_t e = cudaGetLastError();

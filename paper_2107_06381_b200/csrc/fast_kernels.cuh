@@ -303,7 +303,6 @@ struct FastModesArgs {
   StatusDev* st;
   const int2* tiles;  // SYM: upper-triangle 4x4 tile coordinates (a, b), a <= b
   long long ntiles;
-  int skip;           // experiment: 1 = no W stores, 2 = no FFT
   WLayout wl;
 };
 
@@ -365,7 +364,7 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
       const double inv = fast_rcp(den2);
       return make_double2(dr * inv, -di * inv);
     };
-    if (a.skip != 2) ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
+    ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
   }
   // Store phase, per warp (no CTA barrier): warp q writes its own mode's
   // time series. W layout: a.wl (mode-major slabs: contiguous runs of t;
@@ -407,12 +406,12 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
           sim = fma(wi, wi, sim);
           const int tl = t - t0;
           const long long off = wl.mode_major ? (long long)(tl >> 3) * tstep + (tl & 7) : (long long)t * wl.w_ld;
-          if (a.skip != 1) a.W[pd + off] = wr;
+          a.W[pd + off] = wr;
           if (SYM && cm >= 0) {
             const double vr = c2 * zr, vi = c2 * zi;
             sre = fma(vr, vr, sre);
             sim = fma(vi, vi, sim);
-            if (a.skip != 1) a.W[pm + off] = vr;
+            a.W[pm + off] = vr;
           }
         }
       }
