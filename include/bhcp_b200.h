@@ -193,6 +193,17 @@ int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev,
                              const int64_t* koff_dev, double* out_dev, int64_t batch,
                              void* stream);
 
+/* Relative residual of a pint-kind trajectory (replaces
+ * methods.residual / SolveResult.residual_norm, pkg/src/bhcp/methods.py:239-247,
+ * 281-285): result_host[0] = ||rhs - A y||, result_host[1] = ||rhs|| (plain
+ * 2-norms; the reference ratio is [0] / [1]). A y uses the backward-Euler
+ * rows, the corner 1/divisor and the Dirichlet Laplacian with mesh width h.
+ * ws: bhcp_residual_workspace_bytes() bytes of device memory. Synchronises. */
+size_t bhcp_residual_workspace_bytes(void);
+int bhcp_residual_norm(const bhcp_space_plan* sp, const double* y_dev, int64_t n_levels,
+                       double tau, double divisor, double h, const double* g_dev,
+                       void* ws, double* result_host, void* stream);
+
 /* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,
                    int elem_bytes, void* stream);

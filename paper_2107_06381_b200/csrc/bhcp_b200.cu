@@ -591,6 +591,90 @@ __global__ void k_transpose(const E* __restrict__ in, E* __restrict__ out, long 
   }
 }
 
+// ------------------------------------------------------------------ residual
+// Relative residual of the all-at-once system for the pint kinds
+// (methods.py:164-171, 239-247, residual_norm 281-285): r = rhs - A y with
+//   (A y)_0 = y_0 / tau + corner * y_N - lap y_0,   (A y)_t = (y_t - y_{t-1}) / tau - lap y_t,
+//   rhs_0 = g / divisor, rhs_t = 0, corner = 1 / divisor.
+// 3/5/7-point Dirichlet Laplacian on the interior grid. Each CTA writes the
+// partial sums of |r|^2 and |rhs|^2; k_residual_finish reduces them in a
+// fixed order (deterministic).
+struct ResidualArgs {
+  const double* y;
+  const double* g;
+  long long n, nx;
+  int m, dim;
+  double inv_tau, corner, inv_div, inv_h2;
+  double* partial;  // 2 * gridDim.x
+};
+
+__device__ __forceinline__ double lap_at(const double* __restrict__ f, long long x, int m, int dim, double inv_h2) {
+  // x = flattened interior index (C order)
+  double s;
+  if (dim == 1) {
+    const int i = (int)x;
+    s = -2.0 * f[x];
+    if (i > 0) s += f[x - 1];
+    if (i + 1 < m) s += f[x + 1];
+  } else if (dim == 2) {
+    const int i1 = (int)(x / m), i2 = (int)(x - (long long)i1 * m);
+    s = -4.0 * f[x];
+    if (i2 > 0) s += f[x - 1];
+    if (i2 + 1 < m) s += f[x + 1];
+    if (i1 > 0) s += f[x - m];
+    if (i1 + 1 < m) s += f[x + m];
+  } else {
+    const long long mm = (long long)m * m;
+    const int i1 = (int)(x / mm);
+    const long long r = x - i1 * mm;
+    const int i2 = (int)(r / m), i3 = (int)(r - (long long)i2 * m);
+    s = -6.0 * f[x];
+    if (i3 > 0) s += f[x - 1];
+    if (i3 + 1 < m) s += f[x + 1];
+    if (i2 > 0) s += f[x - m];
+    if (i2 + 1 < m) s += f[x + m];
+    if (i1 > 0) s += f[x - mm];
+    if (i1 + 1 < m) s += f[x + mm];
+  }
+  return s * inv_h2;
+}
+
+__global__ void __launch_bounds__(256) k_residual(ResidualArgs a) {
+  __shared__ double red[16];
+  double rr = 0.0, bb = 0.0;
+  const long long total = a.n * a.nx;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+    const long long t = i / a.nx, x = i - t * a.nx;
+    const double* yt = a.y + t * a.nx;
+    double ay = (t == 0) ? yt[x] * a.inv_tau + a.corner * a.y[(a.n - 1) * a.nx + x]
+                         : (yt[x] - yt[x - a.nx]) * a.inv_tau;
+    ay -= lap_at(yt, x, a.m, a.dim, a.inv_h2);
+    const double rhs = (t == 0) ? a.g[x] * a.inv_div : 0.0;
+    const double r = rhs - ay;
+    rr = fma(r, r, rr);
+    bb = fma(rhs, rhs, bb);
+  }
+  block_sum2(rr, bb, red);
+  if (threadIdx.x == 0) {
+    a.partial[2 * blockIdx.x] = rr;
+    a.partial[2 * blockIdx.x + 1] = bb;
+  }
+}
+
+__global__ void k_residual_finish(const double* __restrict__ partial, int nblk, double* out) {
+  __shared__ double red[64];
+  double rr = 0.0, bb = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    rr += partial[2 * i];
+    bb += partial[2 * i + 1];
+  }
+  block_sum2(rr, bb, red);
+  if (threadIdx.x == 0) {
+    out[0] = rr;
+    out[1] = bb;
+  }
+}
+
 }  // namespace bhcp
 
 // ====================================================================== host
@@ -1449,6 +1533,31 @@ int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
   if (rc) return rc;
   // step (c)
   return launch_time(tp, 1, S, 1, nx, 1, nx, y_dev, 0, 1, nx, st, s);
+}
+
+size_t bhcp_residual_workspace_bytes(void) { return sizeof(double) * (2 * 1184 + 2); }
+
+int bhcp_residual_norm(const bhcp_space_plan* sp, const double* y_dev, int64_t n_levels, double tau, double divisor,
+                       double h, const double* g_dev, void* ws, double* result_host, void* stream) {
+  if (!sp || !y_dev || !g_dev || !ws || !result_host || n_levels < 1) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  ResidualArgs a{};
+  a.y = y_dev; a.g = g_dev; a.n = n_levels; a.nx = sp->nx; a.m = sp->m; a.dim = sp->dim;
+  a.inv_tau = 1.0 / tau; a.corner = 1.0 / divisor; a.inv_div = 1.0 / divisor; a.inv_h2 = 1.0 / (h * h);
+  const int nblk = 1184;  // 8 x 148 SMs, fixed for a deterministic reduction order
+  double* part = (double*)ws;
+  a.partial = part;
+  k_residual<<<nblk, 256, 0, s>>>(a);
+  k_residual_finish<<<1, 1024, 0, s>>>(part, nblk, part + 2 * nblk);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_residual");
+  double out[2];
+  if (cudaMemcpyAsync(out, part + 2 * nblk, sizeof(out), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return cuda_fail("residual copy");
+  result_host[0] = sqrt(out[0]);
+  result_host[1] = sqrt(out[1]);
+  return BHCP_OK;
 }
 
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols, int elem_bytes, void* stream) {

@@ -192,6 +192,11 @@ class SolveResult:
         return self.trajectory[-1]
 
     def residual_norm(self) -> float:
-        if self.trajectory is None:
+        """Relative residual (methods.py:281-285). Device trajectories of the
+        pint kinds are checked on the GPU (one fused stencil pass)."""
+        if self._trajectory is None and self.trajectory_device is None:
             return float("nan")
+        if self.trajectory_device is not None and self.system.method.kind.is_circulant:
+            from .pint import device_residual_norm
+            return device_residual_norm(self.system, self.trajectory_device)
         return residual(self.system, self.trajectory)[1]

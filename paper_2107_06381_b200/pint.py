@@ -222,3 +222,19 @@ def solve_pint_unfused(system) -> SolveResult:
             f"imaginary residue {st.residue:.3e} exceeds {RESIDUE_TOL:.1e} of the result norm {st.norm:.3e}"
         )
     return SolveResult(system=system, trajectory=None, solver="pint-unfused", timings={}, trajectory_device=y)
+
+
+def device_residual_norm(system, y_dev: torch.Tensor) -> float:
+    """||rhs - A y|| / ||rhs|| on the device for a pint-kind system
+    (methods.py:239-247)."""
+    _check_kind(system)
+    lib = _lib.lib()
+    sp = plan_for(system.grid)
+    tau = system.timegrid.tau
+    divisor = condition_divisor(system.method.kind, system.method.alpha, tau)
+    g = plans.to_device(system.data, torch.float64)
+    ws = torch.empty(int(lib.bhcp_residual_workspace_bytes()), dtype=torch.uint8, device=y_dev.device)
+    out = (ctypes.c_double * 2)()
+    _lib.check(lib.bhcp_residual_norm(sp.handle, plans.ptr(y_dev), system.n_levels, tau, divisor, system.grid.h,
+                                      plans.ptr(g), plans.ptr(ws), out, plans.stream_handle()), "bhcp_residual_norm")
+    return float(out[0] / out[1]) if out[1] > 0 else float(out[0])

@@ -288,3 +288,24 @@ def test_deterministic_bits():
     a = B.solve_pint(system).trajectory
     b = B.solve_pint(system).trajectory
     assert np.array_equal(a, b)
+
+
+# ----------------------------------------------------------------- residual
+
+@pytest.mark.parametrize("dim,cells,steps", [(1, 16, 16), (2, 8, 8), (2, 20, 9), (3, 6, 5)])
+@pytest.mark.parametrize("kind", [B.MethodKind.PINT_QBVM, B.MethodKind.PINT_MQBVM])
+def test_device_residual_matches_host(dim, cells, steps, kind):
+    w = workloads.make_small(dim, cells, steps, seed=17)
+    grid = B.build_grid(dim, w.length, cells)
+    system = B.assemble(kind, 1e-2, grid, B.TimeGrid(w.horizon, steps), w.g_delta)
+    res = B.solve_pint(system)
+    dev = res.residual_norm()
+    host = B.residual(system, res.trajectory)[1]
+    assert dev == pytest.approx(host, rel=1e-6, abs=1e-15)
+    assert dev <= 1e-8 * max(1.0, abs(system.omega))
+    # a perturbed trajectory gives the host residual too
+    import torch
+    y = res.trajectory_device.clone()
+    y[1] += 1e-3
+    from paper_2107_06381_b200.pint import device_residual_norm
+    assert device_residual_norm(system, y) == pytest.approx(B.residual(system, y.cpu().numpy())[1], rel=1e-9)
