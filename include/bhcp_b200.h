@@ -204,6 +204,22 @@ int bhcp_residual_norm(const bhcp_space_plan* sp, const double* y_dev, int64_t n
                        double tau, double divisor, double h, const double* g_dev,
                        void* ws, double* result_host, void* stream);
 
+/* Closed-form per-mode solve of any of the four kinds (
+ * replaces baseline.solve_spectral_oracle, pkg/src/bhcp/baseline.py:67-112):
+ * y (num_steps+1, n_space) = DST(DST(g)/D_k * rho_k^t). kind: 0 qbvm,
+ * 1 mqbvm, 2 pint-qbvm, 3 pint-mqbvm. Verification / reference solver only;
+ * bhcp_pint_solve never uses it. */
+size_t bhcp_spectral_workspace_bytes(const bhcp_space_plan* sp, int64_t n_levels);
+int bhcp_spectral_solve(const bhcp_space_plan* sp, int kind, double alpha, double tau,
+                        int64_t num_steps, const double* g_dev, double* y_dev, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* Forward model in per-mode form (baseline.march_forward,
+ * baseline.py:115-129, equal to the N-step recursion to roundoff):
+ * g = DST(rho^N DST(z0)). */
+int bhcp_march_forward(const bhcp_space_plan* sp, double tau, int64_t num_steps,
+                       const double* z0_dev, double* g_dev, void* stream);
+
 /* Out-of-place transpose of a (rows, cols) matrix of 8- or 16-byte elements. */
 int bhcp_transpose(const void* in, void* out, int64_t rows, int64_t cols,
                    int elem_bytes, void* stream);

@@ -6,6 +6,7 @@ that belong to the hot path. Numerics run in libbhcp_b200.so (sm_100a); the
 package has no CPU fallback.
 """
 
+from .baseline import march_forward, solve_spectral_oracle
 from .circulant import (
     CirculantDiagonalization,
     ImaginaryResidueError,

@@ -71,6 +71,9 @@ SIGNATURES = {
     "bhcp_pint_level_pass": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "bhcp_pint_levels": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "bhcp_pint_levels_blocked": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
+    "bhcp_spectral_workspace_bytes": (ctypes.c_size_t, [_vp, _i64]),
+    "bhcp_spectral_solve": (_int, [_vp, _int, _dbl, _dbl, _i64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "bhcp_march_forward": (_int, [_vp, _dbl, _i64, _vp, _vp, _vp]),
     "bhcp_residual_workspace_bytes": (ctypes.c_size_t, []),
     "bhcp_residual_norm": (_int, [_vp, _vp, _i64, _dbl, _dbl, _dbl, _vp, _vp, _dp, _vp]),
     "bhcp_transpose": (_int, [_vp, _vp, _i64, _i64, _int, _vp]),

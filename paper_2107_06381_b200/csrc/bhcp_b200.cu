@@ -675,6 +675,46 @@ __global__ void k_residual_finish(const double* __restrict__ partial, int nblk, 
   }
 }
 
+// ------------------------------------------------------------------ closed form
+// Device form of the reference's per-mode closed-form solver
+// solve_spectral_oracle (baseline.py:67-112) and of march_forward's per-mode
+// identity (baseline.py:115-129): W(k, t) = amp_k * rho_k^t in the blocked
+// layout, then the same level passes as the solve. kind: 0 qbvm, 1 mqbvm,
+// 2 pint-qbvm, 3 pint-mqbvm (baseline.py:92-99 denominators).
+struct SpectralArgs {
+  const double* ghat;    // DST(data)
+  const double* mu1;
+  int m, dim, kind;
+  double alpha, tau;
+  long long num_steps, n;  // N and n = N + 1 (levels written: n)
+  double* W;
+  fastk::WLayout wl;
+};
+
+__global__ void k_spectral_w(SpectralArgs a, long long nx) {
+  for (long long k = blockIdx.x * (long long)blockDim.y + threadIdx.y; k < nx; k += (long long)gridDim.x * blockDim.y) {
+    const double mu = mode_mu(a.mu1, a.m, a.dim, k);
+    const double rho = 1.0 / (1.0 + a.tau * mu);
+    const double decay = pow(rho, (double)a.num_steps);
+    double denom;
+    if (a.kind == 0) denom = a.alpha + decay;
+    else if (a.kind == 1) denom = a.alpha * mu * rho + decay;
+    else if (a.kind == 2) denom = a.alpha * (1.0 + a.tau * mu) + decay;
+    else denom = a.alpha * (mu + 1.0 / a.tau) + decay;
+    const double amp = a.ghat[k] / denom;
+    for (long long t = threadIdx.x; t < a.n; t += blockDim.x)
+      a.W[a.wl.addr(k, (int)t)] = amp * pow(rho, (double)t);
+  }
+}
+
+// x_k <- x_k * rho_k^N  (march_forward in per-mode form, in place)
+__global__ void k_decay(double* x, const double* __restrict__ mu1, int m, int dim, double tau, double N, long long nx) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nx; k += (long long)gridDim.x * blockDim.x) {
+    const double rho = 1.0 / (1.0 + tau * mode_mu(mu1, m, dim, k));
+    x[k] *= pow(rho, N);
+  }
+}
+
 }  // namespace bhcp
 
 // ====================================================================== host
@@ -1533,6 +1573,47 @@ int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
   if (rc) return rc;
   // step (c)
   return launch_time(tp, 1, S, 1, nx, 1, nx, y_dev, 0, 1, nx, st, s);
+}
+
+size_t bhcp_spectral_workspace_bytes(const bhcp_space_plan* sp, int64_t n_levels) {
+  if (!sp) return 0;
+  return align256(sizeof(double) * sp->nx) + align256(sizeof(double) * native_w_elems(sp, (int)n_levels));
+}
+
+int bhcp_spectral_solve(const bhcp_space_plan* sp, int kind, double alpha, double tau, int64_t num_steps,
+                        const double* g_dev, double* y_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (!sp || !g_dev || !y_dev || !ws || kind < 0 || kind > 3 || num_steps < 1) return fail(BHCP_ERR_INVALID, "bad argument");
+  const long long n = num_steps + 1;
+  if (ws_bytes < bhcp_spectral_workspace_bytes(sp, n)) return fail(BHCP_ERR_INVALID, "workspace too small");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  double* ghat = (double*)ws;
+  double* W = (double*)((char*)ws + align256(sizeof(double) * sp->nx));
+  int rc = sine_passes(sp, g_dev, ghat, 0, 1, s);
+  if (rc) return rc;
+  SpectralArgs a{};
+  a.ghat = ghat; a.mu1 = sp->mu1_dev; a.m = sp->m; a.dim = sp->dim; a.kind = kind; a.alpha = alpha; a.tau = tau;
+  a.num_steps = num_steps; a.n = n; a.W = W; a.wl = native_layout(sp, sp->nx, (int)n);
+  k_spectral_w<<<2048, dim3(32, 8), 0, s>>>(a, sp->nx);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_spectral_w");
+  for (int p = 0; p < sp->dim; ++p) {
+    rc = level_pass(sp, W, nullptr, y_dev, n, p, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
+}
+
+int bhcp_march_forward(const bhcp_space_plan* sp, double tau, int64_t num_steps, const double* z0_dev,
+                       double* g_dev, void* stream) {
+  if (!sp || !z0_dev || !g_dev || num_steps < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  int rc = sine_passes(sp, z0_dev, g_dev, 0, 1, s);
+  if (rc) return rc;
+  k_decay<<<(unsigned)std::min<long long>((sp->nx + 255) / 256, 4096), 256, 0, s>>>(g_dev, sp->mu1_dev, sp->m, sp->dim,
+                                                                                   tau, (double)num_steps, sp->nx);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_decay");
+  return sine_passes(sp, g_dev, g_dev, 0, 1, s);
 }
 
 size_t bhcp_residual_workspace_bytes(void) { return sizeof(double) * (2 * 1184 + 2); }

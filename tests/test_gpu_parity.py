@@ -309,3 +309,61 @@ def test_device_residual_matches_host(dim, cells, steps, kind):
     y[1] += 1e-3
     from paper_2107_06381_b200.pint import device_residual_norm
     assert device_residual_norm(system, y) == pytest.approx(B.residual(system, y.cpu().numpy())[1], rel=1e-9)
+
+
+# ----------------------------------------------------------------- device closed form / forward model (8(f) f2, f3)
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("kind", list(B.MethodKind))
+def test_device_spectral_oracle_vs_reference(golden, name, kind):
+    dim, length, cells, horizon, steps, alpha = golden[f"case_{name}_params"]
+    grid = B.build_grid(int(dim), length, int(cells))
+    tg = B.TimeGrid(horizon, int(steps))
+    data = golden[f"case_{name}_data"]
+    y = B.solve_spectral_oracle(kind, alpha, grid, tg, data).trajectory
+    ref = O.spectral_oracle(kind.value, alpha, int(dim), length, int(cells), horizon, int(steps), data)
+    assert rel(y, ref) <= 1e-12
+    if kind.is_circulant:
+        assert rel(y, golden[f"oracle_{name}_{kind.value}"]) <= 1e-12
+
+
+def test_device_march_forward_vs_reference(golden):
+    """Per-mode forward model against the reference's N-step recursion."""
+    g = B.march_forward(golden["march_z0"], B.TimeGrid(0.1, 8), B.build_grid(2, 1.0, 8))
+    assert rel(g, golden["march_out"]) <= 1e-13
+    g1 = B.march_forward(golden["c1_z0"], B.TimeGrid(1.0, 256), B.build_grid(1, np.pi, 256))
+    assert rel(g1, golden["c1_g"]) <= 1e-13
+    gt = B.march_forward(torch.from_numpy(golden["c1_z0"]).cuda(), B.TimeGrid(1.0, 256), B.build_grid(1, np.pi, 256))
+    assert isinstance(gt, torch.Tensor) and gt.is_cuda
+
+
+def _chunked_rel(a, b, rows=64):
+    num = den = 0.0
+    for i in range(0, a.shape[0], rows):
+        num += torch.linalg.vector_norm(a[i:i + rows] - b[i:i + rows]).item() ** 2
+        den += torch.linalg.vector_norm(b[i:i + rows]).item() ** 2
+    return (num / den) ** 0.5
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_full_size_solve_vs_device_oracle(name):
+    """c3 / c4 at full size (1.07e9 / 4.26e9 DOF): the whole trajectory against
+    the device closed form, and sampled levels against the host oracle."""
+    from paper_2107_06381_b200 import pint as P
+    w = workloads.make(name)
+    grid = B.build_grid(w.dim, w.length, w.num_cells)
+    tg = B.TimeGrid(w.horizon, w.num_steps)
+    kind = B.MethodKind(w.kinds[0])
+    system = B.assemble(kind, w.alphas[0], grid, tg, w.g_delta)
+    y = B.solve_pint(system).trajectory_device
+    P._plan_cache.clear()
+    torch.cuda.empty_cache()
+    levels = np.array([0, w.num_steps // 3, w.num_steps])
+    ref_host = O.spectral_oracle(kind.value, w.alphas[0], w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
+                                 w.g_delta, levels=levels)
+    tol = O.parity_tolerance(tg.n_levels, system.omega)
+    assert rel(y[torch.from_numpy(levels).cuda()].cpu().numpy(), ref_host) <= tol
+    orc = B.solve_spectral_oracle(kind, w.alphas[0], grid, tg, w.g_delta).trajectory_device
+    assert _chunked_rel(y, orc) <= tol
+    del y, orc
+    torch.cuda.empty_cache()
