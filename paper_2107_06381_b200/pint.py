@@ -187,6 +187,7 @@ def solve_pint(system, backend: str = "spectral", workers: Optional[int] = None)
     _check_kind(system)
     if backend not in ("spectral", "banded"):
         raise ValueError(f"unknown backend {backend!r}")
+    _lib.lib()  # raises NativeLibraryError when the CUDA library cannot run here
     tau = system.timegrid.tau
     plan = pint_plan(system.grid, system.timegrid, system.omega)
     divisor = condition_divisor(system.method.kind, system.method.alpha, tau)
