@@ -14,6 +14,7 @@ import sys
 from pathlib import Path
 
 rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+extra = sys.argv[4:]  # optional further launch lists (e.g. the whole bench command), summarised too
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
@@ -37,7 +38,10 @@ for r in data:
     d["time_unit"] = units[idx["gpu__time_duration.sum"]]
     out_rows.append(d)
     name = d["Kernel Name"].split("(")[0].split("<")[0].replace("void ", "").strip()
-    traffic.setdefault(name, d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])
+    # keep the longest launch per kernel name (the level pass, not the ghat DST of g)
+    t = float(str(d["gpu__time_duration.sum"]).replace(",", ""))
+    if name not in traffic or t > traffic[name][0]:
+        traffic[name] = (t, d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"])
 with open(f"{prefix}_ncu_full.csv", "w", newline="") as f:
     w = csv.DictWriter(f, fieldnames=list(out_rows[0].keys()))
     w.writeheader()
@@ -59,6 +63,18 @@ lines = [f"# ncu summary ({Path(prefix).name})", "", "## Launch list (gpu__time_
          "| kernel | launches | total us | share |", "|---|---|---|---|"]
 for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
     lines.append(f"| {name} | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/tot*100:.1f}% |")
+for ex in extra:
+    shutil.copy(ex, f"{prefix}_{Path(ex).stem}.csv")
+    er = list(csv.reader(open(ex)))
+    eh = next(i for i, r in enumerate(er) if "Kernel Name" in r)
+    eagg = {}
+    for r in er[eh + 1:]:
+        if len(r) > vi:
+            eagg.setdefault(r[ki].split("(")[0].replace("void ", ""), []).append(float(r[vi].replace(",", "")))
+    etot = sum(sum(v) for v in eagg.values())
+    lines += ["", f"## Launch list of {Path(ex).name}", "", "| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for name, v in sorted(eagg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| {name} | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/etot*100:.1f}% |")
 lines += ["", "## --set full capture (one launch each)", "",
           "| kernel | time | DRAM read | DRAM write | DRAM % | SM % | L1 % | FP64 pipe % | IPC | warps % | regs |",
           "|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -74,5 +90,5 @@ for d in out_rows:
                  f"{d.get('launch__registers_per_thread','')} |")
 Path(f"{prefix}_summary.md").write_text("\n".join(lines) + "\n")
 tf = Path("profiles/ncu_traffic_c2.json")
-tf.write_text(json.dumps(traffic, indent=1) + "\n")
+tf.write_text(json.dumps({k: v[1] for k, v in traffic.items()}, indent=1) + "\n")
 print("\n".join(lines))
