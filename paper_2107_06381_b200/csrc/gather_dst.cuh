@@ -56,37 +56,53 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   constexpr int S = 4, T = PlanB2<N>::T, m = N - 1;
   constexpr int RUN = m * kTB;
   constexpr int KU = (N / 2) / 32;   // k values per lane (k = u*32 + lane)
-  using Lay = Interleaved<S, PlanB2<N>::R1>;
+  using Lay = Interleaved<S, 2>;   // pad every 2: conflict-free for q-fastest stages and lane-per-k reads
   extern __shared__ double2 smem[];
   double2* buf = smem;
   double* stage = reinterpret_cast<double*>(smem + Lay::words(N));
-  double* sn = stage + RUN;
+  double* sn = stage + RUN + 16;
+  double* carry = sn + N;           // 8 doubles: lower-half running sums per line
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
-  const long long ntiles = a.P * a.NT;
-  auto issue = [&](long long tile) {
-    const long long o = tile / a.NT, tt = tile - o * a.NT;
-    const long long k1 = o / a.idiv, r2 = o - k1 * a.idiv;
-    const long long kb = a.koff ? __ldg(a.koff + k1) : k1 * a.NT * a.P1 * kTB;
-    const double2* src = reinterpret_cast<const double2*>(a.in + kb + tt * a.P1 * kTB + r2 * (long long)m * kTB);
-    double2* dst = reinterpret_cast<double2*>(stage);
+  // Tiles are walked with 32-bit incremental (o, tt) / (k1, r2) counters
+  // instead of 64-bit divisions per tile.
+  const int NT = (int)a.NT, idiv = (int)a.idiv;
+  const int ntiles = (int)(a.P * a.NT);
+  const int gstep = gridDim.x, step_o = gstep / NT, step_t = gstep - step_o * NT;
+  // the stage copy is shifted so that smem and global addresses agree mod 128 B
+  // (a misaligned cp.async splits every 128 B line into two smem wavefronts)
+  auto src_of = [&](int o, int tt) -> const double* {
+    const int k1 = o / idiv, r2 = o - k1 * idiv;
+    const long long kb = a.koff ? __ldg(a.koff + k1) : (long long)k1 * a.NT * a.P1 * kTB;
+    return a.in + kb + (long long)tt * a.P1 * kTB + (long long)r2 * m * kTB;
+  };
+  auto issue = [&](const double* src_d) {
+    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(stage));
+    const int soff = (int)(((static_cast<unsigned>(reinterpret_cast<uintptr_t>(src_d)) - sbase) & 127u) >> 3);
+    const double2* src = reinterpret_cast<const double2*>(src_d);
+    double2* dst = reinterpret_cast<double2*>(stage + soff);
     for (int i = threadIdx.x; i < RUN / 2; i += T) {
       const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + i));
     }
     cp_async_commit();
+    return soff;
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  long long tile = blockIdx.x;
-  if (tile < ntiles) issue(tile);
-  for (; tile < ntiles; tile += gridDim.x) {
-    const long long o = tile / a.NT, tt = tile - o * a.NT;
+  int tile = blockIdx.x;
+  int o = tile / NT, tt = tile - o * NT;
+  int soff = 0;
+  if (tile < ntiles) soff = issue(src_of(o, tt));
+  for (; tile < ntiles; tile += gstep) {
+    int no = o + step_o, ntt = tt + step_t;
+    if (ntt >= NT) { ntt -= NT; ++no; }
     cp_async_wait_all();
     __syncthreads();
-    const long long tvalid = a.nlev - tt * kTB;
+    const long long tvalid = a.nlev - (long long)tt * kTB;
+    const double* st = stage + soff;
     auto gen = [&](int q, int j) -> double2 {
       if (j == 0) return make_double2(0.0, 0.0);
-      double2 p = *reinterpret_cast<const double2*>(stage + (j - 1) * kTB + 2 * q);      // x_j
-      double2 r = *reinterpret_cast<const double2*>(stage + (N - j - 1) * kTB + 2 * q);  // x_{N-j}
+      double2 p = *reinterpret_cast<const double2*>(st + (j - 1) * kTB + 2 * q);      // x_j
+      double2 r = *reinterpret_cast<const double2*>(st + (N - j - 1) * kTB + 2 * q);  // x_{N-j}
       if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
       if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
       const double s = sn[j];
@@ -94,45 +110,74 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
     };
     using Ff = typename PlanB2<N>::template F<Lay>;
     Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first(buf, gen);
-    if (tile + gridDim.x < ntiles) issue(tile + gridDim.x);
+    const int cur_o = o, cur_tt = tt;
+    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt));
+    o = no; tt = ntt;
     auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
     FftTail<Ff>::run(buf, a.tw, sink);
     __syncthreads();
-    // one warp per output line; k = u*32 + lane, running prefix across u
-    for (int li = warp; li < kTB; li += T / 32) {
-      const long long t = tt * kTB + li;
-      if (t >= a.nlev) continue;
-      const int q = li >> 1;
-      const bool isb = li & 1;
-      double* __restrict__ dst = a.out + (t * a.P + o) * m;
-      double carry = 0.0, c0 = 0.0;
+    // Post-processing: warp w takes sequence q = w & 3 (lines 2q, 2q+1) and
+    // the half h = w >> 2 of the k range; k = (h*KH + u)*32 + lane. Each U_k,
+    // U_{N-k} load serves both lines. The upper half waits for the lower
+    // half's running sums (named barrier 1+q, producer/consumer).
+    {
+      static_assert(T == 256, "post-processing assumes 8 warps");
+      constexpr int KH = KU / 2;
+      const int q = warp & 3, h = warp >> 2;
+      const long long ta = (long long)cur_tt * kTB + 2 * q;
+      const double2 U0 = buf[Lay::addr(q, 0)];
+      const double c0a = U0.x, c0b = U0.y;       // Re U^a_0, Re U^b_0
+      double ca = 0.0, cb = 0.0;
+      double oa[KH], ob[KH], ea[KH], eb[KH];
 #pragma unroll
-      for (int u = 0; u < KU; ++u) {
-        const int k = u * 32 + lane;
+      for (int u = 0; u < KH; ++u) {
+        const int k = (h * KH + u) * 32 + lane;
         const double2 A = buf[Lay::addr(q, k)];
         const double2 Bv = buf[Lay::addr(q, (N - k) & (N - 1))];
-        double ur, ui;
-        if (!isb) { ur = 0.5 * (A.x + Bv.x); ui = 0.5 * (A.y - Bv.y); }
-        else { ur = 0.5 * (A.y + Bv.y); ui = -0.5 * (A.x - Bv.x); }
-        if (u == 0) c0 = __shfl_sync(0xffffffffu, ur, 0);
-        double incl = ur;
+        double ia = 0.5 * (A.x + Bv.x), ib = 0.5 * (A.y + Bv.y);   // Re U^a_k, Re U^b_k
+        ea[u] = -0.5 * (A.y - Bv.y);                                 // S^a_{2k}
+        eb[u] = 0.5 * (A.x - Bv.x);                                  // S^b_{2k}
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
-          const double v = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += v;
+          const double va = __shfl_up_sync(0xffffffffu, ia, off);
+          const double vb = __shfl_up_sync(0xffffffffu, ib, off);
+          if (lane >= off) { ia += va; ib += vb; }
         }
-        const double odd = carry + incl - 0.5 * c0;       // S_{2k+1}
-        carry += __shfl_sync(0xffffffffu, incl, 31);
-        if (k >= 1) dst[2 * k - 1] = a.scale * (-ui);     // S_{2k}
-        dst[2 * k] = a.scale * odd;
+        oa[u] = ca + ia;
+        ob[u] = cb + ib;
+        ca += __shfl_sync(0xffffffffu, ia, 31);
+        cb += __shfl_sync(0xffffffffu, ib, 31);
+      }
+      if (h == 0) {
+        if (lane == 0) { carry[2 * q] = ca; carry[2 * q + 1] = cb; }
+        __threadfence_block();
+        asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
+        ca = 0.0; cb = 0.0;
+      } else {
+        asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+        ca = carry[2 * q]; cb = carry[2 * q + 1];
+      }
+#pragma unroll
+      for (int line = 0; line < 2; ++line) {
+        const long long t = ta + line;
+        if (t >= a.nlev) continue;
+        double* __restrict__ dst = a.out + (t * a.P + cur_o) * m;
+        const double cc = line ? cb : ca, hc = 0.5 * (line ? c0b : c0a);
+#pragma unroll
+        for (int u = 0; u < KH; ++u) {
+          const int k = (h * KH + u) * 32 + lane;
+          const double odd = (cc + (line ? ob[u] : oa[u])) - hc;   // S_{2k+1}
+          if (k >= 1) dst[2 * k - 1] = a.scale * (line ? eb[u] : ea[u]);
+          dst[2 * k] = a.scale * odd;
+        }
       }
     }
   }
 }
 
 template <int N> constexpr size_t smemB2_bytes() {
-  using Lay = Interleaved<4, PlanB2<N>::R1>;
-  return sizeof(double2) * Lay::words(N) + sizeof(double) * ((N - 1) * kTB + N);
+  using Lay = Interleaved<4, 2>;
+  return sizeof(double2) * Lay::words(N) + sizeof(double) * ((N - 1) * kTB + 16 + N + 8);
 }
 
 }  // namespace gdst
