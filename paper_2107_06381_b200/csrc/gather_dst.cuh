@@ -10,6 +10,15 @@
 #pragma once
 #include "static_fft.cuh"
 
+#ifndef BHCP_C3_MINB
+#define BHCP_C3_MINB 2
+#endif
+#ifndef BHCP_COLS_NOFFT
+#define BHCP_COLS_NOFFT 0
+#endif
+#ifndef BHCP_COLS_DIRECT
+#define BHCP_COLS_DIRECT 0
+#endif
 namespace bhcp {
 namespace gdst {
 
@@ -47,11 +56,27 @@ struct ArgsB2 {
   const double2* tw;      // exp(-2 pi i k / N)
   const double* sn;       // sin(pi j / N)
   double scale;           // sqrt(2/N)
+  // MODE 0 (blocked W -> rows of y)
   const long long* koff;
   long long NT, P1, idiv, P, nlev;
+  // MODE 1 (columns of y, in place): lines i in [0, ni) adjacent, element
+  // stride es = ni, outer blocks o in [0, no) at stride m * ni
+  long long ni, no;
 };
 
-template <int N>
+__device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0));
+}
+
+// MODE 0: first level pass from the blocked W. A tile is one spatial line
+//   (k1, r2) x 8 levels, a contiguous 8*m-double run of W; the 8 output
+//   lines are rows of y.
+// MODE 1: a later level pass, in place on y. A tile is 8 adjacent lines
+//   (columns i0..i0+7) x m elements at stride ni: 64 B per element row, all
+//   rows in flight through cp.async. The outputs go back through shared
+//   memory and leave as 64 B row chunks.
+template <int N, int MODE>
 __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   constexpr int S = 4, T = PlanB2<N>::T, m = N - 1;
   constexpr int RUN = m * kTB;
@@ -63,19 +88,38 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   double* sn = stage + RUN + 16;
   double* carry = sn + N;           // 8 doubles: lower-half running sums per line
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
-  // Tiles are walked with 32-bit incremental (o, tt) / (k1, r2) counters
-  // instead of 64-bit divisions per tile.
-  const int NT = (int)a.NT, idiv = (int)a.idiv;
-  const int ntiles = (int)(a.P * a.NT);
+  // Tiles are walked with 32-bit incremental counters (o, tt): MODE 0 (line,
+  // level tile), MODE 1 (outer block, column block).
+  const int NT = MODE == 0 ? (int)a.NT : (int)((a.ni + kTB - 1) / kTB);
+  const int idiv = (int)a.idiv;
+  const int ntiles = MODE == 0 ? (int)(a.P * a.NT) : (int)(a.no * NT);
   const int gstep = gridDim.x, step_o = gstep / NT, step_t = gstep - step_o * NT;
-  // the stage copy is shifted so that smem and global addresses agree mod 128 B
-  // (a misaligned cp.async splits every 128 B line into two smem wavefronts)
+  // MODE 0: the stage copy is shifted so that smem and global addresses agree
+  // mod 128 B (a misaligned cp.async splits every 128 B line into two smem
+  // wavefronts).
   auto src_of = [&](int o, int tt) -> const double* {
+    if (MODE == 1) return a.in + (long long)o * m * a.ni + (long long)tt * kTB;
     const int k1 = o / idiv, r2 = o - k1 * idiv;
     const long long kb = a.koff ? __ldg(a.koff + k1) : (long long)k1 * a.NT * a.P1 * kTB;
     return a.in + kb + (long long)tt * a.P1 * kTB + (long long)r2 * m * kTB;
   };
-  auto issue = [&](const double* src_d) {
+  auto issue = [&](const double* src_d, int tt) {
+    if (MODE == 1) {
+      const int nval = (int)min((long long)kTB, a.ni - (long long)tt * kTB);
+      if (nval == kTB) {
+        for (int i = threadIdx.x; i < RUN; i += T) {
+          const int e = i >> 3, l = i & 7;
+          cp_async8(stage + i, src_d + (long long)e * a.ni + l);
+        }
+      } else {
+        for (int i = threadIdx.x; i < RUN; i += T) {
+          const int e = i >> 3, l = i & 7;
+          cp_async8_zfill(stage + i, src_d + (long long)e * a.ni + (l < nval ? l : 0), l < nval);
+        }
+      }
+      cp_async_commit();
+      return 0;
+    }
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(stage));
     const int soff = (int)(((static_cast<unsigned>(reinterpret_cast<uintptr_t>(src_d)) - sbase) & 127u) >> 3);
     const double2* src = reinterpret_cast<const double2*>(src_d);
@@ -91,27 +135,55 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   int tile = blockIdx.x;
   int o = tile / NT, tt = tile - o * NT;
   int soff = 0;
-  if (tile < ntiles) soff = issue(src_of(o, tt));
+  if (tile < ntiles) soff = issue(src_of(o, tt), tt);
   for (; tile < ntiles; tile += gstep) {
     int no = o + step_o, ntt = tt + step_t;
     if (ntt >= NT) { ntt -= NT; ++no; }
     cp_async_wait_all();
     __syncthreads();
-    const long long tvalid = a.nlev - (long long)tt * kTB;
+    const long long tvalid = MODE == 0 ? a.nlev - (long long)tt * kTB : (long long)kTB;
     const double* st = stage + soff;
     auto gen = [&](int q, int j) -> double2 {
       if (j == 0) return make_double2(0.0, 0.0);
       double2 p = *reinterpret_cast<const double2*>(st + (j - 1) * kTB + 2 * q);      // x_j
       double2 r = *reinterpret_cast<const double2*>(st + (N - j - 1) * kTB + 2 * q);  // x_{N-j}
-      if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
-      if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
+      if (MODE == 0) {
+        if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
+        if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
+      }
       const double s = sn[j];
       return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
     };
     using Ff = typename PlanB2<N>::template F<Lay>;
+#if BHCP_COLS_NOFFT
+    if (MODE == 1) {
+      for (int i = threadIdx.x; i < m * S; i += T) {
+        const int e = i >> 2, q = i & 3;
+        buf[Lay::addr(q, e)] = *reinterpret_cast<const double2*>(st + e * kTB + 2 * q);
+      }
+      const int cur_o = o, cur_tt = tt;
+#if BHCP_COLS_NOFFT == 1
+      if (tile + gstep < ntiles) soff = issue(src_of(no, ntt), ntt);
+#endif
+      o = no; tt = ntt;
+      __syncthreads();
+      double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB;
+      const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
+      // lane -> (row e, line l): 8 lanes write one contiguous 64 B row chunk
+      const double* bufd = reinterpret_cast<const double*>(buf);
+      for (int i = threadIdx.x; i < m * kTB; i += T) {
+        const int e = i >> 3, l = i & 7;
+        if (l < nval) base[(long long)e * a.ni + l] = bufd[2 * Lay::addr(l >> 1, e) + (l & 1)];
+      }
+#if BHCP_COLS_NOFFT == 2
+      if (tile + gstep < ntiles) soff = issue(src_of(o, tt), tt);
+#endif
+      continue;
+    }
+#endif
     Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first(buf, gen);
     const int cur_o = o, cur_tt = tt;
-    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt));
+    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt), ntt);
     o = no; tt = ntt;
     auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
     FftTail<Ff>::run(buf, a.tw, sink);
@@ -119,12 +191,11 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
     // Post-processing: warp w takes sequence q = w & 3 (lines 2q, 2q+1) and
     // the half h = w >> 2 of the k range; k = (h*KH + u)*32 + lane. Each U_k,
     // U_{N-k} load serves both lines. The upper half waits for the lower
-    // half's running sums (named barrier 1+q, producer/consumer).
+    // half's running sums (named barrier 1+q).
     {
       static_assert(T == 256, "post-processing assumes 8 warps");
       constexpr int KH = KU / 2;
       const int q = warp & 3, h = warp >> 2;
-      const long long ta = (long long)cur_tt * kTB + 2 * q;
       const double2 U0 = buf[Lay::addr(q, 0)];
       const double c0a = U0.x, c0b = U0.y;       // Re U^a_0, Re U^b_0
       double ca = 0.0, cb = 0.0;
@@ -148,28 +219,190 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
         ca += __shfl_sync(0xffffffffu, ia, 31);
         cb += __shfl_sync(0xffffffffu, ib, 31);
       }
+      // MODE 1 overwrites buf with the outputs, so both warps of the pair
+      // must have finished reading: full pair barrier instead of arrive/sync.
       if (h == 0) {
         if (lane == 0) { carry[2 * q] = ca; carry[2 * q + 1] = cb; }
         __threadfence_block();
-        asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
+        if (MODE == 0) asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
+        else asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
         ca = 0.0; cb = 0.0;
       } else {
         asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
         ca = carry[2 * q]; cb = carry[2 * q + 1];
       }
+      const double ha = 0.5 * c0a, hb = 0.5 * c0b;
+      if (MODE == 0) {
 #pragma unroll
-      for (int line = 0; line < 2; ++line) {
-        const long long t = ta + line;
-        if (t >= a.nlev) continue;
-        double* __restrict__ dst = a.out + (t * a.P + cur_o) * m;
-        const double cc = line ? cb : ca, hc = 0.5 * (line ? c0b : c0a);
+        for (int line = 0; line < 2; ++line) {
+          const long long t = (long long)cur_tt * kTB + 2 * q + line;
+          if (t >= a.nlev) continue;
+          double* __restrict__ dst = a.out + (t * a.P + cur_o) * m;
+          const double cc = line ? cb : ca, hc = line ? hb : ha;
+#pragma unroll
+          for (int u = 0; u < KH; ++u) {
+            const int k = (h * KH + u) * 32 + lane;
+            const double odd = (cc + (line ? ob[u] : oa[u])) - hc;   // S_{2k+1}
+            if (k >= 1) dst[2 * k - 1] = a.scale * (line ? eb[u] : ea[u]);
+            dst[2 * k] = a.scale * odd;
+          }
+        }
+      } else if (BHCP_COLS_DIRECT) {
+        double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB + 2 * q;
+        const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
 #pragma unroll
         for (int u = 0; u < KH; ++u) {
           const int k = (h * KH + u) * 32 + lane;
-          const double odd = (cc + (line ? ob[u] : oa[u])) - hc;   // S_{2k+1}
-          if (k >= 1) dst[2 * k - 1] = a.scale * (line ? eb[u] : ea[u]);
-          dst[2 * k] = a.scale * odd;
+          double* d0 = base + (long long)(2 * k) * a.ni;
+          if (k >= 1) {
+            double* d1 = d0 - a.ni;
+            if (2 * q < nval) d1[0] = a.scale * ea[u];
+            if (2 * q + 1 < nval) d1[1] = a.scale * eb[u];
+          }
+          if (2 * q < nval) d0[0] = a.scale * ((ca + oa[u]) - ha);
+          if (2 * q + 1 < nval) d0[1] = a.scale * ((cb + ob[u]) - hb);
         }
+      } else {
+        // outputs (line a, line b) of element p at buf[addr(q, p)]
+#pragma unroll
+        for (int u = 0; u < KH; ++u) {
+          const int k = (h * KH + u) * 32 + lane;
+          if (k >= 1) buf[Lay::addr(q, 2 * k - 1)] = make_double2(a.scale * ea[u], a.scale * eb[u]);
+          buf[Lay::addr(q, 2 * k)] = make_double2(a.scale * ((ca + oa[u]) - ha), a.scale * ((cb + ob[u]) - hb));
+        }
+      }
+    }
+    if (MODE == 1 && !BHCP_COLS_DIRECT) {
+      __syncthreads();
+      double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB;
+      const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
+      // lane -> (row e, line l): 8 lanes write one contiguous 64 B row chunk
+      const double* bufd = reinterpret_cast<const double*>(buf);
+      for (int i = threadIdx.x; i < m * kTB; i += T) {
+        const int e = i >> 3, l = i & 7;
+        if (l < nval) base[(long long)e * a.ni + l] = bufd[2 * Lay::addr(l >> 1, e) + (l & 1)];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_dst_cols3: DST-I along a strided axis, in place capable, for real fields
+// (level passes >= 1 and the ghat transform). A tile is 2S adjacent lines
+// (columns i0 .. i0+2S-1, 2S*8 = 256 / 128 / 64 B per element row for
+// N = 256 / 512 / 1024) x m elements at stride ni. Everything happens in ONE
+// dense shared buffer of S*N complex values (64 KB), so three CTAs fit per SM
+// and 192 KB of rows are in flight per SM:
+//   1. cp.async 8 B: x(e, l) -> double (e+1)*2S + l, i.e. complex slot
+//      (q = l/2, idx = e+1) of the interleaved layout (idx*S + q)
+//   2. half-length real DST as in k_dst_blk2, first stage in place
+//   3. post-processing with lanes over (q, k): lane = q + S*kk, so a warp
+//      reads whole 16*S-byte rows (conflict-free) and the running sum over k
+//      needs log2(32/S) shuffle steps; warp totals are combined in smem
+//   4. outputs back into the buffer, then 2S*8-byte row chunks to global.
+template <int N> struct PlanC3;
+template <> struct PlanC3<256> { static constexpr int S = 16; template <class Lay> using F = Fft<256, 16, 256, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
+template <> struct PlanC3<512> { static constexpr int S = 8; template <class Lay> using F = Fft<512, 8, 256, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
+template <> struct PlanC3<1024> { static constexpr int S = 4; template <class Lay> using F = Fft<1024, 4, 256, Lay, 16, 8, 8>; static constexpr int R1 = 16; };
+
+template <int N> constexpr size_t smemC3_bytes() {
+  return sizeof(double2) * (PlanC3<N>::S * N) + sizeof(double) * (N + 2 * 8 * PlanC3<N>::S);
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, BHCP_C3_MINB) k_dst_cols3(ArgsB2 a) {
+  constexpr int S = PlanC3<N>::S, T = 256, m = N - 1, LW = 2 * S;   // LW lines per tile
+  constexpr int KK = 32 / S;                 // k values per warp step
+  constexpr int KW = (N / 2) / 8;            // k values per warp (8 warps)
+  constexpr int STEPS = KW / KK;
+  using Lay = Interleaved<S>;
+  extern __shared__ double2 smem[];
+  double2* buf = smem;
+  double* bufd = reinterpret_cast<double*>(smem);
+  double* sn = reinterpret_cast<double*>(smem + S * N);
+  double* tot = sn + N;                       // [8 warps][S q][2 lines]
+  for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
+  const int NT = (int)((a.ni + LW - 1) / LW);
+  const int ntiles = (int)(a.no * NT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = lane % S, kk = lane / S;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int o = tile / NT, cb = tile - o * NT;
+    const long long i0 = (long long)cb * LW;
+    const int nval = (int)min((long long)LW, a.ni - i0);
+    const double* src = a.in + (long long)o * m * a.ni + i0;
+    double* dst = a.out + (long long)o * m * a.ni + i0;
+    __syncthreads();   // previous tile's copy-out done with buf
+    if (nval == LW) {
+      for (int i = threadIdx.x; i < m * LW; i += T) {
+        const int e = i / LW, l = i - e * LW;
+        cp_async8(bufd + (e + 1) * LW + l, src + (long long)e * a.ni + l);
+      }
+    } else {
+      for (int i = threadIdx.x; i < m * LW; i += T) {
+        const int e = i / LW, l = i - e * LW;
+        cp_async8_zfill(bufd + (e + 1) * LW + l, src + (long long)e * a.ni + (l < nval ? l : 0), l < nval);
+      }
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    auto gen = [&](int qg, int j) -> double2 {
+      if (j == 0) return make_double2(0.0, 0.0);
+      const double2 p = buf[Lay::addr(qg, j)];       // x_j (lines 2q, 2q+1)
+      const double2 r = buf[Lay::addr(qg, N - j)];   // x_{N-j}
+      const double s = sn[j];
+      return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
+    };
+    using Ff = typename PlanC3<N>::template F<Lay>;
+    Stage<N, S, T, Lay, PlanC3<N>::R1, 1>::first_inplace(buf, gen);
+    auto sink = [&](int qs, int idx, double2 X) { buf[Lay::addr(qs, idx)] = X; };
+    FftTail<Ff>::run(buf, a.tw, sink);
+    __syncthreads();
+    // post-processing: warp w covers k in [w*KW, (w+1)*KW), lane (q, kk)
+    const double2 U0 = buf[Lay::addr(q, 0)];
+    double ca = 0.0, cb2 = 0.0;
+    double oa[STEPS], ob[STEPS], ea[STEPS], eb[STEPS];
+#pragma unroll
+    for (int u = 0; u < STEPS; ++u) {
+      const int k = warp * KW + u * KK + kk;
+      const double2 A = buf[Lay::addr(q, k)];
+      const double2 Bv = buf[Lay::addr(q, (N - k) & (N - 1))];
+      double ia = 0.5 * (A.x + Bv.x), ib = 0.5 * (A.y + Bv.y);
+      ea[u] = -0.5 * (A.y - Bv.y);
+      eb[u] = 0.5 * (A.x - Bv.x);
+#pragma unroll
+      for (int off = S; off < 32; off <<= 1) {
+        const double va = __shfl_up_sync(0xffffffffu, ia, off);
+        const double vb = __shfl_up_sync(0xffffffffu, ib, off);
+        if (lane >= off) { ia += va; ib += vb; }
+      }
+      oa[u] = ca + ia;
+      ob[u] = cb2 + ib;
+      ca += __shfl_sync(0xffffffffu, ia, q + 32 - S);
+      cb2 += __shfl_sync(0xffffffffu, ib, q + 32 - S);
+    }
+    if (kk == 0) { tot[(warp * S + q) * 2] = ca; tot[(warp * S + q) * 2 + 1] = cb2; }
+    __syncthreads();   // all U reads done; warp totals visible
+    double pa = 0.0, pb = 0.0;
+    for (int w = 0; w < warp; ++w) { pa += tot[(w * S + q) * 2]; pb += tot[(w * S + q) * 2 + 1]; }
+    const double ha = 0.5 * U0.x, hb = 0.5 * U0.y;
+#pragma unroll
+    for (int u = 0; u < STEPS; ++u) {
+      const int k = warp * KW + u * KK + kk;
+      if (k >= 1) buf[Lay::addr(q, 2 * k - 1)] = make_double2(a.scale * ea[u], a.scale * eb[u]);
+      buf[Lay::addr(q, 2 * k)] = make_double2(a.scale * ((pa + oa[u]) - ha), a.scale * ((pb + ob[u]) - hb));
+    }
+    __syncthreads();
+    if (nval == LW) {
+      for (int i = threadIdx.x; i < m * LW; i += T) {
+        const int e = i / LW, l = i - e * LW;
+        dst[(long long)e * a.ni + l] = bufd[e * LW + l];
+      }
+    } else {
+      for (int i = threadIdx.x; i < m * LW; i += T) {
+        const int e = i / LW, l = i - e * LW;
+        if (l < nval) dst[(long long)e * a.ni + l] = bufd[e * LW + l];
       }
     }
   }

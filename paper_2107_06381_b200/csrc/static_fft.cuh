@@ -239,6 +239,37 @@ struct Stage {
     __syncthreads();
   }
 
+  // first stage in place: gen reads buf itself, so all loads finish (CTA
+  // barrier) before any store.
+  template <class Gen>
+  static __device__ __forceinline__ void first_inplace(double2* buf, Gen& gen) {
+    static_assert(Ns == 1, "first stage");
+    double2 v[PER][R];
+    int qq[PER], jj[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = threadIdx.x + i * T;
+      if (FULL || b < NB) {
+        int q, j;
+        Lay::split(b, L / R, q, j);
+        qq[i] = q; jj[i] = j;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[i][r] = gen(q, j + r * (L / R));
+        Cod<R>::run(v[i]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int b = threadIdx.x + i * T;
+      if (FULL || b < NB) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[Lay::template addr_first<R>(qq[i], jj[i] * R, r)] = v[i][r];
+      }
+    }
+    __syncthreads();
+  }
+
   // last stage (Ns * R == L): outputs to sink(q, idx, value)
   template <class Sink>
   static __device__ __forceinline__ void last(double2* buf, const double2* __restrict__ tw, Sink& sink) {
