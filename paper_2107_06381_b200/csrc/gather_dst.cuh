@@ -333,16 +333,17 @@ __global__ void __launch_bounds__(256, BHCP_C3_MINB) k_dst_cols3(ArgsB2 a) {
     const double* src = a.in + (long long)o * m * a.ni + i0;
     double* dst = a.out + (long long)o * m * a.ni + i0;
     __syncthreads();   // previous tile's copy-out done with buf
-    if (nval == LW) {
-      for (int i = threadIdx.x; i < m * LW; i += T) {
-        const int e = i / LW, l = i - e * LW;
-        cp_async8(bufd + (e + 1) * LW + l, src + (long long)e * a.ni + l);
-      }
+    // thread -> fixed line l, rows e = e0, e0 + T/LW, ... (pointer increments only)
+    constexpr int RSTEP = T / LW;
+    const int l = threadIdx.x % LW, e0 = threadIdx.x / LW;
+    const long long gstep_rows = (long long)RSTEP * a.ni;
+    if (l < nval) {
+      const double* g = src + (long long)e0 * a.ni + l;
+      double* sdst = bufd + (e0 + 1) * LW + l;
+      for (int e = e0; e < m; e += RSTEP, g += gstep_rows, sdst += RSTEP * LW) cp_async8(sdst, g);
     } else {
-      for (int i = threadIdx.x; i < m * LW; i += T) {
-        const int e = i / LW, l = i - e * LW;
-        cp_async8_zfill(bufd + (e + 1) * LW + l, src + (long long)e * a.ni + (l < nval ? l : 0), l < nval);
-      }
+      double* sdst = bufd + (e0 + 1) * LW + l;
+      for (int e = e0; e < m; e += RSTEP, sdst += RSTEP * LW) *sdst = 0.0;
     }
     cp_async_commit();
     cp_async_wait_all();
@@ -394,16 +395,10 @@ __global__ void __launch_bounds__(256, BHCP_C3_MINB) k_dst_cols3(ArgsB2 a) {
       buf[Lay::addr(q, 2 * k)] = make_double2(a.scale * ((pa + oa[u]) - ha), a.scale * ((pb + ob[u]) - hb));
     }
     __syncthreads();
-    if (nval == LW) {
-      for (int i = threadIdx.x; i < m * LW; i += T) {
-        const int e = i / LW, l = i - e * LW;
-        dst[(long long)e * a.ni + l] = bufd[e * LW + l];
-      }
-    } else {
-      for (int i = threadIdx.x; i < m * LW; i += T) {
-        const int e = i / LW, l = i - e * LW;
-        if (l < nval) dst[(long long)e * a.ni + l] = bufd[e * LW + l];
-      }
+    if (l < nval) {
+      double* g = dst + (long long)e0 * a.ni + l;
+      const double* s = bufd + e0 * LW + l;
+      for (int e = e0; e < m; e += RSTEP, g += gstep_rows, s += RSTEP * LW) *g = *s;
     }
   }
 }
