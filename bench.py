@@ -252,7 +252,7 @@ def main():
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
         names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"] + \
-                [("k_dst_blk2" if a == 0 else "k_dst_cols_fast") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
+                [("k_dst_blk2" if a == 0 else "k_dst_cols3") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof

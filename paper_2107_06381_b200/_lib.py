@@ -16,9 +16,6 @@ from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libbhcp_b200.so"
-# Experiment builds (tools/) may point at another in-tree build of the same ABI.
-if os.environ.get("BHCP_LIB_VARIANT"):
-    LIB_PATH = _HERE / f"libbhcp_b200_{os.environ['BHCP_LIB_VARIANT']}.so"
 HEADER_PATH = _HERE.parent / "include" / "bhcp_b200.h"
 
 BHCP_OK = 0

@@ -808,15 +808,13 @@ void set_all_attributes() {
   allow_smem(fastk::k_modes_blue<1025, true>);
   allow_smem(fastk::k_modes_blue<4097, false>);
   allow_smem(fastk::k_modes_blue<4097, true>);
-  allow_smem(gdst::k_dst_blk2<256, 0>);
-  allow_smem(gdst::k_dst_blk2<512, 0>);
-  allow_smem(gdst::k_dst_blk2<1024, 0>);
+  allow_smem(gdst::k_dst_blk2<256>);
+  allow_smem(gdst::k_dst_blk2<512>);
+  allow_smem(gdst::k_dst_blk2<1024>);
   allow_smem(gdst::k_dst_cols3<256>);
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
-  allow_smem(gdst::k_dst_blk2<256, 1>);
-  allow_smem(gdst::k_dst_blk2<512, 1>);
-  allow_smem(gdst::k_dst_blk2<1024, 1>);
+
   allow_smem(fastk::k_modes_fast<513, false>);
   allow_smem(fastk::k_modes_fast<513, true>);
 }
@@ -867,7 +865,6 @@ void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cpl
 
 bool fast_dst_length(int L) { return L == 512 || L == 1024 || L == 2048 || L == 8192; }
 bool g_disable_fast = false;
-bool g_cols_blk2 = false;   // BHCP_COLS_BLK2=1: strided passes with k_dst_blk2 MODE 1 instead of k_dst_cols3
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -1187,15 +1184,15 @@ __global__ void k_unpack_blocked(const double* __restrict__ in, const long long*
   }
 }
 
-template <int N, int MODE>
+template <int N>
 int blk2_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
   using namespace gdst;
-  const long long tiles = MODE == 0 ? a.P * a.NT : a.no * ((a.ni + kTB - 1) / kTB);
+  const long long tiles = a.P * a.NT;
   if (tiles == 0) return BHCP_OK;
   if (tiles > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "too many tiles");
   const size_t sm = gdst::smemB2_bytes<N>();
-  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_blk2<N, MODE>, PlanB2<N>::T, sm));
-  k_dst_blk2<N, MODE><<<(unsigned)grid, PlanB2<N>::T, sm, s>>>(a);
+  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_blk2<N>, PlanB2<N>::T, sm));
+  k_dst_blk2<N><<<(unsigned)grid, PlanB2<N>::T, sm, s>>>(a);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk2 launch");
   return BHCP_OK;
 }
@@ -1213,22 +1210,16 @@ int cols3_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
   return BHCP_OK;
 }
 
-// Real-field DST along a strided axis, in place capable (k_dst_cols3; the
-// MODE 1 k_dst_blk2 variant with BHCP_COLS_BLK2=1).
+// Real-field DST along a strided axis, in place capable (k_dst_cols3).
 int cols_blk2(const bhcp_space_plan* sp, const double* in, double* out, long long ni, long long no,
               cudaStream_t s) {
   gdst::ArgsB2 b{};
   b.in = in; b.out = out; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (sp->m + 1));
   b.ni = ni; b.no = no;
-  if (!g_cols_blk2) switch (2 * (sp->m + 1)) {
+  switch (2 * (sp->m + 1)) {
     case 512: return cols3_launch<256>(sp, b, s);
     case 1024: return cols3_launch<512>(sp, b, s);
     case 2048: return cols3_launch<1024>(sp, b, s);
-  }
-  switch (2 * (sp->m + 1)) {
-    case 512: return blk2_launch<256, 1>(sp, b, s);
-    case 1024: return blk2_launch<512, 1>(sp, b, s);
-    case 2048: return blk2_launch<1024, 1>(sp, b, s);
   }
   return fail(BHCP_ERR_INVALID, "cols_blk2 length");
 }
@@ -1258,9 +1249,9 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
     b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
     b.koff = koff; b.NT = NT; b.P1 = P1; b.idiv = ipow(m, d - 2); b.P = P1; b.nlev = nlev;
     switch (L) {
-      case 512: return blk2_launch<256, 0>(sp, b, s);
-      case 1024: return blk2_launch<512, 0>(sp, b, s);
-      case 2048: return blk2_launch<1024, 0>(sp, b, s);
+      case 512: return blk2_launch<256>(sp, b, s);
+      case 1024: return blk2_launch<512>(sp, b, s);
+      case 2048: return blk2_launch<1024>(sp, b, s);
     }
   }
   const long long total = nlev * sp->nx;
@@ -1299,8 +1290,6 @@ bool ensure_device_constants(int device, std::string* err) {
   {
     const char* e = getenv("BHCP_DISABLE_FAST");
     g_disable_fast = (e && e[0] == '1');
-    const char* e2 = getenv("BHCP_COLS_BLK2");
-    g_cols_blk2 = (e2 && e2[0] == '1');
 
   }
   set_all_attributes();

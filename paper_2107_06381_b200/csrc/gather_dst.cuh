@@ -10,15 +10,6 @@
 #pragma once
 #include "static_fft.cuh"
 
-#ifndef BHCP_C3_MINB
-#define BHCP_C3_MINB 2
-#endif
-#ifndef BHCP_COLS_NOFFT
-#define BHCP_COLS_NOFFT 0
-#endif
-#ifndef BHCP_COLS_DIRECT
-#define BHCP_COLS_DIRECT 0
-#endif
 namespace bhcp {
 namespace gdst {
 
@@ -46,9 +37,9 @@ constexpr int kTB = 8;
 // (one warp per output line) splits U^a/U^b, runs the prefix sum with warp
 // shuffles and writes the row of y directly.
 template <int N> struct PlanB2;
-template <> struct PlanB2<256> { static constexpr int T = 256, R1 = 4; template <class Lay> using F = Fft<256, 4, T, Lay, 4, 8, 8>; };
-template <> struct PlanB2<512> { static constexpr int T = 256, R1 = 8; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };
-template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
+template <> struct PlanB2<256> { static constexpr int T = 256, R1 = 4, MINB = 3; template <class Lay> using F = Fft<256, 4, T, Lay, 4, 8, 8>; };
+template <> struct PlanB2<512> { static constexpr int T = 256, R1 = 8, MINB = 3; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };
+template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16, MINB = 1; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };  // 147 KB smem
 
 struct ArgsB2 {
   const double* in;
@@ -56,11 +47,11 @@ struct ArgsB2 {
   const double2* tw;      // exp(-2 pi i k / N)
   const double* sn;       // sin(pi j / N)
   double scale;           // sqrt(2/N)
-  // MODE 0 (blocked W -> rows of y)
+  // k_dst_blk2 (blocked W -> rows of y)
   const long long* koff;
   long long NT, P1, idiv, P, nlev;
-  // MODE 1 (columns of y, in place): lines i in [0, ni) adjacent, element
-  // stride es = ni, outer blocks o in [0, no) at stride m * ni
+  // k_dst_cols3 (columns, in place capable): lines i in [0, ni) adjacent,
+  // element stride ni, outer blocks o in [0, no) at stride m * ni
   long long ni, no;
 };
 
@@ -69,15 +60,11 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gsrc), "r"(valid ? 8 : 0));
 }
 
-// MODE 0: first level pass from the blocked W. A tile is one spatial line
-//   (k1, r2) x 8 levels, a contiguous 8*m-double run of W; the 8 output
-//   lines are rows of y.
-// MODE 1: a later level pass, in place on y. A tile is 8 adjacent lines
-//   (columns i0..i0+7) x m elements at stride ni: 64 B per element row, all
-//   rows in flight through cp.async. The outputs go back through shared
-//   memory and leave as 64 B row chunks.
-template <int N, int MODE>
-__global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
+// First level pass from the blocked W: a tile is one spatial line (k1, r2)
+// x 8 levels, a contiguous 8*m-double run of W; the 8 output lines are rows
+// of y.
+template <int N>
+__global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(ArgsB2 a) {
   constexpr int S = 4, T = PlanB2<N>::T, m = N - 1;
   constexpr int RUN = m * kTB;
   constexpr int KU = (N / 2) / 32;   // k values per lane (k = u*32 + lane)
@@ -88,38 +75,20 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   double* sn = stage + RUN + 16;
   double* carry = sn + N;           // 8 doubles: lower-half running sums per line
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
-  // Tiles are walked with 32-bit incremental counters (o, tt): MODE 0 (line,
-  // level tile), MODE 1 (outer block, column block).
-  const int NT = MODE == 0 ? (int)a.NT : (int)((a.ni + kTB - 1) / kTB);
+  // Tiles are walked with 32-bit incremental counters (o, tt) = (line, level tile).
+  const int NT = (int)a.NT;
   const int idiv = (int)a.idiv;
-  const int ntiles = MODE == 0 ? (int)(a.P * a.NT) : (int)(a.no * NT);
+  const int ntiles = (int)(a.P * a.NT);
   const int gstep = gridDim.x, step_o = gstep / NT, step_t = gstep - step_o * NT;
-  // MODE 0: the stage copy is shifted so that smem and global addresses agree
-  // mod 128 B (a misaligned cp.async splits every 128 B line into two smem
+  // The stage copy is shifted so that smem and global addresses agree mod
+  // 128 B (a misaligned cp.async splits every 128 B line into two smem
   // wavefronts).
   auto src_of = [&](int o, int tt) -> const double* {
-    if (MODE == 1) return a.in + (long long)o * m * a.ni + (long long)tt * kTB;
     const int k1 = o / idiv, r2 = o - k1 * idiv;
     const long long kb = a.koff ? __ldg(a.koff + k1) : (long long)k1 * a.NT * a.P1 * kTB;
     return a.in + kb + (long long)tt * a.P1 * kTB + (long long)r2 * m * kTB;
   };
-  auto issue = [&](const double* src_d, int tt) {
-    if (MODE == 1) {
-      const int nval = (int)min((long long)kTB, a.ni - (long long)tt * kTB);
-      if (nval == kTB) {
-        for (int i = threadIdx.x; i < RUN; i += T) {
-          const int e = i >> 3, l = i & 7;
-          cp_async8(stage + i, src_d + (long long)e * a.ni + l);
-        }
-      } else {
-        for (int i = threadIdx.x; i < RUN; i += T) {
-          const int e = i >> 3, l = i & 7;
-          cp_async8_zfill(stage + i, src_d + (long long)e * a.ni + (l < nval ? l : 0), l < nval);
-        }
-      }
-      cp_async_commit();
-      return 0;
-    }
+  auto issue = [&](const double* src_d) {
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(stage));
     const int soff = (int)(((static_cast<unsigned>(reinterpret_cast<uintptr_t>(src_d)) - sbase) & 127u) >> 3);
     const double2* src = reinterpret_cast<const double2*>(src_d);
@@ -135,55 +104,27 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
   int tile = blockIdx.x;
   int o = tile / NT, tt = tile - o * NT;
   int soff = 0;
-  if (tile < ntiles) soff = issue(src_of(o, tt), tt);
+  if (tile < ntiles) soff = issue(src_of(o, tt));
   for (; tile < ntiles; tile += gstep) {
     int no = o + step_o, ntt = tt + step_t;
     if (ntt >= NT) { ntt -= NT; ++no; }
     cp_async_wait_all();
     __syncthreads();
-    const long long tvalid = MODE == 0 ? a.nlev - (long long)tt * kTB : (long long)kTB;
+    const long long tvalid = a.nlev - (long long)tt * kTB;
     const double* st = stage + soff;
     auto gen = [&](int q, int j) -> double2 {
       if (j == 0) return make_double2(0.0, 0.0);
       double2 p = *reinterpret_cast<const double2*>(st + (j - 1) * kTB + 2 * q);      // x_j
       double2 r = *reinterpret_cast<const double2*>(st + (N - j - 1) * kTB + 2 * q);  // x_{N-j}
-      if (MODE == 0) {
-        if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
-        if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
-      }
+      if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
+      if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
       const double s = sn[j];
       return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
     };
     using Ff = typename PlanB2<N>::template F<Lay>;
-#if BHCP_COLS_NOFFT
-    if (MODE == 1) {
-      for (int i = threadIdx.x; i < m * S; i += T) {
-        const int e = i >> 2, q = i & 3;
-        buf[Lay::addr(q, e)] = *reinterpret_cast<const double2*>(st + e * kTB + 2 * q);
-      }
-      const int cur_o = o, cur_tt = tt;
-#if BHCP_COLS_NOFFT == 1
-      if (tile + gstep < ntiles) soff = issue(src_of(no, ntt), ntt);
-#endif
-      o = no; tt = ntt;
-      __syncthreads();
-      double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB;
-      const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
-      // lane -> (row e, line l): 8 lanes write one contiguous 64 B row chunk
-      const double* bufd = reinterpret_cast<const double*>(buf);
-      for (int i = threadIdx.x; i < m * kTB; i += T) {
-        const int e = i >> 3, l = i & 7;
-        if (l < nval) base[(long long)e * a.ni + l] = bufd[2 * Lay::addr(l >> 1, e) + (l & 1)];
-      }
-#if BHCP_COLS_NOFFT == 2
-      if (tile + gstep < ntiles) soff = issue(src_of(o, tt), tt);
-#endif
-      continue;
-    }
-#endif
     Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first(buf, gen);
     const int cur_o = o, cur_tt = tt;
-    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt), ntt);
+    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt));
     o = no; tt = ntt;
     auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
     FftTail<Ff>::run(buf, a.tw, sink);
@@ -219,20 +160,17 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
         ca += __shfl_sync(0xffffffffu, ia, 31);
         cb += __shfl_sync(0xffffffffu, ib, 31);
       }
-      // MODE 1 overwrites buf with the outputs, so both warps of the pair
-      // must have finished reading: full pair barrier instead of arrive/sync.
       if (h == 0) {
         if (lane == 0) { carry[2 * q] = ca; carry[2 * q + 1] = cb; }
         __threadfence_block();
-        if (MODE == 0) asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
-        else asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
+        asm volatile("bar.arrive %0, 64;\n" ::"r"(1 + q) : "memory");
         ca = 0.0; cb = 0.0;
       } else {
         asm volatile("bar.sync %0, 64;\n" ::"r"(1 + q) : "memory");
         ca = carry[2 * q]; cb = carry[2 * q + 1];
       }
       const double ha = 0.5 * c0a, hb = 0.5 * c0b;
-      if (MODE == 0) {
+      {
 #pragma unroll
         for (int line = 0; line < 2; ++line) {
           const long long t = (long long)cur_tt * kTB + 2 * q + line;
@@ -247,59 +185,11 @@ __global__ void __launch_bounds__(PlanB2<N>::T, 3) k_dst_blk2(ArgsB2 a) {
             dst[2 * k] = a.scale * odd;
           }
         }
-      } else if (BHCP_COLS_DIRECT) {
-        double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB + 2 * q;
-        const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
-#pragma unroll
-        for (int u = 0; u < KH; ++u) {
-          const int k = (h * KH + u) * 32 + lane;
-          double* d0 = base + (long long)(2 * k) * a.ni;
-          if (k >= 1) {
-            double* d1 = d0 - a.ni;
-            if (2 * q < nval) d1[0] = a.scale * ea[u];
-            if (2 * q + 1 < nval) d1[1] = a.scale * eb[u];
-          }
-          if (2 * q < nval) d0[0] = a.scale * ((ca + oa[u]) - ha);
-          if (2 * q + 1 < nval) d0[1] = a.scale * ((cb + ob[u]) - hb);
-        }
-      } else {
-        // outputs (line a, line b) of element p at buf[addr(q, p)]
-#pragma unroll
-        for (int u = 0; u < KH; ++u) {
-          const int k = (h * KH + u) * 32 + lane;
-          if (k >= 1) buf[Lay::addr(q, 2 * k - 1)] = make_double2(a.scale * ea[u], a.scale * eb[u]);
-          buf[Lay::addr(q, 2 * k)] = make_double2(a.scale * ((ca + oa[u]) - ha), a.scale * ((cb + ob[u]) - hb));
-        }
-      }
-    }
-    if (MODE == 1 && !BHCP_COLS_DIRECT) {
-      __syncthreads();
-      double* base = a.out + (long long)cur_o * m * a.ni + (long long)cur_tt * kTB;
-      const int nval = (int)min((long long)kTB, a.ni - (long long)cur_tt * kTB);
-      // lane -> (row e, line l): 8 lanes write one contiguous 64 B row chunk
-      const double* bufd = reinterpret_cast<const double*>(buf);
-      for (int i = threadIdx.x; i < m * kTB; i += T) {
-        const int e = i >> 3, l = i & 7;
-        if (l < nval) base[(long long)e * a.ni + l] = bufd[2 * Lay::addr(l >> 1, e) + (l & 1)];
       }
     }
   }
 }
 
-// ---------------------------------------------------------------------------
-// k_dst_cols3: DST-I along a strided axis, in place capable, for real fields
-// (level passes >= 1 and the ghat transform). A tile is 2S adjacent lines
-// (columns i0 .. i0+2S-1, 2S*8 = 256 / 128 / 64 B per element row for
-// N = 256 / 512 / 1024) x m elements at stride ni. Everything happens in ONE
-// dense shared buffer of S*N complex values (64 KB), so three CTAs fit per SM
-// and 192 KB of rows are in flight per SM:
-//   1. cp.async 8 B: x(e, l) -> double (e+1)*2S + l, i.e. complex slot
-//      (q = l/2, idx = e+1) of the interleaved layout (idx*S + q)
-//   2. half-length real DST as in k_dst_blk2, first stage in place
-//   3. post-processing with lanes over (q, k): lane = q + S*kk, so a warp
-//      reads whole 16*S-byte rows (conflict-free) and the running sum over k
-//      needs log2(32/S) shuffle steps; warp totals are combined in smem
-//   4. outputs back into the buffer, then 2S*8-byte row chunks to global.
 template <int N> struct PlanC3;
 template <> struct PlanC3<256> { static constexpr int S = 16; template <class Lay> using F = Fft<256, 16, 256, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
 template <> struct PlanC3<512> { static constexpr int S = 8; template <class Lay> using F = Fft<512, 8, 256, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
@@ -310,7 +200,7 @@ template <int N> constexpr size_t smemC3_bytes() {
 }
 
 template <int N>
-__global__ void __launch_bounds__(256, BHCP_C3_MINB) k_dst_cols3(ArgsB2 a) {
+__global__ void __launch_bounds__(256, 2) k_dst_cols3(ArgsB2 a) {
   constexpr int S = PlanC3<N>::S, T = 256, m = N - 1, LW = 2 * S;   // LW lines per tile
   constexpr int KK = 32 / S;                 // k values per warp step
   constexpr int KW = (N / 2) / 8;            // k values per warp (8 warps)
