@@ -1117,10 +1117,14 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
     if (sym) {
       f.tiles = sp->tiles_dev;
       f.ntiles = sp->ntiles;
-      k_modes_fast<513, true><<<(unsigned)sp->ntiles, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+      const long long grid = std::min<long long>(sp->ntiles, resident_ctas(k_modes_fast<513, true>, ModesPlan<513>::T,
+                                                                          modes_smem<513>()));
+      k_modes_fast<513, true><<<(unsigned)grid, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
     } else {
       const long long work = (kc + ModesPlan<513>::S - 1) / ModesPlan<513>::S;
-      k_modes_fast<513, false><<<(unsigned)work, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
+      const long long grid = std::min<long long>(work, resident_ctas(k_modes_fast<513, false>, ModesPlan<513>::T,
+                                                                     modes_smem<513>()));
+      k_modes_fast<513, false><<<(unsigned)grid, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
     }
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_fast launch");
     return BHCP_OK;

@@ -306,113 +306,104 @@ struct FastModesArgs {
   WLayout wl;
 };
 
-// Warp-per-mode pass A: the CTA takes S = 16 modes (a 4x4 upper-triangle tile
-// in 2D, SYM, or 16 consecutive modes); warp q transforms mode q in its own
-// shared-memory region with warp-synchronous stages, then the CTA writes
-// W[t, k] (and the mirrored columns) with coalesced stores.
+// Warp-per-mode pass A, persistent: a CTA loads the shift and 1/gamma tables
+// once and loops over tiles of S = 16 modes (a 4x4 upper-triangle tile in
+// 2D, SYM, or 16 consecutive modes); warp q transforms mode q of the tile in
+// its own shared-memory region with warp-synchronous stages and writes that
+// mode's time series (and the mirrored mode's) itself. No CTA barrier inside
+// the tile loop: warps progress independently.
 template <int N, bool SYM>
 __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_fast(FastModesArgs a) {
   constexpr int S = ModesPlan<N>::S, T = ModesPlan<N>::T;
   static_assert(T == 32 * S, "one warp per mode");
   constexpr int LDW = N;  // per-warp region (odd length: conflict-light)
   extern __shared__ double2 smem[];
-  __shared__ double s_mu[S], s_c[S], s_cm[S], red[2 * (T / 32)];
-  __shared__ long long s_dst[S], s_mir[S];
-  __shared__ bool s_valid[S];
+  __shared__ double red[2 * (T / 32)];
   __shared__ double2 s_gi[N], s_sh[N];
   for (int i = threadIdx.x; i < N; i += T) {
     s_gi[i] = __ldg(a.gaminv + i);
     s_sh[i] = __ldg(a.shifts + i);
   }
-  if (threadIdx.x < S) {
-    const int q = threadIdx.x;
-    bool v;
-    long long kd, km = -1;
-    if (SYM) {
-      const int2 tb = a.tiles[blockIdx.x];
-      const int k1 = 4 * tb.x + (q >> 2), k2 = 4 * tb.y + (q & 3);
-      v = (k1 < a.m) && (k2 < a.m) && (tb.x != tb.y || k1 <= k2);
-      kd = (long long)k1 * a.m + k2;
-      if (v && k1 != k2) km = (long long)k2 * a.m + k1;
-      if (!v) kd = 0;
-    } else {
-      const long long kl = (long long)blockIdx.x * S + q;
-      v = kl < a.k_count;
-      kd = a.k_begin + (v ? kl : 0);
-    }
-    s_valid[q] = v;
-    s_mu[q] = mode_mu(a.mu1, a.m, a.dim, kd);
-    s_c[q] = v ? a.ghat[kd] * a.cscale : 0.0;
-    s_cm[q] = (km >= 0) ? a.ghat[km] * a.cscale : 0.0;
-    s_dst[q] = v ? (SYM ? kd : kd - a.k_begin) : -1;
-    s_mir[q] = km;
-  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* buf = smem + warp * LDW;
-  {
-    const double mu = s_mu[warp];
-    const bool valid = s_valid[warp];
-    StatusDev* st = a.st;
-    const double2* shifts = s_sh;
-    auto gen = [&](int j) -> double2 {
-      const double2 s = shifts[j];
-      if (!valid) return make_double2(0.0, 0.0);
-      const double dr = s.x + mu, di = s.y;
-      const double den2 = dr * dr + di * di;
-      if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(st, j);
-      const double inv = fast_rcp(den2);
-      return make_double2(dr * inv, -di * inv);
-    };
-    ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
-  }
-  // Store phase, per warp (no CTA barrier): warp q writes its own mode's
-  // time series. W layout: a.wl (mode-major slabs: contiguous runs of t;
-  // level-major: stride w_ld) -- see WLayout.
+  StatusDev* st = a.st;
+  const fastk::WLayout& wl = a.wl;
   double sre = 0.0, sim = 0.0;
-  {
-    const int q = warp;
-    const long long cd = s_dst[q];
-    const long long cm = SYM ? s_mir[q] : -1;
-    const double c = s_c[q], c2 = SYM ? s_cm[q] : 0.0;
+  const long long ntiles = SYM ? a.ntiles : (a.k_count + S - 1) / S;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // this warp's mode: destination (k1, r) = (kd / P1, kd % P1), mirror, mu, coefficients
+    bool valid;
+    long long kd, km = -1;
+    int k1d = 0, k1m = 0;
+    long long rd = 0, rm = 0;
+    if (SYM) {
+      const int2 tb = __ldg(a.tiles + tile);
+      const int k1 = 4 * tb.x + (warp >> 2), k2 = 4 * tb.y + (warp & 3);
+      valid = (k1 < a.m) && (k2 < a.m) && (tb.x != tb.y || k1 <= k2);
+      kd = valid ? (long long)k1 * a.m + k2 : 0;
+      if (valid && k1 != k2) km = (long long)k2 * a.m + k1;
+      k1d = k1; rd = k2; k1m = k2; rm = k1;   // 2D: P1 = m
+    } else {
+      const long long kl = tile * S + warp;
+      valid = kl < a.k_count;
+      kd = a.k_begin + (valid ? kl : 0);
+      const long long local = valid ? kl : 0;
+      if (wl.mode_major) { k1d = (int)(local / wl.P1); rd = local - (long long)k1d * wl.P1; }
+    }
+    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    const double c = valid ? __ldg(a.ghat + kd) * a.cscale : 0.0;
+    const double c2 = (SYM && km >= 0) ? __ldg(a.ghat + km) * a.cscale : 0.0;
+    {
+      const double2* shifts = s_sh;
+      auto gen = [&](int j) -> double2 {
+        const double2 s = shifts[j];
+        if (!valid) return make_double2(0.0, 0.0);
+        const double dr = s.x + mu, di = s.y;
+        const double den2 = dr * dr + di * di;
+        if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(st, j);
+        const double inv = fast_rcp(den2);
+        return make_double2(dr * inv, -di * inv);
+      };
+      ModesPlan<N>::WF::run(buf, lane, a.tw, gen);
+    }
+    if (!valid) continue;
+    // W layout a.wl: blocked slabs (runs of 8 levels at stride P1*8) or level-major (stride w_ld)
     const double2* X = buf;
-    if (cd >= 0) {
-      const fastk::WLayout& wl = a.wl;
-      const int nsl = wl.mode_major ? wl.nsl : 1;
-      const long long cds = cm >= 0 ? cm : 0;
-      for (int sl = 0; sl < nsl; ++sl) {
-        const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
-        const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : N;
-        // element t of mode k at pk + (tl / 8) * tstep + tl % 8 (blocked), or pk + t * w_ld
-        long long pd, pm, tstep;
-        if (wl.mode_major) {
-          const long long nt = wl.sl_nt[sl];
-          const long long k1d = cd / wl.P1, k1m = cds / wl.P1;
-          pd = wl.sl_off[sl] + (k1d * nt * wl.P1 + (cd - k1d * wl.P1)) * kTBL;
-          pm = wl.sl_off[sl] + (k1m * nt * wl.P1 + (cds - k1m * wl.P1)) * kTBL;
-          tstep = wl.P1 * kTBL;
-        } else {
-          pd = cd;
-          pm = cds;
-          tstep = 0;
-        }
-        for (int t = t0 + lane; t < t1; t += 32) {
-          const double2 x = X[t];
-          const double2 g = s_gi[t];
-          const double zr = x.x * g.x - x.y * g.y;
-          const double zi = x.x * g.y + x.y * g.x;
-          const double wr = c * zr, wi = c * zi;
-          sre = fma(wr, wr, sre);
-          sim = fma(wi, wi, sim);
-          const int tl = t - t0;
-          const long long off = wl.mode_major ? (long long)(tl >> 3) * tstep + (tl & 7) : (long long)t * wl.w_ld;
-          a.W[pd + off] = wr;
-          if (SYM && cm >= 0) {
-            const double vr = c2 * zr, vi = c2 * zi;
-            sre = fma(vr, vr, sre);
-            sim = fma(vi, vi, sim);
-            a.W[pm + off] = vr;
-          }
+    const int nsl = wl.mode_major ? wl.nsl : 1;
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : N;
+      long long pd, pm, step;
+      if (wl.mode_major) {
+        const long long nt = wl.sl_nt[sl];
+        pd = wl.sl_off[sl] + ((long long)k1d * nt * wl.P1 + rd) * kTBL;
+        pm = wl.sl_off[sl] + ((long long)k1m * nt * wl.P1 + rm) * kTBL;
+        // t = t0 + lane + 32 i  ->  (tl >> 3) * P1*8 + (tl & 7), t0 a multiple of 8
+        const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
+        pd += lo; pm += lo;
+        step = 4 * wl.P1 * kTBL;
+      } else {
+        pd = kd - a.k_begin + (long long)lane * wl.w_ld;
+        pm = km + (long long)lane * wl.w_ld;
+        step = 32 * wl.w_ld;
+      }
+      double* __restrict__ wd = a.W + pd;
+      double* __restrict__ wm = a.W + pm;
+      for (int t = t0 + lane; t < t1; t += 32, wd += step, wm += step) {
+        const double2 x = X[t];
+        const double2 g = s_gi[t];
+        const double zr = x.x * g.x - x.y * g.y;
+        const double zi = x.x * g.y + x.y * g.x;
+        const double wr = c * zr, wi = c * zi;
+        sre = fma(wr, wr, sre);
+        sim = fma(wi, wi, sim);
+        *wd = wr;
+        if (SYM && km >= 0) {
+          const double vr = c2 * zr, vi = c2 * zi;
+          sre = fma(vr, vr, sre);
+          sim = fma(vi, vi, sim);
+          *wm = vr;
         }
       }
     }
