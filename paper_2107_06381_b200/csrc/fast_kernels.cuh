@@ -320,9 +320,12 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
   extern __shared__ double2 smem[];
   __shared__ double red[2 * (T / 32)];
   __shared__ double2 s_gi[N], s_sh[N];
+  __shared__ double s_thr[N];   // singular-shift threshold 1e-28 |s_j|^2 (space.py:237-240)
   for (int i = threadIdx.x; i < N; i += T) {
     s_gi[i] = __ldg(a.gaminv + i);
-    s_sh[i] = __ldg(a.shifts + i);
+    const double2 sh = __ldg(a.shifts + i);
+    s_sh[i] = sh;
+    s_thr[i] = 1e-28 * (sh.x * sh.x + sh.y * sh.y);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
         if (!valid) return make_double2(0.0, 0.0);
         const double dr = s.x + mu, di = s.y;
         const double den2 = dr * dr + di * di;
-        if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(st, j);
+        if (den2 <= s_thr[j]) flag_singular(st, j);
         const double inv = fast_rcp(den2);
         return make_double2(dr * inv, -di * inv);
       };
@@ -369,6 +372,8 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
     }
     if (!valid) continue;
     // W layout a.wl: blocked slabs (runs of 8 levels at stride P1*8) or level-major (stride w_ld)
+    // residue norms: sum over this warp's modes of (c^2 + c2^2) * sum_t zr^2 (zi^2)
+    double zr2 = 0.0, zi2 = 0.0;
     const double2* X = buf;
     const int nsl = wl.mode_major ? wl.nsl : 1;
     for (int sl = 0; sl < nsl; ++sl) {
@@ -395,18 +400,15 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
         const double2 g = s_gi[t];
         const double zr = x.x * g.x - x.y * g.y;
         const double zi = x.x * g.y + x.y * g.x;
-        const double wr = c * zr, wi = c * zi;
-        sre = fma(wr, wr, sre);
-        sim = fma(wi, wi, sim);
-        *wd = wr;
-        if (SYM && km >= 0) {
-          const double vr = c2 * zr, vi = c2 * zi;
-          sre = fma(vr, vr, sre);
-          sim = fma(vi, vi, sim);
-          *wm = vr;
-        }
+        zr2 = fma(zr, zr, zr2);
+        zi2 = fma(zi, zi, zi2);
+        *wd = c * zr;
+        if (SYM && km >= 0) *wm = c2 * zr;
       }
     }
+    const double cc = c * c + c2 * c2;
+    sre = fma(cc, zr2, sre);
+    sim = fma(cc, zi2, sim);
   }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
