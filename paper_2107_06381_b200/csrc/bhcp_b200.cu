@@ -729,7 +729,7 @@ struct bhcp_space_plan {
   long long ntiles;
   double2* twN;          // exp(-2 pi i k / N), N = m + 1 (half-length DST kernels)
   double* snN;           // sin(pi j / N)
-  int4* seg_tiles[9];    // symmetric segment tiles for the Bluestein modes kernel, by segment length S
+  int4* seg_tiles[9];    // symmetric segment tiles of the Bluestein / Rader modes kernels, slot log2(S)
   long long seg_count[9];
 };
 
@@ -738,6 +738,8 @@ struct bhcp_time_plan {
   double2* tables;       // gamma | gamma_inv | shifts  (3n double2)
   FftPlanHost fft;       // FFT of length n
   double2* blue;         // n = 2^p + 1 fast path: tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1)
+  double2* rader;        // prime n = 2^p + 1: tw (n-1) | bhat (n-1)
+  int* rader_idx;        //                    perm (n-1) | qidx (n)
 };
 
 namespace {
@@ -815,6 +817,8 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
 
+  allow_smem(fastk::k_modes_rader<257, false>);
+  allow_smem(fastk::k_modes_rader<257, true>);
   allow_smem(fastk::k_modes_fast<513, false>);
   allow_smem(fastk::k_modes_fast<513, true>);
 }
@@ -1046,7 +1050,10 @@ std::mutex g_tile_mutex;
 const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
   auto* sp = const_cast<bhcp_space_plan*>(sp_c);
   std::lock_guard<std::mutex> lk(g_tile_mutex);
-  if (!sp->seg_tiles[S]) {
+  int slot = 0;
+  while ((1 << slot) < S) ++slot;
+  if ((1 << slot) != S || slot >= 9) return nullptr;   // S a power of two <= 256
+  if (!sp->seg_tiles[slot]) {
     std::vector<int4> t;
     const int m = sp->m;
     if (sp->dim == 2) {
@@ -1057,12 +1064,41 @@ const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
         for (int k2 = k1; k2 < m; ++k2)
           for (int k3a = 0; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
     }
-    if (cudaMalloc(&sp->seg_tiles[S], sizeof(int4) * t.size()) != cudaSuccess) return nullptr;
-    cudaMemcpy(sp->seg_tiles[S], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice);
-    sp->seg_count[S] = (long long)t.size();
+    if (cudaMalloc(&sp->seg_tiles[slot], sizeof(int4) * t.size()) != cudaSuccess) return nullptr;
+    cudaMemcpy(sp->seg_tiles[slot], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice);
+    sp->seg_count[slot] = (long long)t.size();
   }
-  *count = sp->seg_count[S];
-  return sp->seg_tiles[S];
+  *count = sp->seg_count[slot];
+  return sp->seg_tiles[slot];
+}
+
+template <int NL>
+int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
+                long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
+                cudaStream_t s) {
+  using namespace fastk;
+  using Pl = RaderPlan<NL>;
+  RaderModesArgs a{};
+  a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev; a.ghat = ghat;
+  a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
+  a.st = st; a.wl = wl;
+  a.tw = tp->rader; a.bhat = tp->rader + Pl::NP; a.perm = tp->rader_idx; a.qidx = tp->rader_idx + Pl::NP;
+  const size_t sm = rader_smem<NL>();
+  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  if (sym) {
+    long long cnt = 0;
+    a.tiles = seg_tiles(sp, Pl::S, &cnt);
+    if (!a.tiles) return cuda_fail("seg tiles");
+    a.ntiles = cnt;
+    const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_rader<NL, true>, Pl::T, sm));
+    k_modes_rader<NL, true><<<(unsigned)grid, Pl::T, sm, s>>>(a);
+  } else {
+    const long long work = (a.k_count + Pl::S - 1) / Pl::S;
+    const long long grid = std::min<long long>(work, resident_ctas(k_modes_rader<NL, false>, Pl::T, sm));
+    k_modes_rader<NL, false><<<(unsigned)grid, Pl::T, sm, s>>>(a);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_rader launch");
+  return BHCP_OK;
 }
 
 template <int NL>
@@ -1084,10 +1120,12 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
     a.tiles = seg_tiles(sp, Pl::S, &cnt);
     if (!a.tiles) return cuda_fail("seg tiles");
     a.ntiles = cnt;
-    k_modes_blue<NL, true><<<(unsigned)cnt, Pl::T, sm, s>>>(a);
+    const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_blue<NL, true>, Pl::T, sm));
+    k_modes_blue<NL, true><<<(unsigned)grid, Pl::T, sm, s>>>(a);
   } else {
     const long long work = (a.k_count + Pl::S - 1) / Pl::S;
-    k_modes_blue<NL, false><<<(unsigned)work, Pl::T, sm, s>>>(a);
+    const long long grid = std::min<long long>(work, resident_ctas(k_modes_blue<NL, false>, Pl::T, sm));
+    k_modes_blue<NL, false><<<(unsigned)grid, Pl::T, sm, s>>>(a);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_blue launch");
   return BHCP_OK;
@@ -1099,6 +1137,8 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
+  if (!g_disable_fast && tp->rader && tp->n == 257)
+    return rader_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
   if (!g_disable_fast && tp->blue) {
     switch (tp->n) {
       case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
@@ -1404,6 +1444,21 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
     }
     cudaMemcpy(tp->blue, tabs.data(), sizeof(double2) * tabs.size(), cudaMemcpyHostToDevice);
   }
+  tp->rader = nullptr;
+  tp->rader_idx = nullptr;
+  if (n_levels == 257) {
+    std::vector<double2> rc;
+    std::vector<int> ri;
+    if (!build_rader_tables(n_levels, &rc, &ri, &err)) {
+      bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err);
+    }
+    if (cudaMalloc(&tp->rader, sizeof(double2) * rc.size()) != cudaSuccess ||
+        cudaMalloc(&tp->rader_idx, sizeof(int) * ri.size()) != cudaSuccess) {
+      bhcp_time_plan_destroy(tp); return cuda_fail("cudaMalloc rader tables");
+    }
+    cudaMemcpy(tp->rader, rc.data(), sizeof(double2) * rc.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(tp->rader_idx, ri.data(), sizeof(int) * ri.size(), cudaMemcpyHostToDevice);
+  }
   *out = tp;
   return BHCP_OK;
 }
@@ -1414,6 +1469,8 @@ void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
   free_fft_plan(&tp->fft);
   cudaFree(tp->tables);
   if (tp->blue) cudaFree(tp->blue);
+  if (tp->rader) cudaFree(tp->rader);
+  if (tp->rader_idx) cudaFree(tp->rader_idx);
   delete tp;
 }
 

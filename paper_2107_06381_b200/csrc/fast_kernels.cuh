@@ -493,112 +493,123 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
   using F2 = typename AllSmemOf<F1>::type;
   extern __shared__ double2 smem[];
   __shared__ double s_mu[S], s_c[S], s_cm[S], red[2 * (T / 32)];
-  __shared__ long long s_dst[S], s_mir[S];
-  __shared__ bool s_valid[S];
+  __shared__ int s_k1d[S], s_k1m[S];
+  __shared__ long long s_rd[S], s_rm[S];
+  __shared__ bool s_valid[S], s_hasm[S];
   __shared__ double2 s_vM[S];
   double2* buf = smem;
-  if (threadIdx.x < S) {
-    const int q = threadIdx.x;
-    bool v;
-    long long kd, km = -1;
-    if (SYM) {
-      const int4 tb = a.tiles[blockIdx.x];
-      if (a.dim == 2) {
-        const int k1 = tb.x, k2 = tb.y + q;
-        v = k2 < a.m && k2 >= k1;
-        kd = (long long)k1 * a.m + k2;
-        if (v && k2 != k1) km = (long long)k2 * a.m + k1;
-      } else {
-        const int k1 = tb.x, k2 = tb.y, k3 = tb.z + q;
-        v = k3 < a.m;
-        kd = ((long long)k1 * a.m + k2) * a.m + k3;
-        if (v && k1 != k2) km = ((long long)k2 * a.m + k1) * a.m + k3;
-      }
-      if (!v) kd = 0;
-    } else {
-      const long long kl = (long long)blockIdx.x * S + q;
-      v = kl < a.k_count;
-      kd = a.k_begin + (v ? kl : 0);
-    }
-    s_valid[q] = v;
-    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
-    s_mu[q] = mu;
-    s_c[q] = v ? a.ghat[kd] * a.cscale : 0.0;
-    s_cm[q] = (km >= 0) ? a.ghat[km] * a.cscale : 0.0;
-    s_dst[q] = v ? (SYM ? kd : kd - a.k_begin) : -1;
-    s_mir[q] = km;
-    // last input v_M = 1/(s_M + mu)
-    const double2 s = __ldg(a.shifts + M);
-    const double dr = s.x + mu, di = s.y;
-    const double den2 = dr * dr + di * di;
-    if (v && den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, M);
-    const double inv = fast_rcp(den2);
-    s_vM[q] = v ? make_double2(dr * inv, -di * inv) : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  // FFT 1: a_j = v_j c_j (j < M), zero padded to L
-  auto gen = [&](int q, int j) -> double2 {
-    if (j >= M || !s_valid[q]) return make_double2(0.0, 0.0);
-    const double2 s = __ldg(a.shifts + j);
-    const double dr = s.x + s_mu[q], di = s.y;
-    const double den2 = dr * dr + di * di;
-    if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, j);
-    const double inv = fast_rcp(den2);
-    return cmul(make_double2(dr * inv, -di * inv), __ldg(a.bt.chirp + j));
-  };
-  auto sink1 = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = cconj(cmul(X, __ldg(a.bt.bhat + idx))); };
-  F1::run(buf, a.bt.tw, gen, sink1);
-  __syncthreads();
-  // FFT 2 (conjugated inverse): conv_t = conj(X_t); X_t of the DFT = c_t conv_t + v_M w^{Mt}
-  auto sink2 = [&](int q, int idx, double2 X) {
-    if (idx > M) return;
-    const double2 conv = cconj(X);
-    const double2 Y = cadd(cmul(conv, __ldg(a.bt.chirp + idx)), cmul(s_vM[q], __ldg(a.bt.wM + idx)));
-    buf[Lay::addr(q, idx)] = cmul(Y, __ldg(a.gaminv + idx));
-  };
-  F2::run(buf, a.bt.tw, sink2);
-  __syncthreads();
-  // store: warps loop over the S modes; lanes run along t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const WLayout& wl = a.wl;
   double sre = 0.0, sim = 0.0;
-  for (int q = warp; q < S; q += T / 32) {
-    const long long cd = s_dst[q];
-    if (cd < 0) continue;
-    const long long cm = SYM ? s_mir[q] : -1;
-    const double c = s_c[q], c2 = SYM ? s_cm[q] : 0.0;
-    const WLayout& wl = a.wl;
-    const int nsl = wl.mode_major ? wl.nsl : 1;
-    const long long cds = cm >= 0 ? cm : 0;
-    for (int sl = 0; sl < nsl; ++sl) {
-      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
-      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
-      long long pd, pm, tstep;
-      if (wl.mode_major) {
-        const long long nt = wl.sl_nt[sl];
-        const long long k1d = cd / wl.P1, k1m = cds / wl.P1;
-        pd = wl.sl_off[sl] + (k1d * nt * wl.P1 + (cd - k1d * wl.P1)) * kTBL;
-        pm = wl.sl_off[sl] + (k1m * nt * wl.P1 + (cds - k1m * wl.P1)) * kTBL;
-        tstep = wl.P1 * kTBL;
+  const long long ntiles = SYM ? a.ntiles : (a.k_count + S - 1) / S;
+  // Persistent: each CTA loops over tiles of S modes.
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();   // previous tile's stores done with buf / per-mode data
+    if (threadIdx.x < S) {
+      const int q = threadIdx.x;
+      bool v, hm = false;
+      long long kd;
+      int k1d = 0, k1m = 0;
+      long long rd = 0, rm = 0, km = 0;
+      if (SYM) {
+        const int4 tb = a.tiles[tile];
+        if (a.dim == 2) {
+          const int k1 = tb.x, k2 = tb.y + q;
+          v = k2 < a.m && k2 >= k1;
+          kd = (long long)k1 * a.m + k2;
+          hm = v && k2 != k1;
+          km = (long long)k2 * a.m + k1;
+          k1d = k1; rd = k2; k1m = k2; rm = k1;                       // P1 = m
+        } else {
+          const int k1 = tb.x, k2 = tb.y, k3 = tb.z + q;
+          v = k3 < a.m;
+          kd = ((long long)k1 * a.m + k2) * a.m + k3;
+          hm = v && k1 != k2;
+          km = ((long long)k2 * a.m + k1) * a.m + k3;
+          k1d = k1; rd = (long long)k2 * a.m + k3; k1m = k2; rm = (long long)k1 * a.m + k3;   // P1 = m^2
+        }
+        if (!v) kd = 0;
       } else {
-        pd = cd;
-        pm = cds;
-        tstep = 0;
+        const long long kl = tile * S + q;
+        v = kl < a.k_count;
+        kd = a.k_begin + (v ? kl : 0);
+        const long long local = v ? kl : 0;
+        if (wl.mode_major) { k1d = (int)(local / wl.P1); rd = local - (long long)k1d * wl.P1; }
+        else rd = local;
       }
-      for (int t = t0 + lane; t < t1; t += 32) {
-        const double2 z = buf[Lay::addr(q, t)];
-        const double wr = c * z.x, wi = c * z.y;
-        sre = fma(wr, wr, sre);
-        sim = fma(wi, wi, sim);
-        const int tl = t - t0;
-        const long long off = wl.mode_major ? (long long)(tl >> 3) * tstep + (tl & 7) : (long long)t * wl.w_ld;
-        a.W[pd + off] = wr;
-        if (SYM && cm >= 0) {
-          const double vr = c2 * z.x, vi = c2 * z.y;
-          sre = fma(vr, vr, sre);
-          sim = fma(vi, vi, sim);
-          a.W[pm + off] = vr;
+      s_valid[q] = v;
+      s_hasm[q] = hm;
+      const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+      s_mu[q] = mu;
+      s_c[q] = v ? a.ghat[kd] * a.cscale : 0.0;
+      s_cm[q] = hm ? a.ghat[km] * a.cscale : 0.0;
+      s_k1d[q] = k1d; s_rd[q] = rd; s_k1m[q] = k1m; s_rm[q] = rm;
+      // last input v_M = 1/(s_M + mu)
+      const double2 s = __ldg(a.shifts + M);
+      const double dr = s.x + mu, di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (v && den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, M);
+      const double inv = fast_rcp(den2);
+      s_vM[q] = v ? make_double2(dr * inv, -di * inv) : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    // FFT 1: a_j = v_j c_j (j < M), zero padded to L
+    auto gen = [&](int q, int j) -> double2 {
+      if (j >= M || !s_valid[q]) return make_double2(0.0, 0.0);
+      const double2 s = __ldg(a.shifts + j);
+      const double dr = s.x + s_mu[q], di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, j);
+      const double inv = fast_rcp(den2);
+      return cmul(make_double2(dr * inv, -di * inv), __ldg(a.bt.chirp + j));
+    };
+    auto sink1 = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = cconj(cmul(X, __ldg(a.bt.bhat + idx))); };
+    F1::run(buf, a.bt.tw, gen, sink1);
+    __syncthreads();
+    // FFT 2 (conjugated inverse): conv_t = conj(X_t); X_t of the DFT = c_t conv_t + v_M w^{Mt}
+    auto sink2 = [&](int q, int idx, double2 X) {
+      if (idx > M) return;
+      const double2 conv = cconj(X);
+      const double2 Y = cadd(cmul(conv, __ldg(a.bt.chirp + idx)), cmul(s_vM[q], __ldg(a.bt.wM + idx)));
+      buf[Lay::addr(q, idx)] = cmul(Y, __ldg(a.gaminv + idx));
+    };
+    F2::run(buf, a.bt.tw, sink2);
+    __syncthreads();
+    // store: warps loop over the S modes; lanes run along t
+    for (int q = warp; q < S; q += T / 32) {
+      if (!s_valid[q]) continue;
+      const bool hm = SYM && s_hasm[q];
+      const double c = s_c[q], c2 = s_cm[q];
+      const int nsl = wl.mode_major ? wl.nsl : 1;
+      double zr2 = 0.0, zi2 = 0.0;
+      for (int sl = 0; sl < nsl; ++sl) {
+        const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+        const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
+        long long pd, pm, step;
+        if (wl.mode_major) {
+          const long long nt = wl.sl_nt[sl];
+          const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
+          pd = wl.sl_off[sl] + ((long long)s_k1d[q] * nt * wl.P1 + s_rd[q]) * kTBL + lo;
+          pm = wl.sl_off[sl] + ((long long)s_k1m[q] * nt * wl.P1 + s_rm[q]) * kTBL + lo;
+          step = 4 * wl.P1 * kTBL;
+        } else {
+          pd = s_rd[q] + (long long)lane * wl.w_ld;
+          pm = pd;
+          step = 32 * wl.w_ld;
+        }
+        double* __restrict__ wd = a.W + pd;
+        double* __restrict__ wm = a.W + pm;
+        for (int t = t0 + lane; t < t1; t += 32, wd += step, wm += step) {
+          const double2 z = buf[Lay::addr(q, t)];
+          zr2 = fma(z.x, z.x, zr2);
+          zi2 = fma(z.y, z.y, zi2);
+          *wd = c * z.x;
+          if (hm) *wm = c2 * z.x;
         }
       }
+      const double cc = c * c + (hm ? c2 * c2 : 0.0);
+      sre = fma(cc, zr2, sre);
+      sim = fma(cc, zi2, sim);
     }
   }
   block_sum2(sre, sim, red);
@@ -607,6 +618,166 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
     atomicAdd(&a.st->sum_im2, sim);
   }
 }
+
+// ---------------------------------------------------------------- Rader
+// k_modes_rader<n>: pass A for a prime n with n - 1 = NP a power of two
+// (BASELINE n = 257: c1, c4). With j = g^p, t = g^-q (g a primitive root),
+//   X_0 = sum_j v_j,   X_{g^-q} = v_0 + sum_p v_{g^p} w^{g^(p-q)} = v_0 + (a (*) b)_q
+// a cyclic convolution of length NP (a_p = v_{g^p}, b_m = w^{g^-m}), done as
+//   A = FFT(a);  conv = conj(FFT(conj(A * bhat)))   (bhat = FFT(b) / NP)
+// so each mode costs two NP-point FFTs instead of the two 2NP-point FFTs of
+// the power-of-two Bluestein, and X_0 = v_0 + A_0. One warp per mode
+// (warp-synchronous, no CTA barrier in the tile loop), persistent CTAs.
+template <int NL> struct RaderPlan;
+template <> struct RaderPlan<257> {
+  static constexpr int NP = 256, S = 16, T = 512, MINB = 1;
+  using WF = WarpFftPad<256, 8, 8, 8, 4>;
+};
+
+struct RaderModesArgs {
+  const double2* shifts;
+  const double2* gaminv;
+  const double* mu1;
+  const double* ghat;
+  double cscale;
+  long long k_begin, k_count;
+  double* W;
+  int m, dim;
+  StatusDev* st;
+  const double2* tw;    // exp(-2 pi i k / NP)
+  const double2* bhat;  // FFT(b) / NP
+  const int* perm;      // g^p mod n
+  const int* qidx;      // q with g^-q = t
+  WLayout wl;
+  const int4* tiles;    // SYM: seg tiles of S modes (see k_modes_blue)
+  long long ntiles;
+};
+
+template <int NL, bool SYM>
+__global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes_rader(RaderModesArgs a) {
+  using P = RaderPlan<NL>;
+  constexpr int NP = P::NP, S = P::S, T = P::T;
+  using WF = typename P::WF;
+  static_assert(T == 32 * S, "one warp per mode");
+  extern __shared__ double2 smem[];
+  __shared__ double red[2 * (T / 32)];
+  __shared__ double2 s_sh[NL], s_gi[NL], s_bh[NP];
+  __shared__ double s_thr[NL];
+  __shared__ short s_perm[NP], s_q[NL];
+  for (int i = threadIdx.x; i < NL; i += T) {
+    const double2 sh = __ldg(a.shifts + i);
+    s_sh[i] = sh;
+    s_thr[i] = 1e-28 * (sh.x * sh.x + sh.y * sh.y);   // space.py:237-240
+    s_gi[i] = __ldg(a.gaminv + i);
+    s_q[i] = (short)__ldg(a.qidx + i);
+    if (i < NP) { s_bh[i] = __ldg(a.bhat + i); s_perm[i] = (short)__ldg(a.perm + i); }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* buf = smem + warp * WF::words;
+  StatusDev* st = a.st;
+  const WLayout& wl = a.wl;
+  double sre = 0.0, sim = 0.0;
+  const long long ntiles = SYM ? a.ntiles : (a.k_count + S - 1) / S;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    bool valid, hm = false;
+    long long kd, km = 0;
+    int k1d = 0, k1m = 0;
+    long long rd = 0, rm = 0;
+    if (SYM) {
+      const int4 tb = __ldg(a.tiles + tile);
+      if (a.dim == 2) {
+        const int k1 = tb.x, k2 = tb.y + warp;
+        valid = k2 < a.m && k2 >= k1;
+        kd = (long long)k1 * a.m + k2;
+        hm = valid && k2 != k1;
+        km = (long long)k2 * a.m + k1;
+        k1d = k1; rd = k2; k1m = k2; rm = k1;
+      } else {
+        const int k1 = tb.x, k2 = tb.y, k3 = tb.z + warp;
+        valid = k3 < a.m;
+        kd = ((long long)k1 * a.m + k2) * a.m + k3;
+        hm = valid && k1 != k2;
+        km = ((long long)k2 * a.m + k1) * a.m + k3;
+        k1d = k1; rd = (long long)k2 * a.m + k3; k1m = k2; rm = (long long)k1 * a.m + k3;
+      }
+      if (!valid) kd = 0;
+    } else {
+      const long long kl = tile * S + warp;
+      valid = kl < a.k_count;
+      kd = a.k_begin + (valid ? kl : 0);
+      const long long local = valid ? kl : 0;
+      if (wl.mode_major) { k1d = (int)(local / wl.P1); rd = local - (long long)k1d * wl.P1; }
+      else rd = local;
+    }
+    if (!valid) continue;
+    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    const double c = __ldg(a.ghat + kd) * a.cscale;
+    const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
+    auto vinv = [&](int j) -> double2 {   // 1 / (s_j + mu), singular test of space.py:237-240
+      const double2 s = s_sh[j];
+      const double dr = s.x + mu, di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (den2 <= s_thr[j]) flag_singular(st, j);
+      const double inv = fast_rcp(den2);
+      return make_double2(dr * inv, -di * inv);
+    };
+    const double2 v0 = vinv(0);
+    auto gen = [&](int p) -> double2 { return vinv(s_perm[p]); };
+    WF::run(buf, lane, a.tw, gen);                     // A = FFT(a)
+    const double2 A0 = buf[WF::pi(0)];
+    __syncwarp();
+    for (int k = lane; k < NP; k += 32) {             // conj(A * bhat), in place
+      const int i = WF::pi(k);
+      buf[i] = cconj(cmul(buf[i], s_bh[k]));
+    }
+    __syncwarp();
+    WF::run_inplace(buf, lane, a.tw);                  // conv_q = conj(buf[q])
+    // store: t along lanes; X_0 = v0 + A0, X_t = v0 + conv_{qidx[t]}
+    const int nsl = wl.mode_major ? wl.nsl : 1;
+    double zr2 = 0.0, zi2 = 0.0;
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
+      long long pd, pm, step;
+      if (wl.mode_major) {
+        const long long nt = wl.sl_nt[sl];
+        const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
+        pd = wl.sl_off[sl] + ((long long)k1d * nt * wl.P1 + rd) * kTBL + lo;
+        pm = wl.sl_off[sl] + ((long long)k1m * nt * wl.P1 + rm) * kTBL + lo;
+        step = 4 * wl.P1 * kTBL;
+      } else {
+        pd = rd + (long long)lane * wl.w_ld;
+        pm = pd;
+        step = 32 * wl.w_ld;
+      }
+      double* __restrict__ wd = a.W + pd;
+      double* __restrict__ wmr = a.W + pm;
+      for (int t = t0 + lane; t < t1; t += 32, wd += step, wmr += step) {
+        double2 X;
+        if (t == 0) X = cadd(v0, A0);
+        else X = cadd(v0, cconj(buf[WF::pi(s_q[t])]));
+        const double2 g = s_gi[t];
+        const double zr = X.x * g.x - X.y * g.y;
+        const double zi = X.x * g.y + X.y * g.x;
+        zr2 = fma(zr, zr, zr2);
+        zi2 = fma(zi, zi, zi2);
+        *wd = c * zr;
+        if (hm) *wmr = c2 * zr;
+      }
+    }
+    const double cc = c * c + c2 * c2;
+    sre = fma(cc, zr2, sre);
+    sim = fma(cc, zi2, sim);
+    __syncwarp();   // buf is rewritten by the next mode
+  }
+  block_sum2(sre, sim, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.st->sum_re2, sre);
+    atomicAdd(&a.st->sum_im2, sim);
+  }
+}
+template <int NL> constexpr size_t rader_smem() { return sizeof(double2) * RaderPlan<NL>::WF::words * RaderPlan<NL>::S; }
 
 template <int NL> constexpr size_t blue_smem() {
   using P = BluePlan<NL>;

@@ -208,6 +208,47 @@ bool build_blue_tables(int n, std::vector<double2>* out, std::string* err) {
   return true;
 }
 
+bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx, std::string* err) {
+  const int NP = n - 1;
+  if (n < 3 || (NP & (NP - 1))) { *err = "n - 1 must be a power of two"; return false; }
+  for (int d = 2; (long long)d * d <= n; ++d)
+    if (n % d == 0) { *err = "n must be prime"; return false; }
+  // smallest primitive root: g^(NP/2) != 1 suffices since NP is a power of two
+  auto powmod = [n](long long b, long long e) {
+    long long r = 1;
+    b %= n;
+    while (e) { if (e & 1) r = r * b % n; b = b * b % n; e >>= 1; }
+    return r;
+  };
+  int g = 2;
+  while (powmod(g, NP / 2) == 1) ++g;
+  const long long ginv = powmod(g, n - 2);
+  cplx->assign(2 * NP, make_double2(0.0, 0.0));
+  idx->assign(NP + n, 0);
+  double2* tw = cplx->data();
+  double2* bhat = tw + NP;
+  int* perm = idx->data();
+  int* qidx = perm + NP;
+  for (int k = 0; k < NP; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / (long double)NP;
+    tw[k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  // b_m = w^(g^-m), w = exp(-2 pi i / n); bhat = DFT_NP(b) / NP
+  std::vector<cld> bb(NP);
+  long long gp = 1, gm = 1;
+  for (int p = 0; p < NP; ++p) {
+    perm[p] = (int)gp;
+    qidx[gm] = p;                      // g^-p = gm
+    const long double a = -2.0L * kPi * (long double)gm / (long double)n;
+    bb[p] = cld(cosl(a), sinl(a));
+    gp = gp * g % n;
+    gm = gm * ginv % n;
+  }
+  host_dft(bb);
+  for (int k = 0; k < NP; ++k) bhat[k] = to_d2(bb[k] / (long double)NP);
+  return true;
+}
+
 void free_fft_plan(FftPlanHost* p) {
   if (p->mem) cudaFree(p->mem);
   p->mem = nullptr;

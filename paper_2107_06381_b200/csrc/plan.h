@@ -39,6 +39,11 @@ void free_fft_plan(FftPlanHost* p);
 // tw (L) | chirp (n) | bhat (L) | wM (n) for the power-of-two Bluestein, n = 2^p + 1.
 bool build_blue_tables(int n, std::vector<double2>* out, std::string* err);
 
+// Rader tables for a prime n with n - 1 a power of two (see fastk::k_modes_rader):
+// cplx = tw (n-1) | bhat (n-1); idx = perm (n-1) | qidx (n), perm[p] = g^p mod n,
+// qidx[t] = q with g^-q = t (t >= 1), g the smallest primitive root.
+bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx, std::string* err);
+
 // Upload the odd-radix codelet constants to the current device (idempotent).
 bool ensure_device_constants(int device, std::string* err);
 

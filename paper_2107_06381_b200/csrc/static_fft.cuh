@@ -340,11 +340,13 @@ namespace sfft {
 // hides the latency of the FP64 / shared-memory chains at 16 warps per SM.
 // Stage s in place: every lane computes its ceil(L/R / 32) butterflies into
 // registers, the warp synchronises, then stores.
-template <int L, int R, int Ns>
+template <int L, int R, int Ns, int PAD = 0>
 struct WStage {
   static constexpr int NB = L / R;
   static constexpr int PER = (NB + 31) / 32;
   static constexpr int TWS = L / (Ns * R);
+  // element i of the per-warp region (PAD > 0: one spare slot every PAD elements)
+  static __device__ __forceinline__ int pi(int i) { return PAD ? i + i / PAD : i; }
 
   template <class Gen>
   static __device__ __forceinline__ void first(double2* buf, int lane, Gen& gen) {
@@ -358,7 +360,7 @@ struct WStage {
         for (int r = 0; r < R; ++r) v[r] = gen(b + r * NB);
         Cod<R>::run(v);
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[b * R + r] = v[r];
+        for (int r = 0; r < R; ++r) buf[pi(b * R + r)] = v[r];
       }
     }
     __syncwarp();
@@ -371,7 +373,7 @@ struct WStage {
       const int b = lane + 32 * i;
       if (b < NB) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[i][r] = buf[b + r * NB];
+        for (int r = 0; r < R; ++r) v[i][r] = buf[pi(b + r * NB)];
         if (Ns > 1) apply_twiddles<R>(v[i], __ldg(tw + (b % Ns) * TWS));
         Cod<R>::run(v[i]);
       }
@@ -384,18 +386,18 @@ struct WStage {
         const int k = b % Ns;
         const int base = (b - k) * R + k;
 #pragma unroll
-        for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[i][r];
+        for (int r = 0; r < R; ++r) buf[pi(base + r * Ns)] = v[i][r];
       }
     }
     __syncwarp();
   }
 };
 
-template <int L, int Ns, int R, int... Rest>
+template <int L, int PAD, int Ns, int R, int... Rest>
 struct WRunner {
   static __device__ __forceinline__ void tail(double2* buf, int lane, const double2* tw) {
-    WStage<L, R, Ns>::mid(buf, lane, tw);
-    if constexpr (sizeof...(Rest) > 0) WRunner<L, Ns * R, Rest...>::tail(buf, lane, tw);
+    WStage<L, R, Ns, PAD>::mid(buf, lane, tw);
+    if constexpr (sizeof...(Rest) > 0) WRunner<L, PAD, Ns * R, Rest...>::tail(buf, lane, tw);
   }
 };
 
@@ -405,7 +407,23 @@ struct WarpFft {
   template <class Gen>
   static __device__ __forceinline__ void run(double2* buf, int lane, const double2* tw, Gen& gen) {
     WStage<L, R1, 1>::first(buf, lane, gen);
-    if constexpr (sizeof...(Rest) > 0) WRunner<L, R1, Rest...>::tail(buf, lane, tw);
+    if constexpr (sizeof...(Rest) > 0) WRunner<L, 0, R1, Rest...>::tail(buf, lane, tw);
+  }
+};
+
+// Same with a padded per-warp region (element i at i + i/PAD) and a variant
+// whose first stage also reads the region (in place).
+template <int L, int PAD, int R1, int... Rest>
+struct WarpFftPad {
+  static __device__ __forceinline__ int pi(int i) { return WStage<L, R1, 1, PAD>::pi(i); }
+  static constexpr int words = L + L / PAD + 1;
+  template <class Gen>
+  static __device__ __forceinline__ void run(double2* buf, int lane, const double2* tw, Gen& gen) {
+    WStage<L, R1, 1, PAD>::first(buf, lane, gen);
+    if constexpr (sizeof...(Rest) > 0) WRunner<L, PAD, R1, Rest...>::tail(buf, lane, tw);
+  }
+  static __device__ __forceinline__ void run_inplace(double2* buf, int lane, const double2* tw) {
+    WRunner<L, PAD, 1, R1, Rest...>::tail(buf, lane, tw);
   }
 };
 

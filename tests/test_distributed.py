@@ -168,6 +168,7 @@ def emulate(system, world):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dim,cells,steps,world", [(2, 16, 12, 2), (2, 20, 9, 3), (3, 8, 6, 2), (3, 9, 7, 4),
+                                                   (2, 12, 256, 2), (3, 7, 256, 3), (2, 10, 1024, 2),
                                                    (2, 512, 512, 8)])
 def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
     import paper_2107_06381_b200 as B
