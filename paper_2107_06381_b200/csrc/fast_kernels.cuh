@@ -661,18 +661,31 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
   static_assert(T == 32 * S, "one warp per mode");
   extern __shared__ double2 smem[];
   __shared__ double red[2 * (T / 32)];
-  __shared__ double2 s_sh[NL], s_gi[NL], s_bh[NP];
-  __shared__ double s_thr[NL];
-  __shared__ short s_perm[NP], s_q[NL];
+  // shifts and singular thresholds in the permuted order p (j = g^p), so the
+  // generator reads consecutive slots; index 0 of s_sh0 / s_thr0 is j = 0.
+  __shared__ double2 s_shp[NP], s_gi[NL], s_bh[NP];
+  __shared__ double s_thrp[NP];
+  __shared__ short s_q[NL];
+  __shared__ double2 s_sh0;
+  __shared__ double s_thr0;
   for (int i = threadIdx.x; i < NL; i += T) {
-    const double2 sh = __ldg(a.shifts + i);
-    s_sh[i] = sh;
-    s_thr[i] = 1e-28 * (sh.x * sh.x + sh.y * sh.y);   // space.py:237-240
     s_gi[i] = __ldg(a.gaminv + i);
     s_q[i] = (short)__ldg(a.qidx + i);
-    if (i < NP) { s_bh[i] = __ldg(a.bhat + i); s_perm[i] = (short)__ldg(a.perm + i); }
+    if (i < NP) {
+      const int j = __ldg(a.perm + i);
+      const double2 sh = __ldg(a.shifts + j);
+      s_shp[i] = sh;
+      s_thrp[i] = 1e-28 * (sh.x * sh.x + sh.y * sh.y);   // space.py:237-240
+      s_bh[i] = __ldg(a.bhat + i);
+    }
+    if (i == 0) {
+      const double2 sh = __ldg(a.shifts);
+      s_sh0 = sh;
+      s_thr0 = 1e-28 * (sh.x * sh.x + sh.y * sh.y);
+    }
   }
   __syncthreads();
+  const int* perm = a.perm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* buf = smem + warp * WF::words;
   StatusDev* st = a.st;
@@ -714,16 +727,16 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
     const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
     const double c = __ldg(a.ghat + kd) * a.cscale;
     const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
-    auto vinv = [&](int j) -> double2 {   // 1 / (s_j + mu), singular test of space.py:237-240
-      const double2 s = s_sh[j];
+    // 1 / (s + mu) with the singular test of space.py:237-240 (column j reported)
+    auto vinv = [&](double2 s, double thr, auto col) -> double2 {
       const double dr = s.x + mu, di = s.y;
       const double den2 = dr * dr + di * di;
-      if (den2 <= s_thr[j]) flag_singular(st, j);
+      if (den2 <= thr) flag_singular(st, col());
       const double inv = fast_rcp(den2);
       return make_double2(dr * inv, -di * inv);
     };
-    const double2 v0 = vinv(0);
-    auto gen = [&](int p) -> double2 { return vinv(s_perm[p]); };
+    const double2 v0 = vinv(s_sh0, s_thr0, [] { return 0; });
+    auto gen = [&](int p) -> double2 { return vinv(s_shp[p], s_thrp[p], [&] { return __ldg(perm + p); }); };
     WF::run(buf, lane, a.tw, gen);                     // A = FFT(a)
     const double2 A0 = buf[WF::pi(0)];
     __syncwarp();
