@@ -370,3 +370,39 @@ def test_full_size_solve_vs_device_oracle(name):
     assert _chunked_rel(y, orc) <= tol
     del y, orc
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("n", [9, 257, 513, 1025])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_fused_solve_reports_singular_column(n, dim):
+    """A shift s_j = -mu_k makes (s_j - lap) singular (space.py:237-240): every
+    pass-A kernel (generic, Rader 257, warp 513, Bluestein 1025; symmetric and
+    plain tile lists) must report column j, also where j enters permuted."""
+    import ctypes
+    from paper_2107_06381_b200 import _lib, plans
+    if dim == 3 and n > 513:
+        pytest.skip("size")
+    cells = 6
+    grid = B.build_grid(dim, 1.0, cells)
+    mu1 = B.space.mu1_of(grid)
+    sp = plans.space_plan(dim, cells, mu1)
+    diag = B.diagonalize(n, -0.3)
+    shifts = diag.eigenvalues / 0.01
+    k = [1, 2, 0][:dim]
+    mu = mu1[k[0]] if dim == 1 else (mu1[k[0]] + mu1[k[1]] if dim == 2 else (mu1[k[0]] + mu1[k[1]]) + mu1[k[2]])
+    j0 = 5
+    shifts = shifts.copy()
+    shifts[j0] = -mu
+    tp = plans.time_plan(diag.gamma, shifts)
+    lib = _lib.lib()
+    g = torch.ones(grid.n_interior, dtype=torch.float64, device="cuda")
+    y = torch.empty((n, grid.n_interior), dtype=torch.float64, device="cuda")
+    nb = int(lib.bhcp_pint_workspace_bytes(sp.handle, tp.handle))
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.bhcp_pint_solve(sp.handle, tp.handle, plans.ptr(g), 1.0, plans.ptr(y), plans.ptr(ws), nb,
+                                   plans.stream_handle()), "bhcp_pint_solve")
+    st = _lib.Status()
+    status = ctypes.c_void_p(lib.bhcp_pint_status_ptr(sp.handle, tp.handle, plans.ptr(ws)))
+    _lib.check(lib.bhcp_read_status(status, 1e-8, ctypes.byref(st), plans.stream_handle()), "bhcp_read_status")
+    assert st.code == _lib.BHCP_ERR_SINGULAR_SHIFT
+    assert st.bad_column == j0
