@@ -156,6 +156,18 @@ int bhcp_pint_solve_unfused(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
                             const double* g_dev, double divisor, double* y_dev,
                             void* ws, size_t ws_bytes, void* stream);
 
+/* Pass A with per-slab destinations: slab s (levels [slab_bounds[s],
+ * slab_bounds[s+1])) of this rank's W goes to slab_dst[s] (host array of
+ * nslabs device pointers), in the blocked layout of bhcp_pint_modes. A
+ * destination may be another GPU's receive buffer mapped into this process
+ * (NVLink peer memory), so pass A stores straight into the rank that runs
+ * the level passes on that slab and no separate all-to-all runs
+ * (distributed.py, transport "peer"). Replaces, with the all-to-all, the
+ * reference's space<->time transpose. */
+int bhcp_pint_modes_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat,
+                       int64_t k_begin, int64_t k_end, double* const* slab_dst, int nslabs,
+                       const int64_t* slab_bounds, void* status, void* stream);
+
 /* The two halves of the fused solve (also used by the slab-decomposed
  * multi-GPU driver).
  * bhcp_pint_ghat: ghat = DST(g) * scale (n_space float64), scale = 1/(divisor*n).

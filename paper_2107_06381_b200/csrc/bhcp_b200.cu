@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_modes(ModesArgs a) {
     const double wr = c * Z.x, wi = c * Z.y;
     sre = fma(wr, wr, sre);
     sim = fma(wi, wi, sim);
-    a.W[a.wl.addr(kl, t)] = wr;
+    *a.wl.ptr(kl, t) = wr;
   }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
@@ -703,7 +703,7 @@ __global__ void k_spectral_w(SpectralArgs a, long long nx) {
     else denom = a.alpha * (mu + 1.0 / a.tau) + decay;
     const double amp = a.ghat[k] / denom;
     for (long long t = threadIdx.x; t < a.n; t += blockDim.x)
-      a.W[a.wl.addr(k, (int)t)] = amp * pow(rho, (double)t);
+      *a.wl.ptr(k, (int)t) = amp * pow(rho, (double)t);
   }
 }
 
@@ -1132,8 +1132,10 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
 }
 
 int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
-                 long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
+                 long long k_begin, long long k_end, double* W, const fastk::WLayout& wl_in, StatusDev* st,
                  cudaStream_t s) {
+  fastk::WLayout wl = wl_in;
+  if (!wl.sl_base[0]) wl.bind(W);   // local W unless the caller set per-slab destinations
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
@@ -1589,6 +1591,31 @@ int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
                       as_stream(stream));
 }
 
+int bhcp_pint_modes_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat_dev, int64_t k_begin,
+                       int64_t k_end, double* const* slab_dst, int nslabs, const int64_t* slab_bounds,
+                       void* status_dev, void* stream) {
+  if (!sp || !tp || !ghat_dev || !slab_dst || !status_dev) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (nslabs < 1 || nslabs > 8) return fail(BHCP_ERR_INVALID, "nslabs must be in [1, 8]");
+  for (int s = 0; s < nslabs; ++s)
+    if (!slab_dst[s]) return fail(BHCP_ERR_INVALID, "null slab destination");
+  if (k_begin < 0 || k_end > sp->nx || k_begin > k_end) return fail(BHCP_ERR_INVALID, "bad mode range");
+  if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "level slabs need dim >= 2");
+  const long long P1 = ipow(sp->m, sp->dim - 1);
+  if (k_begin % P1 || k_end % P1) return fail(BHCP_ERR_INVALID, "mode range must hold whole k1 planes");
+  if (!slab_bounds || slab_bounds[0] != 0 || slab_bounds[nslabs] != tp->n)
+    return fail(BHCP_ERR_INVALID, "slab bounds must cover [0, n_levels)");
+  for (int i = 1; i <= nslabs; ++i) {
+    if (slab_bounds[i] < slab_bounds[i - 1]) return fail(BHCP_ERR_INVALID, "slab bounds not sorted");
+    if (i < nslabs && slab_bounds[i] % fastk::kTBL && slab_bounds[i] != tp->n)
+      return fail(BHCP_ERR_INVALID, "slab bounds must be multiples of 8");
+  }
+  DeviceGuard g(sp->device);
+  fastk::WLayout wl = make_blocked(sp, k_end - k_begin, nslabs, (const long long*)slab_bounds);
+  for (int s = 0; s < nslabs; ++s) wl.sl_base[s] = slab_dst[s];
+  return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, slab_dst[0], wl, (StatusDev*)status_dev,
+                      as_stream(stream));
+}
+
 int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, double* y_dev,
                          int64_t nlev, int pass, void* stream) {
   if (!sp || !in_dev || !y_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
@@ -1695,6 +1722,7 @@ int bhcp_spectral_solve(const bhcp_space_plan* sp, int kind, double alpha, doubl
   SpectralArgs a{};
   a.ghat = ghat; a.mu1 = sp->mu1_dev; a.m = sp->m; a.dim = sp->dim; a.kind = kind; a.alpha = alpha; a.tau = tau;
   a.num_steps = num_steps; a.n = n; a.W = W; a.wl = native_layout(sp, sp->nx, (int)n);
+  a.wl.bind(W);
   k_spectral_w<<<2048, dim3(32, 8), 0, s>>>(a, sp->nx);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_spectral_w");
   for (int p = 0; p < sp->dim; ++p) {

@@ -37,6 +37,9 @@ __device__ __forceinline__ double fast_rcp(double x) {
 //       k = k1 * P1 + r (local mode), tl = t - c_s, off_s = nmodes * 8 * sum NT_{s'<s}
 //     so a spatial line of 8 levels is contiguous for the level pass and
 //     each destination slab is one contiguous all-to-all chunk.
+//   sl_base[s]: where slab s starts -- W + off_s for a local W, or a chunk of
+//     another GPU's receive buffer (peer memory over NVLink) when pass A
+//     stores straight into the destination rank (bhcp_pint_modes_to).
 constexpr int kTBL = 8;
 struct WLayout {
   int mode_major;
@@ -44,16 +47,21 @@ struct WLayout {
   int sl_c[9];
   long long sl_off[8];
   long long sl_nt[8];
+  double* sl_base[8];
   long long nmodes;
   long long w_ld;
   long long P1;
-  __host__ __device__ __forceinline__ long long addr(long long k, int t) const {
-    if (!mode_major) return (long long)t * w_ld + k;
+  __host__ __device__ __forceinline__ double* ptr(long long k, int t) const {
+    if (!mode_major) return sl_base[0] + (long long)t * w_ld + k;
     int s = 0;
     while (s + 1 < nsl && t >= sl_c[s + 1]) ++s;
     const long long tl = t - sl_c[s];
     const long long k1 = k / P1, r = k - k1 * P1;
-    return sl_off[s] + ((k1 * sl_nt[s] + tl / kTBL) * P1 + r) * kTBL + (tl % kTBL);
+    return sl_base[s] + ((k1 * sl_nt[s] + tl / kTBL) * P1 + r) * kTBL + (tl % kTBL);
+  }
+  // local W: slab s starts at W + sl_off[s]
+  __host__ __device__ __forceinline__ void bind(double* W) {
+    for (int s = 0; s < 8; ++s) sl_base[s] = (mode_major && s < nsl) || s == 0 ? W + (mode_major ? sl_off[s] : 0) : nullptr;
   }
   __host__ __device__ __forceinline__ long long total(int n) const {
     if (!mode_major) return (long long)n * w_ld;
@@ -382,8 +390,8 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
       long long pd, pm, step;
       if (wl.mode_major) {
         const long long nt = wl.sl_nt[sl];
-        pd = wl.sl_off[sl] + ((long long)k1d * nt * wl.P1 + rd) * kTBL;
-        pm = wl.sl_off[sl] + ((long long)k1m * nt * wl.P1 + rm) * kTBL;
+        pd = ((long long)k1d * nt * wl.P1 + rd) * kTBL;
+        pm = ((long long)k1m * nt * wl.P1 + rm) * kTBL;
         // t = t0 + lane + 32 i  ->  (tl >> 3) * P1*8 + (tl & 7), t0 a multiple of 8
         const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
         pd += lo; pm += lo;
@@ -393,8 +401,8 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
         pm = km + (long long)lane * wl.w_ld;
         step = 32 * wl.w_ld;
       }
-      double* __restrict__ wd = a.W + pd;
-      double* __restrict__ wm = a.W + pm;
+      double* __restrict__ wd = wl.sl_base[sl] + pd;
+      double* __restrict__ wm = wl.sl_base[sl] + pm;
       for (int t = t0 + lane; t < t1; t += 32, wd += step, wm += step) {
         const double2 x = X[t];
         const double2 g = s_gi[t];
@@ -589,16 +597,16 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
         if (wl.mode_major) {
           const long long nt = wl.sl_nt[sl];
           const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-          pd = wl.sl_off[sl] + ((long long)s_k1d[q] * nt * wl.P1 + s_rd[q]) * kTBL + lo;
-          pm = wl.sl_off[sl] + ((long long)s_k1m[q] * nt * wl.P1 + s_rm[q]) * kTBL + lo;
+          pd = ((long long)s_k1d[q] * nt * wl.P1 + s_rd[q]) * kTBL + lo;
+          pm = ((long long)s_k1m[q] * nt * wl.P1 + s_rm[q]) * kTBL + lo;
           step = 4 * wl.P1 * kTBL;
         } else {
           pd = s_rd[q] + (long long)lane * wl.w_ld;
           pm = pd;
           step = 32 * wl.w_ld;
         }
-        double* __restrict__ wd = a.W + pd;
-        double* __restrict__ wm = a.W + pm;
+        double* __restrict__ wd = wl.sl_base[sl] + pd;
+        double* __restrict__ wm = wl.sl_base[sl] + pm;
         for (int t = t0 + lane; t < t1; t += 32, wd += step, wm += step) {
           const double2 z = buf[Lay::addr(q, t)];
           zr2 = fma(z.x, z.x, zr2);
@@ -756,16 +764,16 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
       if (wl.mode_major) {
         const long long nt = wl.sl_nt[sl];
         const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-        pd = wl.sl_off[sl] + ((long long)k1d * nt * wl.P1 + rd) * kTBL + lo;
-        pm = wl.sl_off[sl] + ((long long)k1m * nt * wl.P1 + rm) * kTBL + lo;
+        pd = ((long long)k1d * nt * wl.P1 + rd) * kTBL + lo;
+        pm = ((long long)k1m * nt * wl.P1 + rm) * kTBL + lo;
         step = 4 * wl.P1 * kTBL;
       } else {
         pd = rd + (long long)lane * wl.w_ld;
         pm = pd;
         step = 32 * wl.w_ld;
       }
-      double* __restrict__ wd = a.W + pd;
-      double* __restrict__ wmr = a.W + pm;
+      double* __restrict__ wd = wl.sl_base[sl] + pd;
+      double* __restrict__ wmr = wl.sl_base[sl] + pm;
       for (int t = t0 + lane; t < t1; t += 32, wd += step, wmr += step) {
         double2 X;
         if (t == 0) X = cadd(v0, A0);

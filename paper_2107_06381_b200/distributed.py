@@ -134,6 +134,75 @@ def sharded_solve(ops, comm, layout: SlabLayout, rank: int, events=None):
     return y, layout.lev[rank]
 
 
+def peer_offsets(layout: SlabLayout, rank: int) -> List[int]:
+    """Element offset of `rank`'s chunk inside every destination q's receive
+    buffer -- exactly where all_to_all_single places it (senders in rank order)."""
+    return [int(sum(layout.recv_splits(q)[:rank])) for q in range(layout.world)]
+
+
+def sharded_solve_peer(ops, transport, layout: SlabLayout, rank: int, events=None):
+    """The same solve with pass A storing straight into the receivers' buffers
+    (bhcp_pint_modes_to over NVLink peer memory): no separate all-to-all, the
+    transfer overlaps pass A's compute store by store. Two device barriers:
+    receivers are done with the previous solve's buffer; all stores landed."""
+    transport.barrier()
+    if events:
+        events[0].record()
+    ops.modes_to(layout, rank, transport.dst)
+    if events:
+        events[1].record()
+    transport.barrier()
+    if events:
+        events[2].record()
+    koff = ops.tables(layout, rank)
+    y = ops.levels_blocked(transport.recv, koff, layout.levels(rank))
+    if events:
+        events[3].record()
+    return y, layout.lev[rank]
+
+
+class PeerTransport:
+    """Receive buffers in symmetric memory (torch.distributed._symmetric_memory,
+    CUDA peer mappings over NVLink / NVSwitch): rank p's pass A writes its
+    chunk for rank q at q's buffer + peer_offsets(p)[q]."""
+
+    def __init__(self, layout: SlabLayout, rank: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        group = group or dist.group.WORLD
+        try:
+            symm_mem.enable_symm_mem_for_group(group.group_name)
+        except Exception:  # newer torch enables it on rendezvous
+            pass
+        size = max(int(sum(layout.recv_splits(q))) for q in range(layout.world))
+        self.buf = symm_mem.empty(max(size, 1), dtype=torch.float64, device=device)
+        self.hdl = symm_mem.rendezvous(self.buf, group)
+        ptrs = list(self.hdl.buffer_ptrs)
+        offs = peer_offsets(layout, rank)
+        self.dst = (ctypes.c_void_p * layout.world)(*[int(ptrs[q]) + 8 * offs[q] for q in range(layout.world)])
+        self.recv = self.buf[: int(sum(layout.recv_splits(rank)))]
+
+    def barrier(self):
+        self.hdl.barrier()
+
+
+def make_transport(kind: str, layout: SlabLayout, rank: int, device):
+    """'peer' (NVLink stores from pass A), 'nccl' (all_to_all_single), or
+    'auto' = peer when symmetric memory can be set up, else nccl."""
+    if kind not in ("auto", "peer", "nccl"):
+        raise ValueError(f"unknown transport {kind!r}")
+    if kind == "nccl":
+        return None
+    try:
+        return PeerTransport(layout, rank, device)
+    except Exception:
+        if kind == "peer":
+            raise
+        return None
+
+
 def reduce_status(comm, sre: float, sim: float, bad: int) -> Tuple[float, float, int]:
     """Sum the residue accumulators and min-reduce the first singular column."""
     s = comm.all_reduce_sum([sre, sim])
@@ -221,6 +290,18 @@ class DeviceOps:
                                                  p.stream_handle()), "modes")
         return self._W
 
+    def modes_to(self, layout: SlabLayout, rank: int, dst):
+        """Pass A with slab q stored at dst[q] (ctypes array of device pointers,
+        local or peer-mapped)."""
+        p = self.plans
+        kb, ke = layout.mode_range(rank)
+        bounds = layout.slab_bounds()
+        self.prepare()
+        self._lib.check(self.lib.bhcp_pint_modes_to(self.plan.sp.handle, self.plan.tp.handle, p.ptr(self.ghat), kb, ke,
+                                                    ctypes.cast(dst, ctypes.c_void_p), layout.world,
+                                                    bounds.ctypes.data_as(ctypes.c_void_p), p.ptr(self.status),
+                                                    p.stream_handle()), "modes_to")
+
     def tables(self, layout: SlabLayout, rank: int):
         key = (layout.world, rank)
         if key not in self._tables:
@@ -260,10 +341,12 @@ def check_global_status(comm, ops, shifts, tol: float = 1e-8):
     return norm, residue
 
 
-def solve_pint_sharded(system, comm=None):
+def solve_pint_sharded(system, comm=None, transport: str = "auto"):
     """Drop-in style entry point under torch.distributed: every rank calls it
     with the same system; returns (local level slab y (L_r, n_space) on this
-    rank's GPU, (level_begin, level_end))."""
+    rank's GPU, (level_begin, level_end)). ``transport``: 'peer' (pass A
+    stores into the receivers over NVLink), 'nccl' (all_to_all_single) or
+    'auto'. Both give the single-GPU result bit for bit."""
     import torch
     import torch.distributed as dist
 
@@ -279,12 +362,24 @@ def solve_pint_sharded(system, comm=None):
     plan = pint_plan(grid, tg, system.omega)
     divisor = condition_divisor(system.method.kind, system.method.alpha, tg.tau)
     ops = DeviceOps(plan, plans.to_device(system.data, torch.float64), divisor)
-    y, lev = sharded_solve(ops, comm, layout, rank)
+    peer = make_transport(transport, layout, rank, torch.device("cuda", torch.cuda.current_device()))
+    if peer is not None:
+        y, lev = sharded_solve_peer(ops, peer, layout, rank)
+    else:
+        y, lev = sharded_solve(ops, comm, layout, rank)
     check_global_status(comm, ops, plan.shifts)
     return y, lev
 
 
 # ---------------------------------------------------------------- bench (N > 1)
+
+def _nvlink_stats(nbytes: float, ms: float, transport: str) -> dict:
+    """Bytes each rank sends to its peers and the rate over the phase that
+    carries them (the all-to-all, or pass A itself for peer stores)."""
+    gbps = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+    return {"bytes_per_rank": nbytes, "carried_by": "pass A stores" if transport == "peer" else "all_to_all",
+            "achieved_GBps": gbps, "peak_GBps": 770.0, "frac": gbps / 770.0}
+
 
 def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric, unit):
     import torch
@@ -299,10 +394,19 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     divisor = system.method.condition_divisor(tg.tau)
     ops = DeviceOps(plan, torch.from_numpy(w.g_delta).to(dev), divisor)
     comm = TorchComm(dev)
+    import os
+    peer = make_transport(os.environ.get("BHCP_TRANSPORT", "auto"), layout, rank, dev)
+    transport = "peer" if peer is not None else "nccl"
+
+    def solve(events=None):
+        if peer is not None:
+            return sharded_solve_peer(ops, peer, layout, rank, events=events)
+        return sharded_solve(ops, comm, layout, rank, events=events)
+
     sampler = ClockSampler(dev.index)
     sampler.start()
     for _ in range(args.warmup):
-        sharded_solve(ops, comm, layout, rank)
+        solve()
     torch.cuda.synchronize()
     check_global_status(comm, ops, plan.shifts)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
@@ -312,7 +416,7 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     torch.cuda.synchronize()
     t0.record()
     for k in range(args.steps):
-        sharded_solve(ops, comm, layout, rank, events=evs[k])
+        solve(events=evs[k])
     t1.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -336,7 +440,7 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
 
     def e2e_step():
         g_dev.copy_(g_host, non_blocking=True)
-        y, _ = sharded_solve(ops, comm, layout, rank)
+        y, _ = solve()
         y_host.copy_(y, non_blocking=True)
 
     for _ in range(2):
@@ -367,15 +471,17 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
         "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, slab-decomposed over {world} GPUs",
-                   "dof_per_solve": w.dof, "parallelism": f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
+                   "dof_per_solve": w.dof, "transport": transport,
+                   "parallelism": (f"mode slabs -> pass A stores into the level-slab owners over NVLink peer memory "
+                                   f"-> level slabs, P={world}") if peer is not None else
+                                  f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
                    "l2": "working set larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": ["pass A (k_modes_fast)", "", "pass B (level passes)"][dom],
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": kind},
-        "phases_ms_rank0": {"pass_a_modes": ph[0], "all_to_all": ph[1], "pass_b_levels": ph[2]},
-        "nvlink": {"bytes_per_rank": a2a_bytes, "achieved_GBps": a2a_bytes / (ph[1] * 1e-3) / 1e9 if ph[1] > 0 else 0.0,
-                   "peak_GBps": 770.0,
-                   "frac": (a2a_bytes / (ph[1] * 1e-3) / 1e9 / 770.0) if ph[1] > 0 else 0.0},
+        "phases_ms_rank0": {"pass_a_modes": ph[0], ("rank_barrier" if peer is not None else "all_to_all"): ph[1],
+                            "pass_b_levels": ph[2]},
+        "nvlink": _nvlink_stats(a2a_bytes, ph[0] if peer is not None else ph[1], transport),
         "e2e": {"value": w.dof / (e2e_ms * 1e-3), "unit": unit, "h2d_bytes_per_step": 8 * w.n_space,
                 "d2h_bytes_per_step": 8 * (c1 - c0) * w.n_space, "ms_per_step": e2e_ms},
         "gpu_launches": launches * args.steps,

@@ -47,6 +47,25 @@ def test_layout_tables_address_every_line_once(dim, m, n, world):
     assert all(c % tb == 0 or c == n for c, _ in L.lev)
 
 
+@pytest.mark.parametrize("dim,m,n,world", [(2, 7, 9, 2), (2, 5, 30, 3), (3, 4, 17, 4)])
+def test_peer_offsets_match_all_to_all_placement(dim, m, n, world):
+    """Pass A stores of the peer transport land exactly where all_to_all_single
+    would put each sender's chunk."""
+    L = D.SlabLayout(dim, m, n, world)
+    for q in range(world):
+        recv = L.recv_splits(q)
+        starts = np.concatenate([[0], np.cumsum(recv)[:-1]]).astype(int)
+        for p in range(world):
+            assert D.peer_offsets(L, p)[q] == starts[p]
+            assert L.send_splits(p)[q] == recv[p]
+
+
+def test_transport_names():
+    with pytest.raises(ValueError):
+        D.make_transport("shmem", D.SlabLayout(2, 5, 9, 2), 0, None)
+    assert D.make_transport("nccl", D.SlabLayout(2, 5, 9, 2), 0, None) is None
+
+
 def test_layout_rejects_1d():
     with pytest.raises(ValueError):
         D.SlabLayout(1, 255, 257, 2)
@@ -142,6 +161,31 @@ def test_gloo_world2_matches_oracle(kind, dim, cells, steps):
 
 # ---------------------------------------------------------------- GPU emulation
 
+def emulate_peer(system, world):
+    """Peer transport emulated on one GPU: one receive buffer per rank; each
+    rank's pass A stores straight into all of them (bhcp_pint_modes_to)."""
+    import ctypes
+
+    import torch
+
+    import paper_2107_06381_b200 as B
+    from paper_2107_06381_b200 import plans
+
+    grid, tg = system.grid, system.timegrid
+    layout = D.SlabLayout(grid.dim, grid.num_cells - 1, tg.n_levels, world)
+    plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
+    ops = D.DeviceOps(plan, plans.to_device(system.data, torch.float64),
+                      system.method.condition_divisor(tg.tau))
+    recv = [torch.full((max(1, sum(layout.recv_splits(q))),), float("nan"), dtype=torch.float64, device="cuda")
+            for q in range(world)]
+    for p in range(world):
+        offs = D.peer_offsets(layout, p)
+        dst = (ctypes.c_void_p * world)(*[recv[q].data_ptr() + 8 * offs[q] for q in range(world)])
+        ops.modes_to(layout, p, dst)
+    ys = [ops.levels_blocked(recv[q], ops.tables(layout, q), layout.levels(q)).clone() for q in range(world)]
+    return torch.cat(ys).cpu().numpy()
+
+
 def emulate(system, world):
     import torch
 
@@ -180,3 +224,4 @@ def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
     single = B.solve_pint(system).trajectory
     multi = emulate(system, world)
     assert np.array_equal(single, multi)
+    assert np.array_equal(single, emulate_peer(system, world))

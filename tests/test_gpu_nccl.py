@@ -25,11 +25,12 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
 w = workloads.make_small(2, 40, 30, seed=5)
 grid = B.build_grid(2, w.length, 40)
 system = B.assemble(B.MethodKind.PINT_QBVM, 1e-3, grid, B.TimeGrid(w.horizon, 30), w.g_delta)
-y, (c, d) = solve_pint_sharded(system)
 ref = B.solve_pint(system).trajectory
-assert (c, d) == (0, 31)
-assert np.array_equal(y.cpu().numpy(), ref), "sharded != single"
-print("SHARDED_OK")
+for transport in ("nccl", "peer"):
+    y, (c, d) = solve_pint_sharded(system, transport=transport)
+    assert (c, d) == (0, 31)
+    assert np.array_equal(y.cpu().numpy(), ref), f"sharded ({{transport}}) != single"
+    print("SHARDED_OK", transport)
 dist.destroy_process_group()
 '''
 
@@ -52,13 +53,16 @@ def test_solve_pint_sharded_world1_nccl(tmp_path):
     script.write_text(SCRIPT.format(root=ROOT))
     r = torchrun([str(script)])
     assert r.returncode == 0, r.stderr[-2000:]
-    assert "SHARDED_OK" in r.stdout
+    assert "SHARDED_OK nccl" in r.stdout and "SHARDED_OK peer" in r.stdout
 
 
-def test_bench_sharded_line_world1():
-    r = torchrun(["bench.py", "--gpus", "1", "--steps", "3", "--warmup", "1"], env={"BHCP_FORCE_SHARDED": "1"})
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_bench_sharded_line_world1(transport):
+    r = torchrun(["bench.py", "--gpus", "1", "--steps", "3", "--warmup", "1"],
+                 env={"BHCP_FORCE_SHARDED": "1", "BHCP_TRANSPORT": transport})
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for key in ("metric", "value", "unit", "n_gpus", "ms_per_step", "e2e", "gpu_launches", "clocks", "roofline"):
         assert key in line
     assert line["value"] > 0
+    assert line["config"]["transport"] == transport
