@@ -1250,8 +1250,8 @@ int cols3_launch(const bhcp_space_plan* sp, gdst::ArgsB2 a, cudaStream_t s) {
   if (tiles == 0) return BHCP_OK;
   if (tiles > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "too many tiles");
   const size_t sm = gdst::smemC3_bytes<N>();
-  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_cols3<N>, 256, sm));
-  k_dst_cols3<N><<<(unsigned)grid, 256, sm, s>>>(a);
+  const long long grid = std::min<long long>(tiles, resident_ctas(k_dst_cols3<N>, PlanC3<N>::T, sm));
+  k_dst_cols3<N><<<(unsigned)grid, PlanC3<N>::T, sm, s>>>(a);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_cols3 launch");
   return BHCP_OK;
 }

@@ -191,26 +191,28 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
 }
 
 template <int N> struct PlanC3;
-template <> struct PlanC3<256> { static constexpr int S = 16; template <class Lay> using F = Fft<256, 16, 256, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
-template <> struct PlanC3<512> { static constexpr int S = 8; template <class Lay> using F = Fft<512, 8, 256, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
-template <> struct PlanC3<1024> { static constexpr int S = 4; template <class Lay> using F = Fft<1024, 4, 256, Lay, 16, 8, 8>; static constexpr int R1 = 16; };
+// T threads per CTA, 2 CTAs per SM (the in-place stages hold S*N/T points per thread)
+template <> struct PlanC3<256> { static constexpr int S = 16, T = 256; template <class Lay> using F = Fft<256, 16, T, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
+template <> struct PlanC3<512> { static constexpr int S = 8, T = 256; template <class Lay> using F = Fft<512, 8, T, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
+template <> struct PlanC3<1024> { static constexpr int S = 4, T = 256; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; static constexpr int R1 = 16; };
 
 template <int N> constexpr size_t smemC3_bytes() {
-  return sizeof(double2) * (PlanC3<N>::S * N) + sizeof(double) * (N + 2 * 8 * PlanC3<N>::S);
+  return sizeof(double2) * (PlanC3<N>::S * N) + sizeof(double) * (N + 2 * (PlanC3<N>::T / 32) * PlanC3<N>::S);
 }
 
 template <int N>
-__global__ void __launch_bounds__(256, 2) k_dst_cols3(ArgsB2 a) {
-  constexpr int S = PlanC3<N>::S, T = 256, m = N - 1, LW = 2 * S;   // LW lines per tile
+__global__ void __launch_bounds__(PlanC3<N>::T, 2) k_dst_cols3(ArgsB2 a) {
+  constexpr int S = PlanC3<N>::S, T = PlanC3<N>::T, m = N - 1, LW = 2 * S;   // LW lines per tile
+  constexpr int NW = T / 32;
   constexpr int KK = 32 / S;                 // k values per warp step
-  constexpr int KW = (N / 2) / 8;            // k values per warp (8 warps)
+  constexpr int KW = (N / 2) / NW;           // k values per warp
   constexpr int STEPS = KW / KK;
   using Lay = Interleaved<S>;
   extern __shared__ double2 smem[];
   double2* buf = smem;
   double* bufd = reinterpret_cast<double*>(smem);
   double* sn = reinterpret_cast<double*>(smem + S * N);
-  double* tot = sn + N;                       // [8 warps][S q][2 lines]
+  double* tot = sn + N;                       // [NW warps][S q][2 lines]
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
   const int NT = (int)((a.ni + LW - 1) / LW);
   const int ntiles = (int)(a.no * NT);
