@@ -191,55 +191,79 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
 }
 
 template <int N> struct PlanC3;
-// T threads per CTA, 2 CTAs per SM (the in-place stages hold S*N/T points per thread)
-template <> struct PlanC3<256> { static constexpr int S = 16, T = 256; template <class Lay> using F = Fft<256, 16, T, Lay, 4, 8, 8>; static constexpr int R1 = 4; };
-template <> struct PlanC3<512> { static constexpr int S = 8, T = 256; template <class Lay> using F = Fft<512, 8, T, Lay, 8, 8, 8>; static constexpr int R1 = 8; };
-template <> struct PlanC3<1024> { static constexpr int S = 4, T = 256; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; static constexpr int R1 = 16; };
+// S sequences (2S lines) per tile, T threads, NBUF tile buffers (2: the next
+// tile's rows load while this one is transformed), MINB CTAs per SM. Measured
+// on c2: one 64 KB buffer of 16 lines (128 B row chunks) at 2 CTAs/SM beats
+// double-buffered 8-line tiles at 3 CTAs/SM (0.71 vs 1.05 ms): the row chunk
+// width matters more than overlapping load and transform inside a CTA.
+template <> struct PlanC3<256> { static constexpr int S = 16, T = 256, NBUF = 1, MINB = 2, R1 = 4; template <class Lay> using F = Fft<256, 16, T, Lay, 4, 8, 8>; };
+template <> struct PlanC3<512> { static constexpr int S = 8, T = 256, NBUF = 1, MINB = 2, R1 = 8; template <class Lay> using F = Fft<512, 8, T, Lay, 8, 8, 8>; };
+template <> struct PlanC3<1024> { static constexpr int S = 4, T = 256, NBUF = 1, MINB = 2, R1 = 16; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
 
 template <int N> constexpr size_t smemC3_bytes() {
-  return sizeof(double2) * (PlanC3<N>::S * N) + sizeof(double) * (N + 2 * (PlanC3<N>::T / 32) * PlanC3<N>::S);
+  using P = PlanC3<N>;
+  return sizeof(double2) * (P::NBUF * P::S * N) + sizeof(double) * (N + 2 * (P::T / 32) * P::S);
 }
 
 template <int N>
-__global__ void __launch_bounds__(PlanC3<N>::T, 2) k_dst_cols3(ArgsB2 a) {
-  constexpr int S = PlanC3<N>::S, T = PlanC3<N>::T, m = N - 1, LW = 2 * S;   // LW lines per tile
+__global__ void __launch_bounds__(PlanC3<N>::T, PlanC3<N>::MINB) k_dst_cols3(ArgsB2 a) {
+  using P = PlanC3<N>;
+  constexpr int S = P::S, T = P::T, m = N - 1, LW = 2 * S;   // LW lines per tile
   constexpr int NW = T / 32;
   constexpr int KK = 32 / S;                 // k values per warp step
   constexpr int KW = (N / 2) / NW;           // k values per warp
   constexpr int STEPS = KW / KK;
+  static_assert(STEPS >= 1 && KW % KK == 0, "post-processing shape");
   using Lay = Interleaved<S>;
   extern __shared__ double2 smem[];
-  double2* buf = smem;
-  double* bufd = reinterpret_cast<double*>(smem);
-  double* sn = reinterpret_cast<double*>(smem + S * N);
+  double* sn = reinterpret_cast<double*>(smem + P::NBUF * S * N);
   double* tot = sn + N;                       // [NW warps][S q][2 lines]
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
   const int NT = (int)((a.ni + LW - 1) / LW);
   const int ntiles = (int)(a.no * NT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = lane % S, kk = lane / S;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  // thread -> fixed line l, rows e = e0, e0 + T/LW, ... (pointer increments only)
+  constexpr int RSTEP = T / LW;
+  const int l = threadIdx.x % LW, e0 = threadIdx.x / LW;
+  const long long gstep_rows = (long long)RSTEP * a.ni;
+  auto tile_off = [&](int tile, int& nval) -> long long {
     const int o = tile / NT, cb = tile - o * NT;
     const long long i0 = (long long)cb * LW;
-    const int nval = (int)min((long long)LW, a.ni - i0);
-    const double* src = a.in + (long long)o * m * a.ni + i0;
-    double* dst = a.out + (long long)o * m * a.ni + i0;
-    __syncthreads();   // previous tile's copy-out done with buf
-    // thread -> fixed line l, rows e = e0, e0 + T/LW, ... (pointer increments only)
-    constexpr int RSTEP = T / LW;
-    const int l = threadIdx.x % LW, e0 = threadIdx.x / LW;
-    const long long gstep_rows = (long long)RSTEP * a.ni;
+    nval = (int)min((long long)LW, a.ni - i0);
+    return (long long)o * m * a.ni + i0;
+  };
+  // x(e, l) -> double (e+1)*LW + l of buffer b, i.e. complex slot (l/2, e+1)
+  auto issue = [&](int tile, int b) {
+    int nval;
+    const long long off = tile_off(tile, nval);
+    double* sdst = reinterpret_cast<double*>(smem + b * S * N) + (e0 + 1) * LW + l;
     if (l < nval) {
-      const double* g = src + (long long)e0 * a.ni + l;
-      double* sdst = bufd + (e0 + 1) * LW + l;
+      const double* g = a.in + off + (long long)e0 * a.ni + l;
       for (int e = e0; e < m; e += RSTEP, g += gstep_rows, sdst += RSTEP * LW) cp_async8(sdst, g);
     } else {
-      double* sdst = bufd + (e0 + 1) * LW + l;
       for (int e = e0; e < m; e += RSTEP, sdst += RSTEP * LW) *sdst = 0.0;
     }
     cp_async_commit();
-    cp_async_wait_all();
+  };
+  int it = 0;
+  if (P::NBUF == 2 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = P::NBUF == 2 ? (it & 1) : 0;
+    if (P::NBUF == 2) {
+      if (tile + (int)gridDim.x < ntiles) {
+        issue(tile + gridDim.x, b ^ 1);    // buffer b^1 was released at the end of the last iteration
+        asm volatile("cp.async.wait_group 1;\n" ::);
+      } else {
+        cp_async_wait_all();
+      }
+    } else {
+      issue(tile, 0);
+      cp_async_wait_all();
+    }
     __syncthreads();
+    double2* buf = smem + b * S * N;
+    double* bufd = reinterpret_cast<double*>(buf);
     auto gen = [&](int qg, int j) -> double2 {
       if (j == 0) return make_double2(0.0, 0.0);
       const double2 p = buf[Lay::addr(qg, j)];       // x_j (lines 2q, 2q+1)
@@ -247,8 +271,8 @@ __global__ void __launch_bounds__(PlanC3<N>::T, 2) k_dst_cols3(ArgsB2 a) {
       const double s = sn[j];
       return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
     };
-    using Ff = typename PlanC3<N>::template F<Lay>;
-    Stage<N, S, T, Lay, PlanC3<N>::R1, 1>::first_inplace(buf, gen);
+    using Ff = typename P::template F<Lay>;
+    Stage<N, S, T, Lay, P::R1, 1>::first_inplace(buf, gen);
     auto sink = [&](int qs, int idx, double2 X) { buf[Lay::addr(qs, idx)] = X; };
     FftTail<Ff>::run(buf, a.tw, sink);
     __syncthreads();
@@ -287,11 +311,14 @@ __global__ void __launch_bounds__(PlanC3<N>::T, 2) k_dst_cols3(ArgsB2 a) {
       buf[Lay::addr(q, 2 * k)] = make_double2(a.scale * ((pa + oa[u]) - ha), a.scale * ((pb + ob[u]) - hb));
     }
     __syncthreads();
+    int nval;
+    const long long off = tile_off(tile, nval);
     if (l < nval) {
-      double* g = dst + (long long)e0 * a.ni + l;
+      double* g = a.out + off + (long long)e0 * a.ni + l;
       const double* s = bufd + e0 * LW + l;
       for (int e = e0; e < m; e += RSTEP, g += gstep_rows, s += RSTEP * LW) *g = *s;
     }
+    __syncthreads();   // buffer b is refilled by the next iteration's prefetch (NBUF = 2) or load
   }
 }
 
