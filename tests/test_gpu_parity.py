@@ -406,3 +406,27 @@ def test_fused_solve_reports_singular_column(n, dim):
     _lib.check(lib.bhcp_read_status(status, 1e-8, ctypes.byref(st), plans.stream_handle()), "bhcp_read_status")
     assert st.code == _lib.BHCP_ERR_SINGULAR_SHIFT
     assert st.bad_column == j0
+
+
+@pytest.mark.parametrize("dim,cells,steps", [(1, 2, 1), (2, 2, 1), (3, 2, 2), (2, 3, 1), (1, 3, 2)])
+def test_smallest_systems_vs_oracle(dim, cells, steps):
+    """One interior point per axis and one or two time steps (n_levels = 2, 3)."""
+    w = workloads.make_small(dim, cells, steps, seed=2)
+    grid = B.build_grid(dim, w.length, cells)
+    tg = B.TimeGrid(w.horizon, steps)
+    for kind in (B.MethodKind.PINT_QBVM, B.MethodKind.PINT_MQBVM):
+        system = B.assemble(kind, 1e-2, grid, tg, w.g_delta)
+        y = B.solve_pint(system).trajectory
+        ref = O.spectral_oracle(kind.value, 1e-2, dim, w.length, cells, w.horizon, steps, w.g_delta)
+        assert y.shape == (steps + 1, (cells - 1) ** dim)
+        assert rel(y, ref) <= O.parity_tolerance(tg.n_levels, system.omega)
+
+
+@pytest.mark.parametrize("dim,cells,steps", [(2, 10, 256), (2, 8, 512), (2, 6, 1024), (3, 5, 256), (2, 512, 512)])
+def test_zero_data_zero_trajectory_fast_kernels(dim, cells, steps):
+    """test_pint.py::test_zero_data_gives_zero_solution on the specialised kernels:
+    exact zeros and no residue error (0 <= tol * max(0, tiny))."""
+    grid = B.build_grid(dim, 1.0, cells)
+    system = B.assemble(B.MethodKind.PINT_MQBVM, 1e-2, grid, B.TimeGrid(0.5, steps), np.zeros(grid.n_interior))
+    res = B.solve_pint(system)
+    assert not res.trajectory_device.any().item()
