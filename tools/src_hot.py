@@ -1,10 +1,14 @@
 """Per-CUDA-source-line hot spots from an ncu report (--import-source on, -lineinfo).
-usage: python tools/src_hot.py <rep> [n]"""
+usage: python tools/src_hot.py <rep> [n] [kernel-regex] [launch-skip]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"],
-                     capture_output=True, text=True).stdout
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass,cuda"]
+if len(sys.argv) > 3:
+    cmd += ["-k", "regex:" + sys.argv[3]]
+if len(sys.argv) > 4:
+    cmd += ["--launch-skip", sys.argv[4], "--launch-count", "1"]
+raw = subprocess.run(cmd, capture_output=True, text=True).stdout
 out, fname, hdr = [], None, None
 for row in csv.reader(io.StringIO(raw)):
     if not row:
