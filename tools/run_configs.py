@@ -1,5 +1,7 @@
 """Time the fused device solve on every BASELINE config and check sampled
-levels against the closed-form oracle (usage: python tools/run_configs.py [c1 c3 ...])."""
+levels against the closed-form oracle; with --cpu also time the reference
+3-step algorithm (oracle port) on a bounded sample of each config on the
+host cores (usage: python tools/run_configs.py [--cpu] [c1 c3 ...])."""
 import json
 import sys
 import time
@@ -13,7 +15,12 @@ import paper_2107_06381_b200 as B
 from oracle import bhcp_oracle as O
 from paper_2107_06381_b200 import workloads
 
-names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+import os
+cpu = "--cpu" in sys.argv
+names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c1", "c2", "c3", "c4", "c5"]
+# sample fractions: every per-unit op of the 3-step solve on this share of rows / columns (about 5-20 s each)
+CPU_FRACTION = {"c1": 1.0, "c2": 0.3, "c3": 0.03, "c4": 0.01, "c5": 0.2}
+CPU_THREADS = os.cpu_count() or 1
 out = {}
 for name in names:
     t0 = time.time()
@@ -54,6 +61,14 @@ for name in names:
             del y, plan
             torch.cuda.empty_cache()
     out[name] = {"dof": w.dof, "gen_s": gen_s, "results": res}
+    if cpu:
+        kind, alpha = w.kinds[0], w.alphas[0]
+        dof_eq, secs = O.solve_pint_sample(kind, alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
+                                           w.g_delta, CPU_FRACTION[name], workers=CPU_THREADS)
+        gpu_best = min(r["ms"] for r in res.values())
+        out[name]["cpu_reference"] = {"DOF_s": dof_eq / secs, "threads": CPU_THREADS, "fraction": CPU_FRACTION[name],
+                                      "seconds": secs, "kind": "port",
+                                      "gpu_speedup": (w.dof / (gpu_best * 1e-3)) / (dof_eq / secs)}
     print(name, json.dumps(out[name]), flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
 Path("gpurun_out/configs.json").write_text(json.dumps(out, indent=1))
