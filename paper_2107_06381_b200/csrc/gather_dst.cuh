@@ -36,10 +36,14 @@ constexpr int kTB = 8;
 // since Re U_k = S_{2k+1} - S_{2k-1} and -Im U_k = S_{2k}. A per-warp pass
 // (one warp per output line) splits U^a/U^b, runs the prefix sum with warp
 // shuffles and writes the row of y directly.
+// INPL: the W tile is staged straight into the (padded) FFT buffer and the
+// first stage runs in place -- no separate staging buffer, no prefetch of the
+// next tile, more CTAs per SM. Otherwise a staging buffer lets the next tile
+// load while this one is transformed.
 template <int N> struct PlanB2;
-template <> struct PlanB2<256> { static constexpr int T = 256, R1 = 4, MINB = 3; template <class Lay> using F = Fft<256, 4, T, Lay, 4, 8, 8>; };
-template <> struct PlanB2<512> { static constexpr int T = 256, R1 = 8, MINB = 3; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };
-template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16, MINB = 1; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };  // 147 KB smem
+template <> struct PlanB2<256> { static constexpr int T = 256, R1 = 4, MINB = 3; static constexpr bool INPL = false; template <class Lay> using F = Fft<256, 4, T, Lay, 4, 8, 8>; };
+template <> struct PlanB2<512> { static constexpr int T = 256, R1 = 8, MINB = 3; static constexpr bool INPL = false; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };  // in place: 0.70 vs 0.61 ms (c2)
+template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16, MINB = 2; static constexpr bool INPL = true; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
 
 struct ArgsB2 {
   const double* in;
@@ -66,13 +70,14 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem_dst, const void* gsrc
 template <int N>
 __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(ArgsB2 a) {
   constexpr int S = 4, T = PlanB2<N>::T, m = N - 1;
+  constexpr bool INPL = PlanB2<N>::INPL;
   constexpr int RUN = m * kTB;
   constexpr int KU = (N / 2) / 32;   // k values per lane (k = u*32 + lane)
   using Lay = Interleaved<S, 2>;   // pad every 2: conflict-free for q-fastest stages and lane-per-k reads
   extern __shared__ double2 smem[];
   double2* buf = smem;
   double* stage = reinterpret_cast<double*>(smem + Lay::words(N));
-  double* sn = stage + RUN + 16;
+  double* sn = INPL ? stage : stage + RUN + 16;
   double* carry = sn + N;           // 8 doubles: lower-half running sums per line
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
   // Tiles are walked with 32-bit incremental counters (o, tt) = (line, level tile).
@@ -89,6 +94,16 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
     return a.in + kb + (long long)tt * a.P1 * kTB + (long long)r2 * m * kTB;
   };
   auto issue = [&](const double* src_d) {
+    if (INPL) {
+      // 16 B chunk i = (element j-1 = i/4, line pair q = i%4) -> slot (q, j)
+      const double2* src = reinterpret_cast<const double2*>(src_d);
+      for (int i = threadIdx.x; i < RUN / 2; i += T) {
+        const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(buf + Lay::addr(i & 3, (i >> 2) + 1)));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + i));
+      }
+      cp_async_commit();
+      return 0;
+    }
     const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(stage));
     const int soff = (int)(((static_cast<unsigned>(reinterpret_cast<uintptr_t>(src_d)) - sbase) & 127u) >> 3);
     const double2* src = reinterpret_cast<const double2*>(src_d);
@@ -104,27 +119,38 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
   int tile = blockIdx.x;
   int o = tile / NT, tt = tile - o * NT;
   int soff = 0;
-  if (tile < ntiles) soff = issue(src_of(o, tt));
+  if (!INPL && tile < ntiles) soff = issue(src_of(o, tt));
   for (; tile < ntiles; tile += gstep) {
     int no = o + step_o, ntt = tt + step_t;
     if (ntt >= NT) { ntt -= NT; ++no; }
+    if (INPL) {
+      __syncthreads();   // the previous tile's post-processing is done with buf
+      issue(src_of(o, tt));
+    }
     cp_async_wait_all();
     __syncthreads();
     const long long tvalid = a.nlev - (long long)tt * kTB;
     const double* st = stage + soff;
     auto gen = [&](int q, int j) -> double2 {
       if (j == 0) return make_double2(0.0, 0.0);
-      double2 p = *reinterpret_cast<const double2*>(st + (j - 1) * kTB + 2 * q);      // x_j
-      double2 r = *reinterpret_cast<const double2*>(st + (N - j - 1) * kTB + 2 * q);  // x_{N-j}
+      double2 p, r;
+      if (INPL) {
+        p = buf[Lay::addr(q, j)];        // x_j
+        r = buf[Lay::addr(q, N - j)];    // x_{N-j}
+      } else {
+        p = *reinterpret_cast<const double2*>(st + (j - 1) * kTB + 2 * q);
+        r = *reinterpret_cast<const double2*>(st + (N - j - 1) * kTB + 2 * q);
+      }
       if (2 * q >= tvalid) { p.x = 0.0; r.x = 0.0; }
       if (2 * q + 1 >= tvalid) { p.y = 0.0; r.y = 0.0; }
       const double s = sn[j];
       return make_double2(fma(s, p.x + r.x, 0.5 * (p.x - r.x)), fma(s, p.y + r.y, 0.5 * (p.y - r.y)));
     };
     using Ff = typename PlanB2<N>::template F<Lay>;
-    Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first(buf, gen);
+    if (INPL) Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first_inplace(buf, gen);
+    else Stage<N, S, T, Lay, PlanB2<N>::R1, 1>::first(buf, gen);
     const int cur_o = o, cur_tt = tt;
-    if (tile + gstep < ntiles) soff = issue(src_of(no, ntt));
+    if (!INPL && tile + gstep < ntiles) soff = issue(src_of(no, ntt));
     o = no; tt = ntt;
     auto sink = [&](int q, int idx, double2 X) { buf[Lay::addr(q, idx)] = X; };
     FftTail<Ff>::run(buf, a.tw, sink);
@@ -324,7 +350,7 @@ __global__ void __launch_bounds__(PlanC3<N>::T, PlanC3<N>::MINB) k_dst_cols3(Arg
 
 template <int N> constexpr size_t smemB2_bytes() {
   using Lay = Interleaved<4, 2>;
-  return sizeof(double2) * Lay::words(N) + sizeof(double) * ((N - 1) * kTB + 16 + N + 8);
+  return sizeof(double2) * Lay::words(N) + sizeof(double) * ((PlanB2<N>::INPL ? 0 : (N - 1) * kTB + 16) + N + 8);
 }
 
 }  // namespace gdst
