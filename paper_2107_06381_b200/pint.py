@@ -122,6 +122,22 @@ class PintPlan:
             events[3].record()
         return y
 
+    def capture(self, g: torch.Tensor, divisor: float, out: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """Capture one fused solve (g -> out, fixed buffers) into a CUDA graph;
+        ``graph.replay()`` then re-runs status reset, ghat, pass A and the level
+        passes with a single launch from the host. The solve runs once eagerly
+        first so every lazily built device table exists before capture."""
+        self.solve_device(g, divisor, out=out)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                self.solve_device(g, divisor, out=out)
+        torch.cuda.current_stream().wait_stream(side)
+        return graph
+
     def status_ptr(self) -> ctypes.c_void_p:
         ws = self.workspace()
         return ctypes.c_void_p(ws.data_ptr())

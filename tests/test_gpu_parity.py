@@ -430,3 +430,28 @@ def test_zero_data_zero_trajectory_fast_kernels(dim, cells, steps):
     system = B.assemble(B.MethodKind.PINT_MQBVM, 1e-2, grid, B.TimeGrid(0.5, steps), np.zeros(grid.n_interior))
     res = B.solve_pint(system)
     assert not res.trajectory_device.any().item()
+
+
+@pytest.mark.parametrize("dim,cells,steps", [(1, 256, 256), (2, 40, 30), (2, 64, 512)])
+def test_graph_replay_matches_eager(dim, cells, steps):
+    """PintPlan.capture: the CUDA-graph replay of the fused solve gives the
+    eager bits, and a new g copied into the captured input buffer is used."""
+    w = workloads.make_small(dim, cells, steps, seed=9)
+    grid = B.build_grid(dim, w.length, cells)
+    tg = B.TimeGrid(w.horizon, steps)
+    system = B.assemble(B.MethodKind.PINT_QBVM, 1e-3, grid, tg, w.g_delta)
+    plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
+    div = system.method.condition_divisor(tg.tau)
+    g = torch.from_numpy(w.g_delta).cuda()
+    y = torch.empty((tg.n_levels, grid.n_interior), dtype=torch.float64, device="cuda")
+    graph = plan.capture(g, div, y)
+    eager = B.solve_pint(system).trajectory
+    y.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    plan.check_status()
+    assert np.array_equal(y.cpu().numpy(), eager)
+    g.copy_(torch.from_numpy(2.0 * w.g_delta))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(y.cpu().numpy(), 2.0 * eager)

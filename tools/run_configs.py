@@ -40,10 +40,13 @@ for name in names:
             torch.cuda.synchronize()
             plan.check_status()
             reps = 3 if w.dof > 1e9 else 10
+            graph = plan.capture(g, div, y)   # timed as CUDA-graph replays of the step
+            graph.replay()
+            torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(reps):
-                plan.solve_device(g, div, out=y)
+                graph.replay()
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / reps
@@ -58,7 +61,7 @@ for name in names:
             eh_ref = workloads.l2_error(ref[0], w.z0, grid.h, w.dim)
             res[f"{kind} alpha={alpha:.3g}"] = {"ms": ms, "GDOF_s": w.dof / ms / 1e6, "rel_l2_sampled_levels": err,
                                                "tol": tol, "ok": bool(err <= tol), "e_h": eh, "e_h_oracle": eh_ref}
-            del y, plan
+            del y, plan, graph
             torch.cuda.empty_cache()
     out[name] = {"dof": w.dof, "gen_s": gen_s, "results": res}
     if cpu:
