@@ -1113,6 +1113,7 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
   a.st = st; a.wl = wl;
   const int L = Pl::L;
   a.bt.tw = tp->blue; a.bt.chirp = tp->blue + L; a.bt.bhat = tp->blue + L + NL; a.bt.wM = tp->blue + 2 * L + NL;
+  a.bt.cg = tp->blue + 2 * L + 2 * NL; a.bt.wg = tp->blue + 2 * L + 3 * NL; a.bt.thr = tp->blue + 2 * L + 4 * NL;
   const size_t sm = blue_smem<NL>();
   const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
   if (sym) {
@@ -1440,6 +1441,27 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
     std::vector<double2> tabs;
     if (!build_blue_tables(n_levels, &tabs, &err)) {
       free_fft_plan(&tp->fft); cudaFree(tp->tables); delete tp; return fail(BHCP_ERR_INVALID, err);
+    }
+    // fused sink / generator tables: cg_t = chirp_t / gamma_t, wg_t = w^{Mt} / gamma_t,
+    // thr_j = 1e-28 |s_j|^2 (space.py:237-240), products rounded once from long double
+    {
+      const int L = 2 * (n_levels - 1);
+      const double2* chirp = tabs.data() + L;
+      const double2* wM = tabs.data() + 2 * L + n_levels;
+      for (int t = 0; t < n_levels; ++t) {
+        const long double gr = gamma_inv_host[2 * t], gi = gamma_inv_host[2 * t + 1];
+        const long double cr = chirp[t].x, ci = chirp[t].y, wr = wM[t].x, wi = wM[t].y;
+        tabs.push_back(make_double2((double)(cr * gr - ci * gi), (double)(cr * gi + ci * gr)));
+      }
+      for (int t = 0; t < n_levels; ++t) {
+        const long double gr = gamma_inv_host[2 * t], gi = gamma_inv_host[2 * t + 1];
+        const long double wr = wM[t].x, wi = wM[t].y;
+        tabs.push_back(make_double2((double)(wr * gr - wi * gi), (double)(wr * gi + wi * gr)));
+      }
+      for (int j = 0; j < n_levels; ++j) {
+        const double sr = shifts_host[2 * j], si = shifts_host[2 * j + 1];
+        tabs.push_back(make_double2(1e-28 * (sr * sr + si * si), 0.0));
+      }
     }
     if (cudaMalloc(&tp->blue, sizeof(double2) * tabs.size()) != cudaSuccess) {
       free_fft_plan(&tp->fft); cudaFree(tp->tables); delete tp; return cuda_fail("cudaMalloc blue tables");

@@ -457,6 +457,9 @@ struct BlueTables {
   const double2* chirp;  // c_j, j < n
   const double2* bhat;   // FFT_L(b) / L
   const double2* wM;     // w^{M t}, t < n
+  const double2* cg;     // chirp_t / gamma_t
+  const double2* wg;     // w^{M t} / gamma_t
+  const double2* thr;    // (1e-28 |s_j|^2, 0)
 };
 
 template <int NL> struct BluePlan;
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
       const double2 s = __ldg(a.shifts + j);
       const double dr = s.x + s_mu[q], di = s.y;
       const double den2 = dr * dr + di * di;
-      if (den2 <= 1e-28 * (s.x * s.x + s.y * s.y)) flag_singular(a.st, j);
+      if (den2 <= __ldg(&a.bt.thr[j].x)) flag_singular(a.st, j);
       const double inv = fast_rcp(den2);
       return cmul(make_double2(dr * inv, -di * inv), __ldg(a.bt.chirp + j));
     };
@@ -577,9 +580,8 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
     // FFT 2 (conjugated inverse): conv_t = conj(X_t); X_t of the DFT = c_t conv_t + v_M w^{Mt}
     auto sink2 = [&](int q, int idx, double2 X) {
       if (idx > M) return;
-      const double2 conv = cconj(X);
-      const double2 Y = cadd(cmul(conv, __ldg(a.bt.chirp + idx)), cmul(s_vM[q], __ldg(a.bt.wM + idx)));
-      buf[Lay::addr(q, idx)] = cmul(Y, __ldg(a.gaminv + idx));
+      // Gamma^-1 X_t = conj(X) chirp_t / gamma_t + v_M w^{Mt} / gamma_t (tables cg, wg)
+      buf[Lay::addr(q, idx)] = cadd(cmul(cconj(X), __ldg(a.bt.cg + idx)), cmul(s_vM[q], __ldg(a.bt.wg + idx)));
     };
     F2::run(buf, a.bt.tw, sink2);
     __syncthreads();
