@@ -95,6 +95,7 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 }  // namespace bhcp
 #include "fast_kernels.cuh"
 #include "gather_dst.cuh"
+#include "gt_modes.cuh"
 namespace bhcp {
 
 template <int V> struct VT;
@@ -729,8 +730,9 @@ struct bhcp_space_plan {
   long long ntiles;
   double2* twN;          // exp(-2 pi i k / N), N = m + 1 (half-length DST kernels)
   double* snN;           // sin(pi j / N)
-  int4* seg_tiles[9];    // symmetric segment tiles of the Bluestein / Rader modes kernels, slot log2(S)
-  long long seg_count[9];
+  int4* seg_tiles[9];    // symmetric segment tiles of the Bluestein / Rader / Good-Thomas modes kernels,
+  long long seg_count[9];   // one slot per segment length seg_len[slot]
+  int seg_len[9];
 };
 
 struct bhcp_time_plan {
@@ -740,6 +742,8 @@ struct bhcp_time_plan {
   double2* blue;         // n = 2^p + 1 fast path: tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1)
   double2* rader;        // prime n = 2^p + 1: tw (n-1) | bhat (n-1)
   int* rader_idx;        //                    perm (n-1) | qidx (n)
+  double2* gt;           // n = 1025: w40 | w25 | bhat40
+  int* gt_idx;           //           perm41 | tq41
 };
 
 namespace {
@@ -817,6 +821,8 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
 
+  allow_smem(fastk::k_modes_gt<false>);
+  allow_smem(fastk::k_modes_gt<true>);
   allow_smem(fastk::k_modes_rader<257, false>);
   allow_smem(fastk::k_modes_rader<257, true>);
   allow_smem(fastk::k_modes_fast<513, false>);
@@ -1051,9 +1057,10 @@ const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
   auto* sp = const_cast<bhcp_space_plan*>(sp_c);
   std::lock_guard<std::mutex> lk(g_tile_mutex);
   int slot = 0;
-  while ((1 << slot) < S) ++slot;
-  if ((1 << slot) != S || slot >= 9) return nullptr;   // S a power of two <= 256
+  while (slot < 9 && sp->seg_tiles[slot] && sp->seg_len[slot] != S) ++slot;
+  if (slot >= 9 || S < 1) return nullptr;
   if (!sp->seg_tiles[slot]) {
+    sp->seg_len[slot] = S;
     std::vector<int4> t;
     const int m = sp->m;
     if (sp->dim == 2) {
@@ -1070,6 +1077,31 @@ const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
   }
   *count = sp->seg_count[slot];
   return sp->seg_tiles[slot];
+}
+
+int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
+             long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s) {
+  using namespace fastk;
+  GtModesArgs a{};
+  a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev; a.ghat = ghat;
+  a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
+  a.st = st; a.wl = wl; a.tab = tp->gt; a.itab = tp->gt_idx;
+  const size_t sm = gt_smem();
+  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  if (sym) {
+    long long cnt = 0;
+    a.tiles = seg_tiles(sp, GtPlan::S, &cnt);
+    if (!a.tiles) return cuda_fail("seg tiles");
+    a.ntiles = cnt;
+    const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_gt<true>, GtPlan::T, sm));
+    k_modes_gt<true><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+  } else {
+    const long long work = (a.k_count + GtPlan::S - 1) / GtPlan::S;
+    const long long grid = std::min<long long>(work, resident_ctas(k_modes_gt<false>, GtPlan::T, sm));
+    k_modes_gt<false><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_gt launch");
+  return BHCP_OK;
 }
 
 template <int NL>
@@ -1142,6 +1174,7 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
   const FftPlanHost& P = tp->fft;
   if (!g_disable_fast && tp->rader && tp->n == 257)
     return rader_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+  if (!g_disable_fast && tp->gt && tp->n == 1025) return gt_modes(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
   if (!g_disable_fast && tp->blue) {
     switch (tp->n) {
       case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
@@ -1374,7 +1407,7 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
   cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
   sp->tiles_dev = nullptr;
   sp->ntiles = 0;
-  for (int i = 0; i < 9; ++i) { sp->seg_tiles[i] = nullptr; sp->seg_count[i] = 0; }
+  for (int i = 0; i < 9; ++i) { sp->seg_tiles[i] = nullptr; sp->seg_count[i] = 0; sp->seg_len[i] = 0; }
   {
     const int N = num_cells;
     std::vector<double2> tw(N);
@@ -1470,6 +1503,19 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
   }
   tp->rader = nullptr;
   tp->rader_idx = nullptr;
+  tp->gt = nullptr;
+  tp->gt_idx = nullptr;
+  if (n_levels == 1025) {
+    std::vector<double2> gc;
+    std::vector<int> gi;
+    if (!build_gt_tables(&gc, &gi, &err)) { bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err); }
+    if (cudaMalloc(&tp->gt, sizeof(double2) * gc.size()) != cudaSuccess ||
+        cudaMalloc(&tp->gt_idx, sizeof(int) * gi.size()) != cudaSuccess) {
+      bhcp_time_plan_destroy(tp); return cuda_fail("cudaMalloc gt tables");
+    }
+    cudaMemcpy(tp->gt, gc.data(), sizeof(double2) * gc.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(tp->gt_idx, gi.data(), sizeof(int) * gi.size(), cudaMemcpyHostToDevice);
+  }
   if (n_levels == 257) {
     std::vector<double2> rc;
     std::vector<int> ri;
@@ -1495,6 +1541,8 @@ void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
   if (tp->blue) cudaFree(tp->blue);
   if (tp->rader) cudaFree(tp->rader);
   if (tp->rader_idx) cudaFree(tp->rader_idx);
+  if (tp->gt) cudaFree(tp->gt);
+  if (tp->gt_idx) cudaFree(tp->gt_idx);
   delete tp;
 }
 

@@ -249,6 +249,43 @@ bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx
   return true;
 }
 
+bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::string* err) {
+  const int p = 41, NP = 40;
+  auto powmod = [p](long long b, long long e) {
+    long long r = 1;
+    b %= p;
+    while (e) { if (e & 1) r = r * b % p; b = b * b % p; e >>= 1; }
+    return r;
+  };
+  int g = 2;   // smallest primitive root: g^(40/2) != 1 and g^(40/5) != 1
+  while (powmod(g, NP / 2) == 1 || powmod(g, NP / 5) == 1) ++g;
+  const long long ginv = powmod(g, p - 2);
+  cplx->assign(40 + 25 + 40, make_double2(0.0, 0.0));
+  idx->assign(80, 0);
+  for (int k = 0; k < 40; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / 40.0L;
+    (*cplx)[k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  for (int k = 0; k < 25; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / 25.0L;
+    (*cplx)[40 + k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  std::vector<cld> bb(NP);
+  long long gp = 1, gm = 1;
+  for (int q = 0; q < NP; ++q) {
+    (*idx)[q] = (int)gp;        // g^q
+    (*idx)[40 + q] = (int)gm;   // g^-q
+    const long double a = -2.0L * kPi * (long double)gm / (long double)p;
+    bb[q] = cld(cosl(a), sinl(a));   // b_q = w41^(g^-q)
+    gp = gp * g % p;
+    gm = gm * ginv % p;
+  }
+  host_dft(bb);
+  for (int k = 0; k < NP; ++k) (*cplx)[65 + k] = to_d2(bb[k] / (long double)NP);
+  (void)err;
+  return true;
+}
+
 void free_fft_plan(FftPlanHost* p) {
   if (p->mem) cudaFree(p->mem);
   p->mem = nullptr;

@@ -44,6 +44,10 @@ bool build_blue_tables(int n, std::vector<double2>* out, std::string* err);
 // qidx[t] = q with g^-q = t (t >= 1), g the smallest primitive root.
 bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx, std::string* err);
 
+// Good-Thomas / Rader tables for n = 1025 = 25 x 41 (see fastk::k_modes_gt):
+// cplx = w40 (40) | w25 (25) | bhat40 (40); idx = perm (40) g^p mod 41 | tq (40) g^-q mod 41.
+bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::string* err);
+
 // Upload the odd-radix codelet constants to the current device (idempotent).
 bool ensure_device_constants(int device, std::string* err);
 
