@@ -168,6 +168,24 @@ int bhcp_pint_modes_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, cons
                        int64_t k_begin, int64_t k_end, double* const* slab_dst, int nslabs,
                        const int64_t* slab_bounds, void* status, void* stream);
 
+/* Symmetric pass A for the multi-GPU solve. The modes kernels compute one
+ * mode of every mirror pair (k1,k2) / (k2,k1) (2D) or (k1,k2,k3) /
+ * (k2,k1,k3) (3D), whose shifted spectra are bit-identical, from a tile
+ * list. bhcp_pint_sym_tiles returns the list length for (sp, tp), or 0 when
+ * that time length has no symmetric kernel. bhcp_pint_modes_sym_to
+ * computes tiles [tile_begin, tile_end) and stores both modes of each pair
+ * into every level slab s: at slab_dst[s] + slab_koff[s][k1] +
+ * ((t - b[s]) / 8 * P1 + r) * 8 + (t - b[s]) % 8, where slab_koff[s] is the
+ * device int64 block table (length m) of slab s's receiver, as for
+ * bhcp_pint_levels_blocked. P ranks that split the list evenly do half the
+ * FFT work of a k1-slab split, and store straight into the receivers (peer
+ * memory). */
+int64_t bhcp_pint_sym_tiles(const bhcp_space_plan* sp, const bhcp_time_plan* tp);
+int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat,
+                           int64_t tile_begin, int64_t tile_end, double* const* slab_dst,
+                           const int64_t* const* slab_koff, int nslabs,
+                           const int64_t* slab_bounds, void* status, void* stream);
+
 /* The two halves of the fused solve (also used by the slab-decomposed
  * multi-GPU driver).
  * bhcp_pint_ghat: ghat = DST(g) * scale (n_space float64), scale = 1/(divisor*n).

@@ -68,6 +68,8 @@ SIGNATURES = {
     "bhcp_pint_solve_unfused": (_int, [_vp, _vp, _vp, _dbl, _vp, _vp, ctypes.c_size_t, _vp]),
     "bhcp_pint_ghat": (_int, [_vp, _vp, _dbl, _vp, _vp]),
     "bhcp_pint_modes": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _int, _vp, _vp, _vp]),
+    "bhcp_pint_sym_tiles": (_i64, [_vp, _vp]),
+    "bhcp_pint_modes_sym_to": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _int, _vp, _vp, _vp]),
     "bhcp_pint_modes_to": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _int, _vp, _vp, _vp]),
     "bhcp_pint_level_pass": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "bhcp_pint_levels": (_int, [_vp, _vp, _vp, _i64, _vp]),

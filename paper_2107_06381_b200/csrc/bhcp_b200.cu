@@ -1053,6 +1053,14 @@ std::mutex g_tile_mutex;
 // Symmetric work list of the Bluestein modes kernel: 2D tiles (k1, k2a) cover
 // k2 in [k2a, k2a+S) with k2 >= k1; 3D tiles (k1, k2, k3a) with k1 <= k2 cover
 // k3 in [k3a, k3a+S). Each computed mode also writes its (k1 <-> k2) mirror.
+// Optional window [begin, end) of the symmetric tile list of the modes kernel
+// (multi-GPU: each rank computes a share of the upper triangle and stores
+// both mirrors straight into their owners through per-slab block tables).
+struct SymRange {
+  bool on = false;
+  long long begin = 0, end = -1;
+};
+
 const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
   auto* sp = const_cast<bhcp_space_plan*>(sp_c);
   std::lock_guard<std::mutex> lk(g_tile_mutex);
@@ -1079,19 +1087,38 @@ const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
   return sp->seg_tiles[slot];
 }
 
+// apply a tile window to a symmetric work list
+inline void window(const SymRange& sr, const int4*& tiles, long long& cnt) {
+  if (!sr.on) return;
+  const long long e = sr.end < 0 || sr.end > cnt ? cnt : sr.end;
+  const long long b = sr.begin < 0 ? 0 : (sr.begin > e ? e : sr.begin);
+  tiles += b;
+  cnt = e - b;
+}
+inline void window(const SymRange& sr, const int2*& tiles, long long& cnt) {
+  if (!sr.on) return;
+  const long long e = sr.end < 0 || sr.end > cnt ? cnt : sr.end;
+  const long long b = sr.begin < 0 ? 0 : (sr.begin > e ? e : sr.begin);
+  tiles += b;
+  cnt = e - b;
+}
+
 int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
-             long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s) {
+             long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s,
+             const SymRange& sr = SymRange()) {
   using namespace fastk;
   GtModesArgs a{};
   a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev; a.ghat = ghat;
   a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
   a.st = st; a.wl = wl; a.tab = tp->gt; a.itab = tp->gt_idx;
   const size_t sm = gt_smem();
-  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
   if (sym) {
     long long cnt = 0;
     a.tiles = seg_tiles(sp, GtPlan::S, &cnt);
     if (!a.tiles) return cuda_fail("seg tiles");
+    window(sr, a.tiles, cnt);
+    if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
     const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_gt<true>, GtPlan::T, sm));
     k_modes_gt<true><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
@@ -1107,7 +1134,7 @@ int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
 template <int NL>
 int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
                 long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
-                cudaStream_t s) {
+                cudaStream_t s, const SymRange& sr = SymRange()) {
   using namespace fastk;
   using Pl = RaderPlan<NL>;
   RaderModesArgs a{};
@@ -1116,11 +1143,13 @@ int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doubl
   a.st = st; a.wl = wl;
   a.tw = tp->rader; a.bhat = tp->rader + Pl::NP; a.perm = tp->rader_idx; a.qidx = tp->rader_idx + Pl::NP;
   const size_t sm = rader_smem<NL>();
-  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
   if (sym) {
     long long cnt = 0;
     a.tiles = seg_tiles(sp, Pl::S, &cnt);
     if (!a.tiles) return cuda_fail("seg tiles");
+    window(sr, a.tiles, cnt);
+    if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
     const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_rader<NL, true>, Pl::T, sm));
     k_modes_rader<NL, true><<<(unsigned)grid, Pl::T, sm, s>>>(a);
@@ -1136,7 +1165,7 @@ int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doubl
 template <int NL>
 int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
                long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
-               cudaStream_t s) {
+               cudaStream_t s, const SymRange& sr = SymRange()) {
   using namespace fastk;
   using Pl = BluePlan<NL>;
   BlueModesArgs a{};
@@ -1147,11 +1176,13 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
   a.bt.tw = tp->blue; a.bt.chirp = tp->blue + L; a.bt.bhat = tp->blue + L + NL; a.bt.wM = tp->blue + 2 * L + NL;
   a.bt.cg = tp->blue + 2 * L + 2 * NL; a.bt.wg = tp->blue + 2 * L + 3 * NL; a.bt.thr = tp->blue + 2 * L + 4 * NL;
   const size_t sm = blue_smem<NL>();
-  const bool sym = sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx;
+  const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
   if (sym) {
     long long cnt = 0;
     a.tiles = seg_tiles(sp, Pl::S, &cnt);
     if (!a.tiles) return cuda_fail("seg tiles");
+    window(sr, a.tiles, cnt);
+    if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
     const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_blue<NL, true>, Pl::T, sm));
     k_modes_blue<NL, true><<<(unsigned)grid, Pl::T, sm, s>>>(a);
@@ -1166,20 +1197,21 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
 
 int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
                  long long k_begin, long long k_end, double* W, const fastk::WLayout& wl_in, StatusDev* st,
-                 cudaStream_t s) {
+                 cudaStream_t s, const SymRange& sr = SymRange()) {
   fastk::WLayout wl = wl_in;
   if (!wl.sl_base[0]) wl.bind(W);   // local W unless the caller set per-slab destinations
   const long long kc = k_end - k_begin;
   if (kc <= 0) return BHCP_OK;
   const FftPlanHost& P = tp->fft;
   if (!g_disable_fast && tp->rader && tp->n == 257)
-    return rader_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
-  if (!g_disable_fast && tp->gt && tp->n == 1025) return gt_modes(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+    return rader_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
+  if (!g_disable_fast && tp->gt && tp->n == 1025)
+    return gt_modes(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
   if (!g_disable_fast && tp->blue) {
     switch (tp->n) {
-      case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
-      case 1025: return blue_modes<1025>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
-      case 4097: return blue_modes<4097>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s);
+      case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
+      case 1025: return blue_modes<1025>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
+      case 4097: return blue_modes<4097>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
     }
   }
   if (!g_disable_fast && tp->n == 513) {
@@ -1189,12 +1221,17 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
     f.cscale = cscale; f.k_begin = k_begin; f.k_count = kc; f.W = W; f.m = sp->m; f.dim = sp->dim;
     f.tw = P.d.tw; f.st = st; f.wl = wl;
     // symmetric 4x4 tiles need the whole mode range with global column indices
-    const bool sym = sp->dim == 2 && k_begin == 0 && k_end == sp->nx && sp->tiles_dev && wl.nmodes == sp->nx;
+    const bool sym = sp->dim == 2 && sp->tiles_dev &&
+                     (sr.on || (k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx));
     if (sym) {
-      f.tiles = sp->tiles_dev;
-      f.ntiles = sp->ntiles;
-      const long long grid = std::min<long long>(sp->ntiles, resident_ctas(k_modes_fast<513, true>, ModesPlan<513>::T,
-                                                                          modes_smem<513>()));
+      const int2* tl = sp->tiles_dev;
+      long long cnt = sp->ntiles;
+      window(sr, tl, cnt);
+      if (cnt == 0) return BHCP_OK;
+      f.tiles = tl;
+      f.ntiles = cnt;
+      const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_fast<513, true>, ModesPlan<513>::T,
+                                                                   modes_smem<513>()));
       k_modes_fast<513, true><<<(unsigned)grid, ModesPlan<513>::T, modes_smem<513>(), s>>>(f);
     } else {
       const long long work = (kc + ModesPlan<513>::S - 1) / ModesPlan<513>::S;
@@ -1684,6 +1721,52 @@ int bhcp_pint_modes_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, cons
   for (int s = 0; s < nslabs; ++s) wl.sl_base[s] = slab_dst[s];
   return launch_modes(sp, tp, ghat_dev, 1.0, k_begin, k_end, slab_dst[0], wl, (StatusDev*)status_dev,
                       as_stream(stream));
+}
+
+int64_t bhcp_pint_sym_tiles(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
+  if (!sp || !tp || sp->dim < 2 || g_disable_fast) return 0;
+  DeviceGuard g(sp->device);
+  long long cnt = 0;
+  const int4* t = nullptr;
+  if (tp->rader && tp->n == 257) t = seg_tiles(sp, fastk::RaderPlan<257>::S, &cnt);
+  else if (tp->gt && tp->n == 1025) t = seg_tiles(sp, fastk::GtPlan::S, &cnt);
+  else if (tp->blue && tp->n == 4097) t = seg_tiles(sp, fastk::BluePlan<4097>::S, &cnt);
+  else if (tp->blue && tp->n == 257) t = seg_tiles(sp, fastk::BluePlan<257>::S, &cnt);
+  else if (tp->blue && tp->n == 1025) t = seg_tiles(sp, fastk::BluePlan<1025>::S, &cnt);
+  else if (tp->n == 513 && sp->dim == 2 && sp->tiles_dev) return sp->ntiles;
+  return t ? cnt : 0;
+}
+
+int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat_dev,
+                           int64_t tile_begin, int64_t tile_end, double* const* slab_dst,
+                           const int64_t* const* slab_koff, int nslabs, const int64_t* slab_bounds,
+                           void* status_dev, void* stream) {
+  if (!sp || !tp || !ghat_dev || !slab_dst || !slab_koff || !status_dev) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (nslabs < 1 || nslabs > 8) return fail(BHCP_ERR_INVALID, "nslabs must be in [1, 8]");
+  const int64_t total = bhcp_pint_sym_tiles(sp, tp);
+  if (total <= 0) return fail(BHCP_ERR_INVALID, "no symmetric work list for this grid / time length");
+  if (tile_begin < 0 || tile_end < tile_begin || tile_end > total) return fail(BHCP_ERR_INVALID, "bad tile range");
+  for (int s = 0; s < nslabs; ++s)
+    if (!slab_dst[s] || !slab_koff[s]) return fail(BHCP_ERR_INVALID, "null slab destination or table");
+  if (!slab_bounds || slab_bounds[0] != 0 || slab_bounds[nslabs] != tp->n)
+    return fail(BHCP_ERR_INVALID, "slab bounds must cover [0, n_levels)");
+  for (int i = 1; i <= nslabs; ++i) {
+    if (slab_bounds[i] < slab_bounds[i - 1]) return fail(BHCP_ERR_INVALID, "slab bounds not sorted");
+    if (i < nslabs && slab_bounds[i] % fastk::kTBL && slab_bounds[i] != tp->n)
+      return fail(BHCP_ERR_INVALID, "slab bounds must be multiples of 8");
+  }
+  DeviceGuard g(sp->device);
+  fastk::WLayout wl = make_blocked(sp, sp->nx, nslabs, (const long long*)slab_bounds);
+  for (int s = 0; s < nslabs; ++s) {
+    wl.sl_base[s] = slab_dst[s];
+    wl.sl_koff[s] = (const long long*)slab_koff[s];
+  }
+  SymRange sr;
+  sr.on = true;
+  sr.begin = tile_begin;
+  sr.end = tile_end;
+  return launch_modes(sp, tp, ghat_dev, 1.0, 0, sp->nx, slab_dst[0], wl, (StatusDev*)status_dev,
+                      as_stream(stream), sr);
 }
 
 int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev, double* y_dev,

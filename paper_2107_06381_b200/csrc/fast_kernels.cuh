@@ -48,6 +48,7 @@ struct WLayout {
   long long sl_off[8];
   long long sl_nt[8];
   double* sl_base[8];
+  const long long* sl_koff[8];   // optional: k1 row -> offset from sl_base[s] (receiver block tables)
   long long nmodes;
   long long w_ld;
   long long P1;
@@ -57,7 +58,11 @@ struct WLayout {
     while (s + 1 < nsl && t >= sl_c[s + 1]) ++s;
     const long long tl = t - sl_c[s];
     const long long k1 = k / P1, r = k - k1 * P1;
-    return sl_base[s] + ((k1 * sl_nt[s] + tl / kTBL) * P1 + r) * kTBL + (tl % kTBL);
+    return sl_base[s] + row_off(s, k1) + ((tl / kTBL) * P1 + r) * kTBL + (tl % kTBL);
+  }
+  // offset of k1 row's first block in slab s
+  __host__ __device__ __forceinline__ long long row_off(int s, long long k1) const {
+    return sl_koff[s] ? sl_koff[s][k1] : k1 * sl_nt[s] * P1 * kTBL;
   }
   // local W: slab s starts at W + sl_off[s]
   __host__ __device__ __forceinline__ void bind(double* W) {
@@ -389,9 +394,8 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
       const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : N;
       long long pd, pm, step;
       if (wl.mode_major) {
-        const long long nt = wl.sl_nt[sl];
-        pd = ((long long)k1d * nt * wl.P1 + rd) * kTBL;
-        pm = ((long long)k1m * nt * wl.P1 + rm) * kTBL;
+        pd = wl.row_off(sl, k1d) + rd * kTBL;
+        pm = wl.row_off(sl, k1m) + rm * kTBL;
         // t = t0 + lane + 32 i  ->  (tl >> 3) * P1*8 + (tl & 7), t0 a multiple of 8
         const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
         pd += lo; pm += lo;
@@ -597,10 +601,9 @@ __global__ void __launch_bounds__(BluePlan<NL>::T, BluePlan<NL>::MINB) k_modes_b
         const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
         long long pd, pm, step;
         if (wl.mode_major) {
-          const long long nt = wl.sl_nt[sl];
           const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-          pd = ((long long)s_k1d[q] * nt * wl.P1 + s_rd[q]) * kTBL + lo;
-          pm = ((long long)s_k1m[q] * nt * wl.P1 + s_rm[q]) * kTBL + lo;
+          pd = wl.row_off(sl, s_k1d[q]) + s_rd[q] * kTBL + lo;
+          pm = wl.row_off(sl, s_k1m[q]) + s_rm[q] * kTBL + lo;
           step = 4 * wl.P1 * kTBL;
         } else {
           pd = s_rd[q] + (long long)lane * wl.w_ld;
@@ -764,10 +767,9 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
       const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
       long long pd, pm, step;
       if (wl.mode_major) {
-        const long long nt = wl.sl_nt[sl];
         const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-        pd = ((long long)k1d * nt * wl.P1 + rd) * kTBL + lo;
-        pm = ((long long)k1m * nt * wl.P1 + rm) * kTBL + lo;
+        pd = wl.row_off(sl, k1d) + rd * kTBL + lo;
+        pm = wl.row_off(sl, k1m) + rm * kTBL + lo;
         step = 4 * wl.P1 * kTBL;
       } else {
         pd = rd + (long long)lane * wl.w_ld;

@@ -225,10 +225,9 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {   //
       const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
       long long pd, pm, step;
       if (wl.mode_major) {
-        const long long nt = wl.sl_nt[sl];
         const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-        pd = ((long long)k1d * nt * wl.P1 + rd) * kTBL + lo;
-        pm = ((long long)k1m * nt * wl.P1 + rm) * kTBL + lo;
+        pd = wl.row_off(sl, k1d) + rd * kTBL + lo;
+        pm = wl.row_off(sl, k1m) + rm * kTBL + lo;
         step = 4 * wl.P1 * kTBL;
       } else {
         pd = rd + (long long)lane * wl.w_ld;

@@ -142,13 +142,20 @@ def peer_offsets(layout: SlabLayout, rank: int) -> List[int]:
 
 def sharded_solve_peer(ops, transport, layout: SlabLayout, rank: int, events=None):
     """The same solve with pass A storing straight into the receivers' buffers
-    (bhcp_pint_modes_to over NVLink peer memory): no separate all-to-all, the
-    transfer overlaps pass A's compute store by store. Two device barriers:
+    over NVLink peer memory: no separate all-to-all, the transfer overlaps
+    pass A's compute store by store. When the time length has a symmetric
+    pass-A kernel, the ranks split its mirror-pair tile list evenly
+    (bhcp_pint_modes_sym_to: half the FFT work of a k1-slab split, each pair
+    stored into both owners through the receivers' block tables); otherwise
+    each rank runs its k1 slab (bhcp_pint_modes_to). Two device barriers:
     receivers are done with the previous solve's buffer; all stores landed."""
     transport.barrier()
     if events:
         events[0].record()
-    ops.modes_to(layout, rank, transport.dst)
+    if ops.sym_tiles() > 0:
+        ops.modes_sym_to(layout, rank, transport.bases)
+    else:
+        ops.modes_to(layout, rank, transport.dst)
     if events:
         events[1].record()
     transport.barrier()
@@ -182,6 +189,7 @@ class PeerTransport:
         ptrs = list(self.hdl.buffer_ptrs)
         offs = peer_offsets(layout, rank)
         self.dst = (ctypes.c_void_p * layout.world)(*[int(ptrs[q]) + 8 * offs[q] for q in range(layout.world)])
+        self.bases = (ctypes.c_void_p * layout.world)(*[int(p) for p in ptrs[: layout.world]])
         self.recv = self.buf[: int(sum(layout.recv_splits(rank)))]
 
     def barrier(self):
@@ -301,6 +309,31 @@ class DeviceOps:
                                                     ctypes.cast(dst, ctypes.c_void_p), layout.world,
                                                     bounds.ctypes.data_as(ctypes.c_void_p), p.ptr(self.status),
                                                     p.stream_handle()), "modes_to")
+
+    def sym_tiles(self) -> int:
+        """Length of the symmetric pass-A tile list for this plan (0: none)."""
+        if not hasattr(self, "_sym_tiles"):
+            self._sym_tiles = int(self.lib.bhcp_pint_sym_tiles(self.plan.sp.handle, self.plan.tp.handle))
+        return self._sym_tiles
+
+    def sym_range(self, rank: int, world: int):
+        total = self.sym_tiles()
+        return total * rank // world, total * (rank + 1) // world
+
+    def modes_sym_to(self, layout: SlabLayout, rank: int, bases):
+        """Symmetric pass A over this rank's share of the tile list, both
+        mirrors stored into every receiver q at bases[q] + block_tables(q)."""
+        p = self.plans
+        tb, te = self.sym_range(rank, layout.world)
+        koffs = [self.tables(layout, q) for q in range(layout.world)]
+        karr = (ctypes.c_void_p * layout.world)(*[k.data_ptr() for k in koffs])
+        bounds = layout.slab_bounds()
+        self.prepare()
+        self._lib.check(self.lib.bhcp_pint_modes_sym_to(self.plan.sp.handle, self.plan.tp.handle, p.ptr(self.ghat),
+                                                        tb, te, ctypes.cast(bases, ctypes.c_void_p),
+                                                        ctypes.cast(karr, ctypes.c_void_p), layout.world,
+                                                        bounds.ctypes.data_as(ctypes.c_void_p), p.ptr(self.status),
+                                                        p.stream_handle()), "modes_sym_to")
 
     def tables(self, layout: SlabLayout, rank: int):
         key = (layout.world, rank)

@@ -186,6 +186,33 @@ def emulate_peer(system, world):
     return torch.cat(ys).cpu().numpy()
 
 
+def emulate_peer_sym(system, world):
+    """Symmetric pass A split over emulated ranks (bhcp_pint_modes_sym_to):
+    every rank computes a share of the mirror-pair tiles and stores both modes
+    into all receivers through their block tables."""
+    import ctypes
+
+    import torch
+
+    import paper_2107_06381_b200 as B
+    from paper_2107_06381_b200 import plans
+
+    grid, tg = system.grid, system.timegrid
+    layout = D.SlabLayout(grid.dim, grid.num_cells - 1, tg.n_levels, world)
+    plan = B.PintPlan(grid, tg.n_levels, tg.tau, system.omega)
+    ops = D.DeviceOps(plan, plans.to_device(system.data, torch.float64),
+                      system.method.condition_divisor(tg.tau))
+    if ops.sym_tiles() == 0:
+        return None
+    recv = [torch.full((max(1, sum(layout.recv_splits(q))),), float("nan"), dtype=torch.float64, device="cuda")
+            for q in range(world)]
+    bases = (ctypes.c_void_p * world)(*[recv[q].data_ptr() for q in range(world)])
+    for p in range(world):
+        ops.modes_sym_to(layout, p, bases)
+    ys = [ops.levels_blocked(recv[q], ops.tables(layout, q), layout.levels(q)).clone() for q in range(world)]
+    return torch.cat(ys).cpu().numpy()
+
+
 def emulate(system, world):
     import torch
 
@@ -213,6 +240,7 @@ def emulate(system, world):
 @pytest.mark.gpu
 @pytest.mark.parametrize("dim,cells,steps,world", [(2, 16, 12, 2), (2, 20, 9, 3), (3, 8, 6, 2), (3, 9, 7, 4),
                                                    (2, 12, 256, 2), (3, 7, 256, 3), (2, 10, 1024, 2),
+                                                   (2, 20, 512, 3), (2, 6, 4096, 2), (3, 6, 1024, 2),
                                                    (2, 512, 512, 8)])
 def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
     import paper_2107_06381_b200 as B
@@ -225,3 +253,6 @@ def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
     multi = emulate(system, world)
     assert np.array_equal(single, multi)
     assert np.array_equal(single, emulate_peer(system, world))
+    sym = emulate_peer_sym(system, world)
+    if sym is not None:
+        assert np.array_equal(single, sym)
