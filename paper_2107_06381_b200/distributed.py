@@ -505,8 +505,9 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
         "data": "synthetic (seeded, BASELINE.json config construction)",
         "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, slab-decomposed over {world} GPUs",
                    "dof_per_solve": w.dof, "transport": transport,
-                   "parallelism": (f"mode slabs -> pass A stores into the level-slab owners over NVLink peer memory "
-                                   f"-> level slabs, P={world}") if peer is not None else
+                   "parallelism": (f"pass A over 1/P of the mirror-pair tiles (or a k1 slab) storing into the "
+                                   f"level-slab owners over NVLink peer memory -> level slabs, P={world}")
+                                  if peer is not None else
                                   f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
                    "l2": "working set larger than L2; no flush"},
         "roofline": {"bound": "hbm", "kernel": ["pass A (k_modes_fast)", "", "pass B (level passes)"][dom],
