@@ -224,7 +224,7 @@ template <int N> struct PlanC3;
 // width matters more than overlapping load and transform inside a CTA.
 template <> struct PlanC3<256> { static constexpr int S = 16, T = 256, NBUF = 1, MINB = 2, R1 = 4; template <class Lay> using F = Fft<256, 16, T, Lay, 4, 8, 8>; };
 template <> struct PlanC3<512> { static constexpr int S = 8, T = 256, NBUF = 1, MINB = 2, R1 = 8; template <class Lay> using F = Fft<512, 8, T, Lay, 8, 8, 8>; };
-template <> struct PlanC3<1024> { static constexpr int S = 4, T = 256, NBUF = 1, MINB = 2, R1 = 16; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
+template <> struct PlanC3<1024> { static constexpr int S = 8, T = 512, NBUF = 1, MINB = 1, R1 = 16; template <class Lay> using F = Fft<1024, 8, T, Lay, 16, 8, 8>; };
 
 template <int N> constexpr size_t smemC3_bytes() {
   using P = PlanC3<N>;
