@@ -96,6 +96,7 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 #include "fast_kernels.cuh"
 #include "gather_dst.cuh"
 #include "gt_modes.cuh"
+#include "pf_modes.cuh"
 namespace bhcp {
 
 template <int V> struct VT;
@@ -744,6 +745,9 @@ struct bhcp_time_plan {
   int* rader_idx;        //                    perm (n-1) | qidx (n)
   double2* gt;           // n = 1025: w40 | w25 | bhat40
   int* gt_idx;           //           perm41 | tq41
+  double2* pf;           // n = 4097: w240 | bhat240 | shifts in prime-factor order (4097)
+  double* pf_thr;        //           singular thresholds, prime-factor order (4097)
+  int* pf_idx;           //           tq241 (240) | time index j per (row, slot) (4097)
 };
 
 namespace {
@@ -821,6 +825,8 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
 
+  allow_smem(fastk::k_modes_pf<false>);
+  allow_smem(fastk::k_modes_pf<true>);
   allow_smem(fastk::k_modes_gt<false>);
   allow_smem(fastk::k_modes_gt<true>);
   allow_smem(fastk::k_modes_rader<257, false>);
@@ -1131,6 +1137,33 @@ int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
   return BHCP_OK;
 }
 
+int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
+             long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s,
+             const SymRange& sr = SymRange()) {
+  using namespace fastk;
+  PfModesArgs a{};
+  a.shg = tp->pf + 2 * kPfNp; a.thrg = tp->pf_thr; a.jg = tp->pf_idx + kPfNp; a.gaminv = tp->tables + tp->n;
+  a.mu1 = sp->mu1_dev; a.ghat = ghat; a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin;
+  a.m = sp->m; a.dim = sp->dim; a.st = st; a.tab = tp->pf; a.tq = tp->pf_idx; a.wl = wl;
+  const size_t sm = pf_smem();
+  const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
+  if (sym) {
+    long long cnt = 0;
+    a.tiles = seg_tiles(sp, 1, &cnt);
+    if (!a.tiles) return cuda_fail("seg tiles");
+    window(sr, a.tiles, cnt);
+    if (cnt == 0) return BHCP_OK;
+    a.ntiles = cnt;
+    const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_pf<true>, PfPlan::T, sm));
+    k_modes_pf<true><<<(unsigned)grid, PfPlan::T, sm, s>>>(a);
+  } else {
+    const long long grid = std::min<long long>(a.k_count, resident_ctas(k_modes_pf<false>, PfPlan::T, sm));
+    k_modes_pf<false><<<(unsigned)grid, PfPlan::T, sm, s>>>(a);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_pf launch");
+  return BHCP_OK;
+}
+
 template <int NL>
 int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
                 long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st,
@@ -1207,6 +1240,8 @@ int launch_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doub
     return rader_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
   if (!g_disable_fast && tp->gt && tp->n == 1025)
     return gt_modes(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
+  if (!g_disable_fast && tp->pf && tp->n == 4097)
+    return pf_modes(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
   if (!g_disable_fast && tp->blue) {
     switch (tp->n) {
       case 257: return blue_modes<257>(sp, tp, ghat, cscale, k_begin, k_end, W, wl, st, s, sr);
@@ -1542,6 +1577,34 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
   tp->rader_idx = nullptr;
   tp->gt = nullptr;
   tp->gt_idx = nullptr;
+  tp->pf = nullptr;
+  tp->pf_thr = nullptr;
+  tp->pf_idx = nullptr;
+  if (n_levels == 4097) {
+    std::vector<double2> pc;
+    std::vector<int> tq, perm;
+    if (!build_pf_tables(&pc, &tq, &perm, &err)) { bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err); }
+    std::vector<double> thr(4097);
+    std::vector<int> idx(tq);
+    idx.resize(240 + 4097);
+    for (int i = 0; i < 4097; ++i) {
+      const int row = i / 241, slot = i - row * 241;
+      const int j2 = slot ? perm[slot - 1] : 0;
+      const int j = (241 * row + 17 * j2) % 4097;
+      const double sr = shifts_host[2 * j], si = shifts_host[2 * j + 1];
+      pc.push_back(make_double2(sr, si));
+      thr[i] = 1e-28 * (sr * sr + si * si);
+      idx[240 + i] = j;
+    }
+    if (cudaMalloc(&tp->pf, sizeof(double2) * pc.size()) != cudaSuccess ||
+        cudaMalloc(&tp->pf_thr, sizeof(double) * thr.size()) != cudaSuccess ||
+        cudaMalloc(&tp->pf_idx, sizeof(int) * idx.size()) != cudaSuccess) {
+      bhcp_time_plan_destroy(tp); return cuda_fail("cudaMalloc pf tables");
+    }
+    cudaMemcpy(tp->pf, pc.data(), sizeof(double2) * pc.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(tp->pf_thr, thr.data(), sizeof(double) * thr.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(tp->pf_idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice);
+  }
   if (n_levels == 1025) {
     std::vector<double2> gc;
     std::vector<int> gi;
@@ -1580,6 +1643,9 @@ void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
   if (tp->rader_idx) cudaFree(tp->rader_idx);
   if (tp->gt) cudaFree(tp->gt);
   if (tp->gt_idx) cudaFree(tp->gt_idx);
+  if (tp->pf) cudaFree(tp->pf);
+  if (tp->pf_thr) cudaFree(tp->pf_thr);
+  if (tp->pf_idx) cudaFree(tp->pf_idx);
   delete tp;
 }
 
@@ -1730,6 +1796,7 @@ int64_t bhcp_pint_sym_tiles(const bhcp_space_plan* sp, const bhcp_time_plan* tp)
   const int4* t = nullptr;
   if (tp->rader && tp->n == 257) t = seg_tiles(sp, fastk::RaderPlan<257>::S, &cnt);
   else if (tp->gt && tp->n == 1025) t = seg_tiles(sp, fastk::GtPlan::S, &cnt);
+  else if (tp->pf && tp->n == 4097) t = seg_tiles(sp, 1, &cnt);
   else if (tp->blue && tp->n == 4097) t = seg_tiles(sp, fastk::BluePlan<4097>::S, &cnt);
   else if (tp->blue && tp->n == 257) t = seg_tiles(sp, fastk::BluePlan<257>::S, &cnt);
   else if (tp->blue && tp->n == 1025) t = seg_tiles(sp, fastk::BluePlan<1025>::S, &cnt);

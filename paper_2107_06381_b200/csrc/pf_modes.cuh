@@ -1,0 +1,257 @@
+// pf_modes.cuh -- pass A for n = 4097 time levels (BASELINE config 5) by the
+// prime-factor algorithm, 4097 = 17 x 241, with Rader's algorithm for the
+// 241-point transforms. Included by bhcp_b200.cu after gt_modes.cuh.
+//
+// Same construction as k_modes_gt (n = 1025 = 25 x 41), one CTA per mode:
+//   j = (241 j1 + 17 j2) mod 4097, t1 = t mod 17, t2 = t mod 241,
+//   X_t = sum_{j1} w17^{j1 t1} sum_{j2} w241^{j2 t2} v(j1, j2);
+//   241-point DFTs along rows by Rader (g a primitive root of 241):
+//     Y_0 = y_0 + A_0, Y_{g^-q} = y_0 + conj(FFT240(conj(A * bhat)))_q, A = FFT240(a),
+//     a_p = y_{g^p}, FFT240 = radix 4 x 4 x 5 x 3;
+//   17-point DFTs down the 241 columns (direct odd codelet).
+// About 0.55x the FLOPs of the 8192-point Bluestein pair; 65.5 KB of shared
+// memory per mode, so three CTAs share an SM. Every stage runs in place: a
+// thread loads all of its butterflies, the CTA synchronises, then it stores.
+#pragma once
+
+namespace bhcp {
+namespace fastk {
+
+constexpr int kPfRows = 17, kPfLen = 241, kPfN = kPfRows * kPfLen, kPfNp = 240;
+
+struct PfModesArgs {
+  const double2* shg;   // shifts in prime-factor input order (row j1, slot)
+  const double* thrg;   // singular thresholds 1e-28 |s|^2, same order
+  const int* jg;        // time index j of each (row, slot)
+  const double2* gaminv;
+  const double* mu1;
+  const double* ghat;
+  double cscale;
+  long long k_begin, k_count;
+  int m, dim;
+  StatusDev* st;
+  const double2* tab;   // w240 (240) | bhat240 (240)
+  const int* tq;        // g^-q mod 241 (240)
+  WLayout wl;
+  const int4* tiles;    // SYM: seg tiles with S = 1
+  long long ntiles;
+};
+
+struct PfPlan { static constexpr int T = 256, MINB = 2; };   // the 17-point column codelet needs ~140 registers
+
+// One in-place Stockham stage of radix R over slots 1..240 of all 17 rows:
+// butterfly (row, b), b < 240/R, reads slots 1 + b + (240/R) r, twiddles
+// w240^{TWS k r} (k = b % Ns), writes slots 1 + (b - k) R + k + Ns r. Rounds
+// of whole rows (one butterfly per thread): a round's loads finish (CTA
+// barrier) before its stores, and different rounds touch different rows.
+template <int R, int Ns, class Store>
+__device__ __forceinline__ void pf_row_stage(double2* buf, const double2* __restrict__ w240, Store&& store) {
+  constexpr int NB = kPfNp / R, T = PfPlan::T, RPR = T / NB;
+  constexpr int TWS = kPfNp / (Ns * R);
+  static_assert(RPR >= 1, "one row per round at least");
+  const int lr = threadIdx.x / NB, b = threadIdx.x - lr * NB;
+  const int k = b % Ns;
+  double2 tw[R];
+  if (Ns > 1) {
+#pragma unroll
+    for (int r = 1; r < R; ++r) tw[r] = w240[(TWS * k * r) % kPfNp];
+  }
+#pragma unroll 1
+  for (int r0 = 0; r0 < kPfRows; r0 += RPR) {
+    const int row = r0 + lr;
+    const bool act = lr < RPR && row < kPfRows;
+    double2 v[R];
+    double2* rowp = buf + row * kPfLen + 1;
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = rowp[b + NB * r];
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r]);
+      }
+      sfft::Cod<R>::run(v);
+    }
+    __syncthreads();
+    if (act) {
+      const int base = (b - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) store(rowp, base + Ns * r, v[r]);
+    }
+  }
+  __syncthreads();
+}
+
+template <bool SYM>
+__global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArgs a) {
+  constexpr int NL = kPfN, T = PfPlan::T;
+  extern __shared__ double2 smem[];
+  __shared__ double2 s_w[kPfNp], s_bh[kPfNp];
+  __shared__ short s_tq[kPfNp];
+  __shared__ double2 s_x0[kPfRows];
+  __shared__ double red[2 * (T / 32)];
+  for (int i = threadIdx.x; i < kPfNp; i += T) {
+    s_w[i] = __ldg(a.tab + i);
+    s_bh[i] = __ldg(a.tab + kPfNp + i);
+    s_tq[i] = (short)__ldg(a.tq + i);
+  }
+  double2* buf = smem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  StatusDev* st = a.st;
+  const WLayout& wl = a.wl;
+  double sre = 0.0, sim = 0.0;
+  const long long ntiles = SYM ? a.ntiles : a.k_count;
+  __syncthreads();
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    bool valid, hm = false;
+    long long kd, km = 0;
+    int k1d = 0, k1m = 0;
+    long long rd = 0, rm = 0;
+    if (SYM) {
+      const int4 tb = __ldg(a.tiles + tile);
+      if (a.dim == 2) {
+        const int k1 = tb.x, k2 = tb.y;
+        valid = k2 < a.m && k2 >= k1;
+        kd = (long long)k1 * a.m + k2;
+        hm = valid && k2 != k1;
+        km = (long long)k2 * a.m + k1;
+        k1d = k1; rd = k2; k1m = k2; rm = k1;
+      } else {
+        const int k1 = tb.x, k2 = tb.y, k3 = tb.z;
+        valid = k3 < a.m;
+        kd = ((long long)k1 * a.m + k2) * a.m + k3;
+        hm = valid && k1 != k2;
+        km = ((long long)k2 * a.m + k1) * a.m + k3;
+        k1d = k1; rd = (long long)k2 * a.m + k3; k1m = k2; rm = (long long)k1 * a.m + k3;
+      }
+      if (!valid) kd = 0;
+    } else {
+      valid = true;
+      kd = a.k_begin + tile;
+      if (wl.mode_major) { k1d = (int)(tile / wl.P1); rd = tile - (long long)k1d * wl.P1; }
+      else rd = tile;
+    }
+    if (!valid) continue;   // uniform across the CTA
+    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    const double c = __ldg(a.ghat + kd) * a.cscale;
+    const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
+    // 1. generator in prime-factor order (slot 0: j2 = 0; slot 1 + p: j2 = g^p)
+    for (int i = threadIdx.x; i < NL; i += T) {
+      const double2 s = __ldg(a.shg + i);
+      const double dr = s.x + mu, di = s.y;
+      const double den2 = dr * dr + di * di;
+      if (den2 <= __ldg(a.thrg + i)) flag_singular(st, __ldg(a.jg + i));
+      const double inv = fast_rcp(den2);
+      buf[i] = make_double2(dr * inv, -di * inv);
+    }
+    __syncthreads();
+    // 2. A = FFT240(a) per row
+    auto natural = [](double2* rowp, int q, double2 x) { rowp[q] = x; };
+    pf_row_stage<4, 1>(buf, s_w, natural);
+    pf_row_stage<4, 4>(buf, s_w, natural);
+    pf_row_stage<5, 16>(buf, s_w, natural);
+    pf_row_stage<3, 80>(buf, s_w, natural);
+    // 3. Y(row, 0) = y0 + A_0 kept aside; slots <- conj(A_k * bhat_k)
+    for (int i = threadIdx.x; i < kPfRows * kPfNp; i += T) {
+      const int row = i / kPfNp, k = i - row * kPfNp;
+      double2* p = buf + row * kPfLen + 1 + k;
+      const double2 A = *p;
+      if (k == 0) s_x0[row] = cadd(buf[row * kPfLen], A);
+      *p = cconj(cmul(A, s_bh[k]));
+    }
+    __syncthreads();
+    // 4. FFT240 again; the last stage stores y0 + conj(out_q) at slot t2 = g^-q
+    pf_row_stage<4, 1>(buf, s_w, natural);
+    pf_row_stage<4, 4>(buf, s_w, natural);
+    pf_row_stage<5, 16>(buf, s_w, natural);
+    {
+      // last stage: all loads of the CTA complete before the permuted stores
+      pf_row_stage<3, 80>(buf, s_w, [&](double2* rowp, int q, double2 x) { rowp[s_tq[q] - 1] = cadd(rowp[-1], cconj(x)); });
+    }
+    if (threadIdx.x < kPfRows) buf[threadIdx.x * kPfLen] = s_x0[threadIdx.x];
+    __syncthreads();
+    // 5. 17-point DFT down each of the 241 columns (one per thread), the
+    //    symmetric odd-prime codelet with outputs stored as they are formed
+    //    (only the 8 pair sums / differences stay in registers)
+    {
+      const int col = threadIdx.x;
+      if (col < kPfLen) {
+        constexpr int R = kPfRows, H = (R - 1) / 2, off = odd_root_offset(R);
+        double2* colp = buf + col;
+        const double2 x0 = colp[0];
+        double2 sa[H], sb[H];
+        double2 sum = x0;
+#pragma unroll
+        for (int j = 1; j <= H; ++j) {
+          const double2 p = colp[j * kPfLen], q = colp[(R - j) * kPfLen];
+          sa[j - 1] = cadd(p, q);
+          sb[j - 1] = csub(p, q);
+          sum = cadd(sum, sa[j - 1]);
+        }
+        colp[0] = sum;
+#pragma unroll
+        for (int k = 1; k <= H; ++k) {
+          double2 A = x0, B = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int j = 1; j <= H; ++j) {
+            const int qq = (j * k) % R;
+            const double cs = c_root_cos[off + qq], sn = c_root_sin[off + qq];
+            A.x = fma(sa[j - 1].x, cs, A.x);
+            A.y = fma(sa[j - 1].y, cs, A.y);
+            B.x = fma(sb[j - 1].x, sn, B.x);
+            B.y = fma(sb[j - 1].y, sn, B.y);
+          }
+          colp[k * kPfLen] = make_double2(A.x + B.y, A.y - B.x);
+          colp[(R - k) * kPfLen] = make_double2(A.x - B.y, A.y + B.x);
+        }
+      }
+    }
+    __syncthreads();
+    // 6. store: X_t at (t mod 17, t mod 241); W = c Re(Gamma^-1 X), residue norms
+    const int nsl = wl.mode_major ? wl.nsl : 1;
+    double zr2 = 0.0, zi2 = 0.0;
+    for (int sl = 0; sl < nsl; ++sl) {
+      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
+      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
+      // thread -> t = t0 + threadIdx.x + T i: (t / 8) blocks at stride P1*8
+      long long pd, pm, step;
+      if (wl.mode_major) {
+        const long long lo = (long long)(threadIdx.x >> 3) * wl.P1 * kTBL + (threadIdx.x & 7);
+        pd = wl.row_off(sl, k1d) + rd * kTBL + lo;
+        pm = wl.row_off(sl, k1m) + rm * kTBL + lo;
+        step = (T / kTBL) * wl.P1 * kTBL;
+      } else {
+        pd = rd + (long long)threadIdx.x * wl.w_ld;
+        pm = pd;
+        step = (long long)T * wl.w_ld;
+      }
+      double* __restrict__ wd = wl.sl_base[sl] + pd;
+      double* __restrict__ wmr = wl.sl_base[sl] + pm;
+      for (int t = t0 + threadIdx.x; t < t1; t += T, wd += step, wmr += step) {
+        const double2 X = buf[(t % kPfRows) * kPfLen + (t % kPfLen)];
+        const double2 g = __ldg(a.gaminv + t);
+        const double zr = X.x * g.x - X.y * g.y;
+        const double zi = X.x * g.y + X.y * g.x;
+        zr2 = fma(zr, zr, zr2);
+        zi2 = fma(zi, zi, zi2);
+        *wd = c * zr;
+        if (hm) *wmr = c2 * zr;
+      }
+    }
+    const double cc = c * c + c2 * c2;
+    sre = fma(cc, zr2, sre);
+    sim = fma(cc, zi2, sim);
+    __syncthreads();   // buf is rewritten by the next mode
+  }
+  (void)warp;
+  (void)lane;
+  block_sum2(sre, sim, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.st->sum_re2, sre);
+    atomicAdd(&a.st->sum_im2, sim);
+  }
+}
+
+constexpr size_t pf_smem() { return sizeof(double2) * kPfN; }
+
+}  // namespace fastk
+}  // namespace bhcp

@@ -286,6 +286,40 @@ bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::str
   return true;
 }
 
+bool build_pf_tables(std::vector<double2>* cplx, std::vector<int>* tq, std::vector<int>* perm, std::string* err) {
+  const int p = 241, NP = 240;
+  auto powmod = [p](long long b, long long e) {
+    long long r = 1;
+    b %= p;
+    while (e) { if (e & 1) r = r * b % p; b = b * b % p; e >>= 1; }
+    return r;
+  };
+  int g = 2;   // smallest primitive root: g^(240/q) != 1 for q = 2, 3, 5
+  while (powmod(g, NP / 2) == 1 || powmod(g, NP / 3) == 1 || powmod(g, NP / 5) == 1) ++g;
+  const long long ginv = powmod(g, p - 2);
+  cplx->assign(2 * NP, make_double2(0.0, 0.0));
+  tq->assign(NP, 0);
+  perm->assign(NP, 0);
+  for (int k = 0; k < NP; ++k) {
+    const long double a = -2.0L * kPi * (long double)k / (long double)NP;
+    (*cplx)[k] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  std::vector<cld> bb(NP);
+  long long gp = 1, gm = 1;
+  for (int q = 0; q < NP; ++q) {
+    (*perm)[q] = (int)gp;
+    (*tq)[q] = (int)gm;
+    const long double a = -2.0L * kPi * (long double)gm / (long double)p;
+    bb[q] = cld(cosl(a), sinl(a));   // b_q = w241^(g^-q)
+    gp = gp * g % p;
+    gm = gm * ginv % p;
+  }
+  host_dft(bb);
+  for (int k = 0; k < NP; ++k) (*cplx)[NP + k] = to_d2(bb[k] / (long double)NP);
+  (void)err;
+  return true;
+}
+
 void free_fft_plan(FftPlanHost* p) {
   if (p->mem) cudaFree(p->mem);
   p->mem = nullptr;

@@ -48,6 +48,10 @@ bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx
 // cplx = w40 (40) | w25 (25) | bhat40 (40); idx = perm (40) g^p mod 41 | tq (40) g^-q mod 41.
 bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::string* err);
 
+// Prime-factor / Rader tables for n = 4097 = 17 x 241 (see fastk::k_modes_pf):
+// cplx = w240 (240) | bhat240 (240); tq (240) = g^-q mod 241; perm (240) = g^p mod 241.
+bool build_pf_tables(std::vector<double2>* cplx, std::vector<int>* tq, std::vector<int>* perm, std::string* err);
+
 // Upload the odd-radix codelet constants to the current device (idempotent).
 bool ensure_device_constants(int device, std::string* err);
 

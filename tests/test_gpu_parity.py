@@ -372,7 +372,7 @@ def test_full_size_solve_vs_device_oracle(name):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("n", [9, 257, 513, 1025])
+@pytest.mark.parametrize("n", [9, 257, 513, 1025, 4097])
 @pytest.mark.parametrize("dim", [1, 2, 3])
 def test_fused_solve_reports_singular_column(n, dim):
     """A shift s_j = -mu_k makes (s_j - lap) singular (space.py:237-240): every
