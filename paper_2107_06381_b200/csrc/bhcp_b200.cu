@@ -1507,6 +1507,10 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
     }
     cudaMemcpy(sp->tiles_dev, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice);
   }
+  if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {   // a failed table upload
+    bhcp_space_plan_destroy(sp);
+    return fail(BHCP_ERR_CUDA, std::string("space plan upload: ") + cudaGetErrorString(e));
+  }
   *out = sp;
   return BHCP_OK;
 }
@@ -1628,6 +1632,10 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
     }
     cudaMemcpy(tp->rader, rc.data(), sizeof(double2) * rc.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(tp->rader_idx, ri.data(), sizeof(int) * ri.size(), cudaMemcpyHostToDevice);
+  }
+  if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {   // a failed table upload
+    bhcp_time_plan_destroy(tp);
+    return fail(BHCP_ERR_CUDA, std::string("time plan upload: ") + cudaGetErrorString(e));
   }
   *out = tp;
   return BHCP_OK;
