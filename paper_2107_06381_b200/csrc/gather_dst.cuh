@@ -20,6 +20,24 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+// 1D bulk copy global -> shared on the TMA unit, completion tracked by an mbarrier
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile("{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
 // Levels per contiguous W block (fastk::kTBL).
@@ -79,15 +97,22 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
   double* stage = reinterpret_cast<double*>(smem + Lay::words(N));
   double* sn = INPL ? stage : stage + RUN + 16;
   double* carry = sn + N;           // 8 doubles: lower-half running sums per line
+  __shared__ alignas(8) unsigned long long tile_bar;   // TMA bulk-copy completion of the staged tile
   for (int j = threadIdx.x; j < N; j += T) sn[j] = __ldg(a.sn + j);
+  if (!INPL && threadIdx.x == 0) {
+    mbar_init(&tile_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   // Tiles are walked with 32-bit incremental counters (o, tt) = (line, level tile).
   const int NT = (int)a.NT;
   const int idiv = (int)a.idiv;
   const int ntiles = (int)(a.P * a.NT);
   const int gstep = gridDim.x, step_o = gstep / NT, step_t = gstep - step_o * NT;
-  // The stage copy is shifted so that smem and global addresses agree mod
-  // 128 B (a misaligned cp.async splits every 128 B line into two smem
-  // wavefronts).
+  // Staged path: one thread hands the tile (a contiguous 8m-double run) to
+  // the TMA unit as a single bulk copy (cp.async.bulk, completion on an
+  // mbarrier); the next tile is issued once the first FFT stage has read the
+  // current one. In-place path: 16 B cp.async chunks into the padded slots.
   auto src_of = [&](int o, int tt) -> const double* {
     const int k1 = o / idiv, r2 = o - k1 * idiv;
     const long long kb = a.koff ? __ldg(a.koff + k1) : (long long)k1 * a.NT * a.P1 * kTB;
@@ -104,21 +129,15 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
       cp_async_commit();
       return 0;
     }
-    const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(stage));
-    const int soff = (int)(((static_cast<unsigned>(reinterpret_cast<uintptr_t>(src_d)) - sbase) & 127u) >> 3);
-    const double2* src = reinterpret_cast<const double2*>(src_d);
-    double2* dst = reinterpret_cast<double2*>(stage + soff);
-    for (int i = threadIdx.x; i < RUN / 2; i += T) {
-      const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst + i));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src + i));
-    }
-    cp_async_commit();
-    return soff;
+    // one thread hands the contiguous 8 m doubles of the tile to the TMA unit
+    if (threadIdx.x == 0) bulk_load(stage, src_d, (unsigned)(RUN * sizeof(double)), &tile_bar);
+    return 0;
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int tile = blockIdx.x;
   int o = tile / NT, tt = tile - o * NT;
   int soff = 0;
+  unsigned phase = 0;
   if (!INPL && tile < ntiles) soff = issue(src_of(o, tt));
   for (; tile < ntiles; tile += gstep) {
     int no = o + step_o, ntt = tt + step_t;
@@ -127,7 +146,12 @@ __global__ void __launch_bounds__(PlanB2<N>::T, PlanB2<N>::MINB) k_dst_blk2(Args
       __syncthreads();   // the previous tile's post-processing is done with buf
       issue(src_of(o, tt));
     }
-    cp_async_wait_all();
+    if (INPL) {
+      cp_async_wait_all();
+    } else {
+      mbar_wait(&tile_bar, phase);
+      phase ^= 1u;
+    }
     __syncthreads();
     const long long tvalid = a.nlev - (long long)tt * kTB;
     const double* st = stage + soff;
