@@ -61,7 +61,7 @@ constexpr int kTB = 8;
 template <int N> struct PlanB2;
 template <> struct PlanB2<256> { static constexpr int T = 256, R1 = 4, MINB = 3; static constexpr bool INPL = false; template <class Lay> using F = Fft<256, 4, T, Lay, 4, 8, 8>; };
 template <> struct PlanB2<512> { static constexpr int T = 256, R1 = 8, MINB = 3; static constexpr bool INPL = false; template <class Lay> using F = Fft<512, 4, T, Lay, 8, 8, 8>; };  // in place: 0.70 vs 0.61 ms (c2)
-template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16, MINB = 2; static constexpr bool INPL = true; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
+template <> struct PlanB2<1024> { static constexpr int T = 256, R1 = 16, MINB = 1; static constexpr bool INPL = false; template <class Lay> using F = Fft<1024, 4, T, Lay, 16, 8, 8>; };
 
 struct ArgsB2 {
   const double* in;
