@@ -208,6 +208,7 @@ def main():
         sh = plans.stream_handle()
         sp, tp = plan.sp.handle, plan.tp.handle
         ev = None
+        wax = bool(lib.bhcp_pint_w_passes_supported(sp))
 
         def step(record=None):
             # phases: [0] ghat, [1] k_modes, [2 + a] DST axis pass a
@@ -220,10 +221,21 @@ def main():
             _lib.check(lib.bhcp_pint_modes(sp, tp, ghat, 0, nx, W, 0, None, status, sh), "modes")
             if record:
                 record[2].record()
-            for a in range(w.dim):
-                _lib.check(lib.bhcp_pint_level_pass(sp, W, None, plans.ptr(y), n, a, sh), "level pass")
+            # the solve's own pass order (bhcp_pint_levels): strided axes in place
+            # on W (k_dst_wax), then the last axis W -> y (k_dst_blk2)
+            if wax:
+                for a in range(w.dim - 1):
+                    _lib.check(lib.bhcp_pint_w_pass(sp, W, n, a, sh), "w pass")
+                    if record:
+                        record[3 + a].record()
+                _lib.check(lib.bhcp_pint_level_pass(sp, W, None, plans.ptr(y), n, 0, sh), "level pass")
                 if record:
-                    record[3 + a].record()
+                    record[2 + w.dim].record()
+            else:
+                for a in range(w.dim):
+                    _lib.check(lib.bhcp_pint_level_pass(sp, W, None, plans.ptr(y), n, a, sh), "level pass")
+                    if record:
+                        record[3 + a].record()
 
         launches_per_step = 1 + (w.dim + 1) + 1 + w.dim  # reset, ghat passes + scale, modes, level passes
         sampler = ClockSampler(local)
@@ -260,8 +272,13 @@ def main():
             for p in range(nph - 1):
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
-        names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"] + \
-                [("k_dst_blk2" if a == 0 else "k_dst_cols3") + f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
+        names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"]
+        if wax:
+            names += [f"k_dst_wax W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]
+            names += [f"k_dst_blk2 level pass (axis -1, W -> y)"]
+        else:
+            names += [("k_dst_blk2" if a == 0 else "k_dst_cols3") + f" level pass {a} (axis -{a + 1})"
+                      for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof

@@ -205,9 +205,17 @@ int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, 
  *   blocked W with k1's first block at koff_dev[k1] (device int64 table of
  *   length m) or, when koff_dev is null, the single-slab layout above.
  *   pass p >= 1 = inverse DST along axis -(p+1) in place on y.
- * bhcp_pint_levels: passes 0..dim-1 on the single-slab layout.
- * bhcp_pint_levels_blocked: passes 0..dim-1 on an all-to-all receive buffer
- *   of blocked chunks (dim >= 2). */
+ * bhcp_pint_w_pass: inverse DST along spatial axis `axis` (0 .. dim-2) in
+ *   place on the blocked W of `nlev` levels (single-slab layout, or a receive
+ *   buffer whose k1 blocks sit at the uniform stride NT * m^(dim-1) * 8, which
+ *   is what the slab layouts produce). TMA tensor loads/stores; needs dim 2/3
+ *   and m + 1 in {256, 512, 1024} (bhcp_pint_w_passes_supported), W 16-byte
+ *   aligned.
+ * bhcp_pint_levels / bhcp_pint_levels_blocked: all spatial passes, W (or the
+ *   receive buffer) -> y. When bhcp_pint_w_passes_supported, the strided axes
+ *   run first in place on the input (which is therefore overwritten), then
+ *   pass 0; otherwise passes 0..dim-1 as above and the input is untouched.
+ *   levels_blocked needs dim >= 2. */
 int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
                    double* ghat_dev, void* stream);
 int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
@@ -217,9 +225,12 @@ int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
 int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev,
                          const int64_t* koff_dev, double* y_dev, int64_t nlev,
                          int pass, void* stream);
-int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
+int bhcp_pint_w_pass(const bhcp_space_plan* sp, double* w_dev, int64_t nlev, int axis,
+                     void* stream);
+int bhcp_pint_w_passes_supported(const bhcp_space_plan* sp);
+int bhcp_pint_levels(const bhcp_space_plan* sp, double* in_dev, double* out_dev,
                      int64_t batch, void* stream);
-int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev,
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev,
                              const int64_t* koff_dev, double* out_dev, int64_t batch,
                              void* stream);
 

@@ -72,6 +72,8 @@ SIGNATURES = {
     "bhcp_pint_modes_sym_to": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _int, _vp, _vp, _vp]),
     "bhcp_pint_modes_to": (_int, [_vp, _vp, _vp, _i64, _i64, _vp, _int, _vp, _vp, _vp]),
     "bhcp_pint_level_pass": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "bhcp_pint_w_pass": (_int, [_vp, _vp, _i64, _int, _vp]),
+    "bhcp_pint_w_passes_supported": (_int, [_vp]),
     "bhcp_pint_levels": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "bhcp_pint_levels_blocked": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "bhcp_spectral_workspace_bytes": (ctypes.c_size_t, [_vp, _i64]),

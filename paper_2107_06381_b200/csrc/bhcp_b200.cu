@@ -97,6 +97,8 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 #include "gather_dst.cuh"
 #include "gt_modes.cuh"
 #include "pf_modes.cuh"
+#include "wax_dst.cuh"
+#include <cudaTypedefs.h>
 namespace bhcp {
 
 template <int V> struct VT;
@@ -824,6 +826,9 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<256>);
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
+  allow_smem(wax::k_dst_wax<256>);
+  allow_smem(wax::k_dst_wax<512>);
+  allow_smem(wax::k_dst_wax<1024>);
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
@@ -1413,6 +1418,105 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
   return launch_rows(sp, y, y, 0, nlev * P1, 0, nullptr, nullptr, s, Blocked(), P1);
 }
 
+// ---- strided axes in place on the blocked W (wax_dst.cuh), TMA tensor maps
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+std::mutex g_encode_mutex;
+
+int tensor_map_3d(CUtensorMap* tm, double* base, long long Li, long long m, long long No, long long as_elems,
+                  long long os_elems, int box_lines) {
+  {
+    std::lock_guard<std::mutex> lk(g_encode_mutex);
+    if (!g_encode_tiled) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+        return fail(BHCP_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+      g_encode_tiled = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)Li, (cuuint64_t)m, (cuuint64_t)No};
+  const cuuint64_t strides[2] = {(cuuint64_t)as_elems * sizeof(double), (cuuint64_t)os_elems * sizeof(double)};
+  const cuuint32_t box[3] = {(cuuint32_t)box_lines, (cuuint32_t)wax::kBoxRows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode_tiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BHCP_ERR_INVALID, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  return BHCP_OK;
+}
+
+template <int N>
+int wax_launch(const bhcp_space_plan* sp, double* W, long long Li, long long No, long long nlev, long long lpl,
+               cudaStream_t s) {
+  using P = wax::PlanWX<N>;
+  constexpr int LW = 2 * P::S;
+  const long long m = N - 1;
+  const long long lchunks = (Li + LW - 1) / LW;
+  const long long tiles = lchunks * No;
+  if (tiles == 0) return BHCP_OK;
+  if (tiles > 0x7fffffffLL || Li > 0x7fffffffLL || No > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "too many tiles");
+  if (reinterpret_cast<uintptr_t>(W) % 16 != 0) return fail(BHCP_ERR_INVALID, "W must be 16-byte aligned");
+  alignas(64) CUtensorMap tm;
+  int rc = tensor_map_3d(&tm, W, Li, m, No, Li, Li * m, LW);
+  if (rc) return rc;
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  wax::ArgsWX a{sp->twN, sp->snN, sqrt(2.0 / N), (int)lchunks, (int)tiles,
+                (int)(nlev - (NT - 1) * fastk::kTBL), (int)NT, lpl};
+  const size_t sm = wax::smem_bytes<N>();
+  const long long grid = std::min<long long>(tiles, resident_ctas(wax::k_dst_wax<N>, P::T, sm));
+  wax::k_dst_wax<N><<<(unsigned)grid, P::T, sm, s>>>(tm, a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_wax launch");
+  return BHCP_OK;
+}
+
+bool wax_ok(const bhcp_space_plan* sp) {
+  const int L = 2 * (sp->m + 1);
+  return !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && (L == 512 || L == 1024 || L == 2048);
+}
+
+// In-place inverse DST of the blocked W (single-slab layout with NT level
+// tiles, or an all-to-all receive buffer, whose k1 blocks sit at the same
+// uniform stride NT * P1 * 8) along spatial axis `axis` < dim - 1.
+//   axis 0 (k1):  lines = a whole k1 block (NT * P1 * 8 contiguous doubles)
+//   axis 1 (k2, 3D): lines = (k3, level) runs of 8m doubles, outer = (k1, level tile)
+int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaStream_t s) {
+  if (!wax_ok(sp)) return fail(BHCP_ERR_INVALID, "w_pass: unsupported length or dimension");
+  if (axis < 0 || axis > sp->dim - 2) return fail(BHCP_ERR_INVALID, "w_pass: axis out of range");
+  const long long m = sp->m, d = sp->dim;
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  const long long P1 = ipow(m, d - 1);
+  if (nlev == 0) return BHCP_OK;
+  long long Li, No, lpl;
+  if (axis == 0) { Li = NT * P1 * fastk::kTBL; No = 1; lpl = P1 * fastk::kTBL; }
+  else { Li = ipow(m, d - 1 - axis) * fastk::kTBL; No = m * NT * ipow(m, axis - 1); lpl = 0; }
+  switch (m + 1) {
+    case 256: return wax_launch<256>(sp, W, Li, No, nlev, lpl, s);
+    case 512: return wax_launch<512>(sp, W, Li, No, nlev, lpl, s);
+    case 1024: return wax_launch<1024>(sp, W, Li, No, nlev, lpl, s);
+  }
+  return fail(BHCP_ERR_INVALID, "w_pass length");
+}
+
+// All spatial passes of the fused solve: W (blocked, consumed) -> y.
+// Fast lengths in 2D/3D: the strided axes in place on W (k_dst_wax), then
+// the last axis W -> y (k_dst_blk2). Otherwise pass 0 into y, then the
+// strided axes in place on y.
+int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, double* y, long long nlev,
+               cudaStream_t s) {
+  if (wax_ok(sp)) {
+    for (int a = 0; a < sp->dim - 1; ++a) {
+      int rc = w_pass(sp, W, nlev, a, s);
+      if (rc) return rc;
+    }
+    return level_pass(sp, W, koff, y, nlev, 0, s);
+  }
+  for (int p = 0; p < sp->dim; ++p) {
+    int rc = level_pass(sp, W, koff, y, nlev, p, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
+}
+
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace
@@ -1852,15 +1956,19 @@ int bhcp_pint_level_pass(const bhcp_space_plan* sp, const double* in_dev, const 
   return level_pass(sp, in_dev, (const long long*)koff_dev, y_dev, nlev, pass, as_stream(stream));
 }
 
-int bhcp_pint_levels(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t batch,
+int bhcp_pint_w_pass(const bhcp_space_plan* sp, double* w_dev, int64_t nlev, int axis, void* stream) {
+  if (!sp || !w_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  DeviceGuard g(sp->device);
+  return w_pass(sp, w_dev, nlev, axis, as_stream(stream));
+}
+
+int bhcp_pint_w_passes_supported(const bhcp_space_plan* sp) { return sp && wax_ok(sp) ? 1 : 0; }
+
+int bhcp_pint_levels(const bhcp_space_plan* sp, double* in_dev, double* out_dev, int64_t batch,
                      void* stream) {
   if (!sp || !in_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   DeviceGuard g(sp->device);
-  for (int p = 0; p < sp->dim; ++p) {
-    int rc = level_pass(sp, in_dev, nullptr, out_dev, batch, p, as_stream(stream));
-    if (rc) return rc;
-  }
-  return BHCP_OK;
+  return levels_all(sp, in_dev, nullptr, out_dev, batch, as_stream(stream));
 }
 
 int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* g_dev, double divisor,
@@ -1880,23 +1988,15 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   const double cscale = 1.0 / (divisor * (double)tp->n);
   rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, native_layout(sp, sp->nx, tp->n), st, s);
   if (rc) return rc;
-  for (int p = 0; p < sp->dim; ++p) {
-    rc = level_pass(sp, W, nullptr, y_dev, tp->n, p, s);
-    if (rc) return rc;
-  }
-  return BHCP_OK;
+  return levels_all(sp, W, nullptr, y_dev, tp->n, s);
 }
 
-int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, const double* in_dev, const int64_t* koff_dev,
+int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev, const int64_t* koff_dev,
                              double* out_dev, int64_t batch, void* stream) {
   if (!sp || !in_dev || !koff_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
   DeviceGuard g(sp->device);
-  for (int p = 0; p < sp->dim; ++p) {
-    int rc = level_pass(sp, in_dev, (const long long*)koff_dev, out_dev, batch, p, as_stream(stream));
-    if (rc) return rc;
-  }
-  return BHCP_OK;
+  return levels_all(sp, in_dev, (const long long*)koff_dev, out_dev, batch, as_stream(stream));
 }
 
 size_t bhcp_pint_unfused_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
