@@ -98,6 +98,7 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 #include "gt_modes.cuh"
 #include "pf_modes.cuh"
 #include "wax_dst.cuh"
+#include "wax2_dst.cuh"
 #include <cudaTypedefs.h>
 namespace bhcp {
 
@@ -826,9 +827,10 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<256>);
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
-  allow_smem(wax::k_dst_wax<256>);
-  allow_smem(wax::k_dst_wax<512>);
-  allow_smem(wax::k_dst_wax<1024>);
+  allow_smem(wax::k_dst_wax<wax::PlanWX<256>>);
+  allow_smem(wax::k_dst_wax<wax::PlanWX<1024>>);
+  allow_smem(wax2::k_dst_wax2<512>);
+  allow_smem(wax2::k_dst_blk3<512>);
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
@@ -1381,6 +1383,8 @@ int cols_blk2(const bhcp_space_plan* sp, const double* in, double* out, long lon
   return fail(BHCP_ERR_INVALID, "cols_blk2 length");
 }
 
+int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s);
+
 // One level pass of the fused solve on `nlev` levels. pass 0: W (1D:
 // level-major; else blocked, k1's first block at koff[k1] or k1*NT*P1*8) ->
 // y (level-major) with the DST along the last axis; pass p >= 1: DST along
@@ -1401,6 +1405,7 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
   const long long P1 = ipow(m, d - 1);
   if (pass >= 1)
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
+  if (!g_disable_fast && L == 1024 && d <= 3 && !koff) return blk3_launch(sp, in, y, nlev, s);
   if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
     gdst::ArgsB2 b{};
     b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
@@ -1423,7 +1428,7 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 std::mutex g_encode_mutex;
 
 int tensor_map_3d(CUtensorMap* tm, double* base, long long Li, long long m, long long No, long long as_elems,
-                  long long os_elems, int box_lines) {
+                  long long os_elems, int box_lines, int swizzle_bytes = 0) {
   {
     std::lock_guard<std::mutex> lk(g_encode_mutex);
     if (!g_encode_tiled) {
@@ -1439,16 +1444,19 @@ int tensor_map_3d(CUtensorMap* tm, double* base, long long Li, long long m, long
   const cuuint32_t box[3] = {(cuuint32_t)box_lines, (cuuint32_t)wax::kBoxRows, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = g_encode_tiled(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                              : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                    : CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(BHCP_ERR_INVALID, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
   return BHCP_OK;
 }
 
-template <int N>
+template <class P>
 int wax_launch(const bhcp_space_plan* sp, double* W, long long Li, long long No, long long nlev, long long lpl,
                cudaStream_t s) {
-  using P = wax::PlanWX<N>;
+  constexpr int N = P::N;
   constexpr int LW = 2 * P::S;
   const long long m = N - 1;
   const long long lchunks = (Li + LW - 1) / LW;
@@ -1461,11 +1469,59 @@ int wax_launch(const bhcp_space_plan* sp, double* W, long long Li, long long No,
   if (rc) return rc;
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
   wax::ArgsWX a{sp->twN, sp->snN, sqrt(2.0 / N), (int)lchunks, (int)tiles,
-                (int)(nlev - (NT - 1) * fastk::kTBL), (int)NT, lpl};
-  const size_t sm = wax::smem_bytes<N>();
-  const long long grid = std::min<long long>(tiles, resident_ctas(wax::k_dst_wax<N>, P::T, sm));
-  wax::k_dst_wax<N><<<(unsigned)grid, P::T, sm, s>>>(tm, a);
+                (int)(nlev - (NT - 1) * fastk::kTBL), (int)NT, lpl > 0 ? (int)((NT - 1) * lpl) : -1};
+  const size_t sm = wax::smem_bytes<P>();
+  const long long grid = std::min<long long>(tiles, resident_ctas(wax::k_dst_wax<P>, P::T, sm));
+  wax::k_dst_wax<P><<<(unsigned)grid, P::T, sm, s>>>(tm, a);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_wax launch");
+  return BHCP_OK;
+}
+
+template <int N>
+int wax2_launch(const bhcp_space_plan* sp, double* W, long long Li, long long No, long long nlev, long long lpl,
+                cudaStream_t s) {
+  constexpr int LW = wax2::kLW;
+  const long long m = N - 1;
+  const long long lchunks = (Li + LW - 1) / LW;
+  const long long tiles = lchunks * No;
+  if (tiles == 0) return BHCP_OK;
+  if (tiles > 0x7fffffffLL || Li > 0x7fffffffLL || No > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "too many tiles");
+  if (reinterpret_cast<uintptr_t>(W) % 16 != 0) return fail(BHCP_ERR_INVALID, "W must be 16-byte aligned");
+  alignas(64) CUtensorMap tm;
+  int rc = tensor_map_3d(&tm, W, Li, m, No, Li, Li * m, LW, 128);
+  if (rc) return rc;
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  wax::ArgsWX a{sp->twN, sp->snN, sqrt(2.0 / N), (int)lchunks, (int)tiles,
+                (int)(nlev - (NT - 1) * fastk::kTBL), (int)NT, lpl > 0 ? (int)((NT - 1) * lpl) : -1};
+  const size_t sm = wax2::smem_bytes<N>();
+  const int threads = (wax2::kCW + 1) * 32;
+  const long long grid = std::min<long long>(tiles, resident_ctas(wax2::k_dst_wax2<N>, threads, sm));
+  wax2::k_dst_wax2<N><<<(unsigned)grid, threads, sm, s>>>(tm, a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_wax2 launch");
+  return BHCP_OK;
+}
+
+// last spatial axis, blocked W -> y, N = 512 (k_dst_blk3, wax2_dst.cuh)
+int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s) {
+  constexpr int N = 512;
+  const long long m = sp->m, d = sp->dim;
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  const long long idiv = ipow(m, d - 2);
+  const long long No = m * NT * idiv;   // W blocks (k1, level tile, r2)
+  if (No == 0) return BHCP_OK;
+  if (No > 0x7fffffffLL) return fail(BHCP_ERR_INVALID, "too many tiles");
+  if (reinterpret_cast<uintptr_t>(W) % 16 != 0) return fail(BHCP_ERR_INVALID, "W must be 16-byte aligned");
+  alignas(64) CUtensorMap tm;
+  // view {8 levels, m elements (64 B rows), No blocks}
+  int rc = tensor_map_3d(&tm, const_cast<double*>(W), fastk::kTBL, m, No, fastk::kTBL, fastk::kTBL * m,
+                         fastk::kTBL, 64);
+  if (rc) return rc;
+  wax2::ArgsB3 a{sp->twN, sp->snN, sqrt(2.0 / N), y, (int)No, (int)NT, (int)idiv, (int)nlev, (int)m};
+  const size_t sm = wax2::smem_bytes_b3<N>();
+  const int threads = (wax2::kCW + 1) * 32;
+  const long long grid = std::min<long long>(No, resident_ctas(wax2::k_dst_blk3<N>, threads, sm));
+  wax2::k_dst_blk3<N><<<(unsigned)grid, threads, sm, s>>>(tm, a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk3 launch");
   return BHCP_OK;
 }
 
@@ -1490,9 +1546,9 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
   if (axis == 0) { Li = NT * P1 * fastk::kTBL; No = 1; lpl = P1 * fastk::kTBL; }
   else { Li = ipow(m, d - 1 - axis) * fastk::kTBL; No = m * NT * ipow(m, axis - 1); lpl = 0; }
   switch (m + 1) {
-    case 256: return wax_launch<256>(sp, W, Li, No, nlev, lpl, s);
-    case 512: return wax_launch<512>(sp, W, Li, No, nlev, lpl, s);
-    case 1024: return wax_launch<1024>(sp, W, Li, No, nlev, lpl, s);
+    case 256: return wax_launch<wax::PlanWX<256>>(sp, W, Li, No, nlev, lpl, s);
+    case 512: return wax2_launch<512>(sp, W, Li, No, nlev, lpl, s);   // warp per line pair (wax2_dst.cuh)
+    case 1024: return wax_launch<wax::PlanWX<1024>>(sp, W, Li, No, nlev, lpl, s);
   }
   return fail(BHCP_ERR_INVALID, "w_pass length");
 }
@@ -1508,6 +1564,7 @@ int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, doub
       int rc = w_pass(sp, W, nlev, a, s);
       if (rc) return rc;
     }
+    if (sp->m + 1 == 512) return blk3_launch(sp, W, y, nlev, s);   // k1 blocks at the uniform stride
     return level_pass(sp, W, koff, y, nlev, 0, s);
   }
   for (int p = 0; p < sp->dim; ++p) {

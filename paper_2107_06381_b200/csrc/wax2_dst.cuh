@@ -1,0 +1,481 @@
+// wax2_dst.cuh -- strided spatial axes in place on the blocked W, one warp
+// per line pair, no CTA barriers (N = 512: c2).
+//
+// Same job and tiling as k_dst_wax (wax_dst.cuh): a tile is 16 adjacent
+// lines x 511 elements of a 3D view of W, moved by TMA tensor loads/stores.
+// The difference is who works on it:
+//   * the tile lands 128B-swizzled (16-byte chunk q of row e at chunk
+//     q ^ (e & 7)), so one line pair q -- a column of 16-byte elements -- is
+//     read and written conflict-free by a warp whose lanes walk the rows;
+//   * each of the 8 consumer warps owns one line pair and runs the whole
+//     half-length real DST-I on its own column: pre-step + three radix-8
+//     Stockham stages in place, synchronised with __syncwarp only, then the
+//     even/odd output split with the odd-output prefix sum as warp shuffles;
+//   * a producer warp issues the TMA loads, waits for the 8 consumer warps of
+//     a buffer (mbarrier), issues its TMA store and refills it.
+// Warps therefore progress independently across tiles (the latency hiding of
+// k_modes_fast), and every element is read once by the pre-step (lane u
+// takes butterflies u and 64 - u, whose inputs are each other's mirrors
+// x_j / x_{N-j}) and the prefix-sum split is fused into the last stage
+// (the same pairing holds U_k and U_{N-k}): 8 shared-memory passes per tile
+// instead of 11.
+// Bank conflicts: stage 1 writes index i = 8a + b; it is stored at row
+// 8a + ((a + b) & 7) (a within-octet rotation that stage 2 reads back), so
+// both the stride-8 writes of stage 1 and the unit-stride reads of stage 2
+// hit 8 distinct chunks per 8 lanes.
+// Reference: the DSTs of space.py:163-177 per level (pint.py:94-96).
+#pragma once
+#include "wax_dst.cuh"
+
+namespace bhcp {
+namespace wax2 {
+
+using namespace sfft;
+using wax::su32;
+using wax::mbar_init;
+using wax::mbar_expect;
+using wax::mbar_wait;
+using wax::tma_load3;
+using wax::tma_store3;
+
+constexpr int kCW = 8;      // consumer warps = line pairs per tile
+constexpr int kNBUF = 3;    // tile buffers
+constexpr int kLW = 16;     // lines per tile (128 B rows)
+
+template <int N> constexpr size_t smem_bytes() {
+  return 1024 /* alignment slack */ + (size_t)kNBUF * N * 128 + sizeof(double) * N + 16 * kNBUF;
+}
+
+// try_wait with a suspend-time hint: the thread sleeps in hardware until the
+// phase completes (or the hint expires) instead of spinning on issue slots
+__device__ __forceinline__ void mbar_sleep_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(su32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+// rows 2k - 1 (pe <- ev) and 2k (po <- od) of one k: lanes with sw store them
+// in the other order, so each of the two stores covers 8 distinct chunks per
+// 8 lanes (explicit selects; predicated stores would split the warp)
+__device__ __forceinline__ void store_pair(bool sw, double2* pe, double2 ev, double2* po, double2 od, bool has_ev) {
+  asm volatile(
+      "{\n .reg .pred q, h;\n .reg .f64 x1, y1, x2, y2;\n .reg .b32 a1, a2;\n"
+      " setp.ne.u32 q, %0, 0;\n setp.ne.u32 h, %1, 0;\n"
+      " selp.f64 x1, %2, %4, q;\n selp.f64 y1, %3, %5, q;\n"
+      " selp.f64 x2, %4, %2, q;\n selp.f64 y2, %5, %3, q;\n"
+      " selp.b32 a1, %6, %7, q;\n selp.b32 a2, %7, %6, q;\n"
+      " @h st.shared.v2.f64 [a1], {x1, y1};\n"
+      " st.shared.v2.f64 [a2], {x2, y2};\n}\n" ::"r"((unsigned)sw),
+      "r"((unsigned)has_ev), "d"(od.x), "d"(od.y), "d"(ev.x), "d"(ev.y), "r"(su32(po)), "r"(su32(pe))
+      : "memory");
+}
+// Relaxed arrive: orders nothing, so it does not wait for the warp's global
+// stores to drain. Used where the only hazard is the buffer's shared-memory
+// reads, which have completed (their values feed the stores issued before).
+__device__ __forceinline__ void mbar_arrive_relaxed(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+
+// TMA-swizzled tiles of 16-byte chunks (one chunk = one line pair):
+//   Sw128: 128 B rows (8 pairs), chunk q of row e at q ^ (e & 7)          (SWIZZLE_128B)
+//   Sw64:   64 B rows (4 pairs), chunk q of row e at q ^ ((e >> 1) & 3)   (SWIZZLE_64B)
+// Either way the 16-byte bank group of (e, q) is a bijection of e & 7 for a
+// fixed q, so 8 lanes on rows with distinct e & 7 are conflict-free.
+struct Sw128 {
+  static constexpr int RS = 8;
+  static __device__ __forceinline__ int key(int e) { return e & 7; }
+};
+struct Sw64 {
+  static constexpr int RS = 4;
+  static __device__ __forceinline__ int key(int e) { return (e >> 1) & 3; }
+};
+template <class L>
+__device__ __forceinline__ double2* at(double2* tile, int e, int q) { return tile + e * L::RS + (q ^ L::key(e)); }
+
+// Per-lane constants of warp_dst512.
+struct LaneK {
+  int u, j1, j2;          // lane; butterflies of stages 1 and 3 (u, 64 - u; lane 0: 0, 32)
+  double2 w2, w3a, w3b;   // stage-2 twiddle w^((lane%8)*8), stage-3 twiddles w^j1, w^j2
+  double mup[5], mdn[5];  // scan masks: 1 where the shuffled neighbour exists
+  double scale;
+  __device__ __forceinline__ LaneK(int lane, const double2* tw, double sc) {
+    u = lane; j1 = lane; j2 = lane == 0 ? 32 : 64 - lane;
+    w2 = __ldg(tw + (lane & 7) * 8);
+    w3a = __ldg(tw + j1); w3b = __ldg(tw + j2);
+    scale = sc;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      mup[s] = lane >= (1 << s) ? 1.0 : 0.0;
+      mdn[s] = lane + (1 << s) < 32 ? 1.0 : 0.0;
+    }
+  }
+};
+
+// The half-length real DST-I of line pair q (a column of the swizzled tile T,
+// rows e = 0..N-2 = the m elements, row N-1 zero) in place, by one warp:
+// pre-step + three radix-8 Stockham stages + even/odd split with the
+// odd-output prefix sum. Output e (scaled) is left in row e.
+// Default output sink: rows 2k - 1 / 2k of the column (conflict-free order).
+template <class L>
+struct ColumnSink {
+  double2 *lo_ev, *lo_od, *hi_ev, *hi_od;
+  __device__ __forceinline__ ColumnSink(double2* T, int q, int u, int j1, int j2) {
+    // output rows 2k - 1, 2k of k = j + 64 r: chunk independent of r (rows step 128)
+    lo_ev = at<L>(T, u == 0 ? 127 : 2 * j1 - 1, q) - (u == 0 ? 128 * L::RS : 0);   // lane 0: row 128 r - 1 (r >= 1)
+    lo_od = at<L>(T, 2 * j1, q);
+    hi_ev = at<L>(T, 2 * j2 - 1, q);
+    hi_od = at<L>(T, 2 * j2, q);
+  }
+  // k = j1 + 64 r (hi = false) or j2 + 64 r (hi = true); ev = S_{2k} -> element 2k - 1, od = S_{2k+1} -> 2k
+  __device__ __forceinline__ void put(int r, bool hi, int u, double2 ev, double2 od) {
+    const bool sw = (u & 4) != 0;
+    if (!hi) store_pair(sw, lo_ev + 128 * L::RS * r, ev, lo_od + 128 * L::RS * r, od, (u | r) != 0);
+    else store_pair(sw, hi_ev + 128 * L::RS * r, ev, hi_od + 128 * L::RS * r, od, true);
+  }
+};
+
+template <class L, class Sink>
+__device__ __forceinline__ void warp_dst512(double2* T, int q, const LaneK& K, const double* sn, Sink& sink) {
+  constexpr int N = 512;
+  constexpr int R8 = 8 * L::RS, R64 = 64 * L::RS, R128 = 128 * L::RS;   // 8 / 64 / 128 rows
+  const int u = K.u, j1 = K.j1, j2 = K.j2;
+  const double2 w2 = K.w2, w3a = K.w3a, w3b = K.w3b;
+  const double scale = K.scale;
+  const int lane = u;
+    // ---- stage 1: u_i = s_i (x_i + x_{N-i}) + (x_i - x_{N-i})/2 for the 16 indices
+    // i = j1 + 64 r, j2 + 64 r; x_i is tile row i - 1 (x_0 = 0)
+    double2 A[8], B[8];
+    {
+      double2 xa[8], xb[8];
+      // x_i sits in row i - 1; row (j + 64 r - 1) & 7 does not depend on r. Lane 0's
+      // x_0 (= 0) is read from row N - 1, the row past m that the TMA unit zero-fills.
+      const double2* pa0 = at<L>(T, u == 0 ? N - 1 : j1 - 1, q);
+      const double2* pa1 = at<L>(T, j1 + 63, q) - R64;   // rows j1 - 1 + 64 r, r >= 1
+      const double2* pb = at<L>(T, j2 - 1, q);
+      xa[0] = *pa0;
+#pragma unroll
+      for (int r = 1; r < 8; ++r) xa[r] = pa1[R64 * r];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) xb[r] = pb[R64 * r];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        // partner of index j1 + 64 r: u >= 1 -> j2 + 64 (7 - r); u == 0 -> j1 + 64 (8 - r) (mod N)
+        const double2 pa = u == 0 ? xa[(8 - r) & 7] : xb[7 - r];
+        const double2 pb = u == 0 ? xb[7 - r] : xa[7 - r];
+        const double sa = sn[j1 + 64 * r], sb = sn[j2 + 64 * r];
+        A[r] = make_double2(fma(sa, xa[r].x + pa.x, 0.5 * (xa[r].x - pa.x)), fma(sa, xa[r].y + pa.y, 0.5 * (xa[r].y - pa.y)));
+        B[r] = make_double2(fma(sb, xb[r].x + pb.x, 0.5 * (xb[r].x - pb.x)), fma(sb, xb[r].y + pb.y, 0.5 * (xb[r].y - pb.y)));
+      }
+    }
+    Cod<8>::run(A);
+    Cod<8>::run(B);
+    __syncwarp();   // every lane has read its inputs
+    // outputs of butterfly j at index 8 j + r, stored at row 8 j + ((j + r) & 7)
+    {
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        *at<L>(T, 8 * j1 + ((j1 + r) & 7), q) = A[r];
+        *at<L>(T, 8 * j2 + ((j2 + r) & 7), q) = B[r];
+      }
+    }
+    __syncwarp();
+    // ---- stage 2: butterflies j = lane, lane + 32; read index j + 64 r (rotated rows),
+    // twiddle w^((j%8) * 8 * r), write index 64 (j/8) + j%8 + 8 r (natural rows)
+    {
+      double2 v[2][8];
+      // index i = j + 64 r = 8 a + b (a = j/8 + 8 r, b = j%8) is at row
+      // 8 a + ((a + b) & 7) = 64 r + 8 (j/8) + ((j/8 + j%8) & 7): r-independent chunk
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        const double2* p = at<L>(T, 8 * (j >> 3) + (((j >> 3) + (j & 7)) & 7), q);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) v[h][r] = p[R64 * r];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        apply_twiddles<8>(v[h], w2);
+        Cod<8>::run(v[h]);
+        double2* p = at<L>(T, 64 * (j >> 3) + (j & 7), q);   // rows base + 8 r: chunk fixed
+#pragma unroll
+        for (int r = 0; r < 8; ++r) p[R8 * r] = v[h][r];
+      }
+    }
+    __syncwarp();
+    // ---- stage 3: butterflies j1, j2: read j + 64 r, twiddle w^(j r), outputs U_{j + 64 r}
+    {
+      const double2* pa = at<L>(T, j1, q);
+      const double2* pb = at<L>(T, j2, q);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        A[r] = pa[R64 * r];
+        B[r] = pb[R64 * r];
+      }
+    }
+    apply_twiddles<8>(A, w3a);
+    apply_twiddles<8>(B, w3b);
+    Cod<8>::run(A);
+    Cod<8>::run(B);
+    __syncwarp();   // all of U read before the outputs overwrite the column
+    // ---- split: for k < N/2, U^a_k = (U_k + conj U_{N-k})/2, U^b_k = (U_k - conj U_{N-k})/(2i);
+    // S_{2k} = -Im U_k per line, S_{2k+1} = sum_{i<=k} Re U_i - Re U_0 / 2.
+    // Block r (k in [64 r, 64 r + 64)): lane u holds position u ("lo", k = j1 + 64 r)
+    // and position 64 - u ("hi", k = j2 + 64 r; lane 0: position 32).
+    const double2 U0 = make_double2(__shfl_sync(0xffffffffu, A[0].x, 0), __shfl_sync(0xffffffffu, A[0].y, 0));
+    double offa = -0.5 * U0.x, offb = -0.5 * U0.y;   // running block offsets minus Re U_0 / 2
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double2 P = A[r], Q = u == 0 ? A[(8 - r) & 7] : B[7 - r];     // U_k, U_{N-k}, k = j1 + 64 r
+      const double2 Ph = B[r], Qh = u == 0 ? B[7 - r] : A[7 - r];         // k = j2 + 64 r
+      double la = 0.5 * (P.x + Q.x), lb = 0.5 * (P.y + Q.y);
+      double ha = 0.5 * (Ph.x + Qh.x), hb = 0.5 * (Ph.y + Qh.y);
+      const double ela = -0.5 * (P.y - Q.y), elb = 0.5 * (P.x - Q.x);     // S_{2k}, k = j1 + 64 r
+      const double eha = -0.5 * (Ph.y - Qh.y), ehb = 0.5 * (Ph.x - Qh.x); // S_{2k}, k = j2 + 64 r
+      // inclusive scan of lo over lanes; suffix scan of hi over lanes 1..31
+      const double h0a = __shfl_sync(0xffffffffu, ha, 0), h0b = __shfl_sync(0xffffffffu, hb, 0);
+      if (u == 0) { ha = 0.0; hb = 0.0; }
+#pragma unroll
+      for (int s = 0; s < 5; ++s) {
+        const int off = 1 << s;
+        const double va = __shfl_up_sync(0xffffffffu, la, off), vb = __shfl_up_sync(0xffffffffu, lb, off);
+        const double wa = __shfl_down_sync(0xffffffffu, ha, off), wb = __shfl_down_sync(0xffffffffu, hb, off);
+        la = fma(K.mup[s], va, la);
+        lb = fma(K.mup[s], vb, lb);
+        ha = fma(K.mdn[s], wa, ha);
+        hb = fma(K.mdn[s], wb, hb);
+      }
+      const double tla = __shfl_sync(0xffffffffu, la, 31), tlb = __shfl_sync(0xffffffffu, lb, 31);
+      const double tha = __shfl_sync(0xffffffffu, ha, 0), thb = __shfl_sync(0xffffffffu, hb, 0);
+      const double mida = tla + h0a, midb = tlb + h0b;   // prefix through position 32
+      const double oloa = offa + la, olob = offb + lb;                                      // S_{2k+1}, lo
+      const double ohia = offa + mida + (u == 0 ? 0.0 : ha), ohib = offb + midb + (u == 0 ? 0.0 : hb);  // hi
+      offa += mida + tha;
+      offb += midb + thb;
+      sink.put(r, false, u, make_double2(scale * ela, scale * elb), make_double2(scale * oloa, scale * olob));
+      sink.put(r, true, u, make_double2(scale * eha, scale * ehb), make_double2(scale * ohia, scale * ohib));
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_wax2(const __grid_constant__ CUtensorMap tm,
+                                                                 wax::ArgsWX a) {
+  static_assert(N == 512, "three radix-8 stages");
+  constexpr int NBOX = N / wax::kBoxRows;
+  constexpr unsigned TILE_BYTES = (unsigned)(N * kLW * sizeof(double));
+  extern __shared__ unsigned char smem_raw[];
+  // TMA 128B swizzle needs 1024-byte aligned tiles
+  unsigned char* base = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  double2* tiles = reinterpret_cast<double2*>(base);
+  double* sn = reinterpret_cast<double*>(base + (size_t)kNBUF * N * 128);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sn + N);
+  unsigned long long* done = full + kNBUF;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) sn[j] = __ldg(a.sn + j);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
+    for (int b = 0; b < kNBUF; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(done + b, kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int ntiles_cta = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
+
+  if (warp == kCW) {
+    // ------------------------------------------------------------ producer
+    if (lane != 0) return;
+    auto load = [&](int it, int b) {
+      const int tile = blockIdx.x + it * G;
+      const int o = tile / a.lchunks, c = tile - o * a.lchunks;
+      double2* dst = tiles + b * N * 8;
+      mbar_expect(full + b, TILE_BYTES);
+#pragma unroll
+      for (int x = 0; x < NBOX; ++x) tma_load3(dst + x * wax::kBoxRows * 8, &tm, c * kLW, x * wax::kBoxRows, o, full + b);
+    };
+    auto store = [&](int it, int b) {
+      const int tile = blockIdx.x + it * G;
+      const int o = tile / a.lchunks, c = tile - o * a.lchunks;
+      // the producer is not latency critical: back off instead of spinning on
+      // the issue slots the consumer warps need
+      mbar_sleep_wait(done + b, (unsigned)((it / kNBUF) & 1));
+      const double2* src = tiles + b * N * 8;
+#pragma unroll
+      for (int x = 0; x < NBOX; ++x) tma_store3(&tm, c * kLW, x * wax::kBoxRows, o, src + x * wax::kBoxRows * 8);
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    };
+    for (int it = 0; it < ntiles_cta; ++it) {
+      const int b = it % kNBUF;
+      if (it >= kNBUF) {
+        store(it - kNBUF, b);
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      }
+      load(it, b);
+    }
+    for (int it = ntiles_cta - kNBUF < 0 ? 0 : ntiles_cta - kNBUF; it < ntiles_cta; ++it) store(it, it % kNBUF);
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int q = warp;   // line pair (lines 2q, 2q+1) of every tile
+  const LaneK K(lane, a.tw, a.scale);
+  // tile = blockIdx.x + it * G as (outer o, chunk c), advanced incrementally
+  const int dG_o = G / a.lchunks, dG_c = G - dG_o * a.lchunks;
+  int to = (int)blockIdx.x / a.lchunks, tc = (int)blockIdx.x - to * a.lchunks;
+  for (int it = 0; it < ntiles_cta; ++it) {
+    const int b = it % kNBUF;
+    const int o = to, c = tc;
+    tc += dG_c; to += dG_o;
+    if (tc >= a.lchunks) { tc -= a.lchunks; ++to; }
+    double2* T = tiles + b * N * 8;
+    mbar_sleep_wait(full + b, (unsigned)((it / kNBUF) & 1));
+    if (a.vlast < 8) {
+      // padding levels of the last level tile share a complex FFT with a
+      // valid level: zero them (rare tiles only)
+      const int l0 = c * kLW + 2 * q;
+      const bool lastA = a.llast >= 0 ? l0 >= a.llast : (o % a.nt == a.nt - 1);
+      const bool lastB = a.llast >= 0 ? l0 + 1 >= a.llast : lastA;
+      const bool za = lastA && (int)(l0 & 7) >= a.vlast, zb = lastB && (int)((l0 + 1) & 7) >= a.vlast;
+      if (za || zb) {
+        for (int e = lane; e < N; e += 32) {
+          double2* p = at<Sw128>(T, e, q);
+          if (za) p->x = 0.0;
+          if (zb) p->y = 0.0;
+        }
+        __syncwarp();
+      }
+    }
+    ColumnSink<Sw128> sink(T, q, K.u, K.j1, K.j2);
+    warp_dst512<Sw128>(T, q, K, sn, sink);
+    // hand the buffer to the producer (its TMA store reads it through the async proxy)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(done + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_dst_blk3: the last spatial axis, W -> y (replaces k_dst_blk2 for N = 512).
+// A tile is one W block: 8 levels x m elements of one spatial line, a
+// contiguous 32 KB run ([element][8 levels], 64 B rows), loaded by TMA with
+// the 64-byte swizzle. Four warps (line pairs = level pairs) transform it
+// with warp_dst512 and write their two levels as coalesced rows of y. Eight
+// consumer warps = two groups working on alternate tiles; a producer warp
+// keeps the other buffers loading.
+struct ArgsB3 {
+  const double2* tw;
+  const double* sn;
+  double scale;
+  double* y;           // level-major (nlev, n_space)
+  int ntiles;          // W blocks = m^(d-2) * NT * m
+  int nt;              // NT (level tiles)
+  int idiv;            // m^(d-2): spatial lines per (k1, level tile)
+  int nlev;
+  int m;
+};
+
+// Output sink of k_dst_blk3: the two y rows of the line pair, straight from
+// registers (elements 2k - 1 and 2k of every k the lane holds).
+struct RowSink {
+  double* ya;
+  double* yb;
+  bool va, vb;
+  int j1, j2;
+  __device__ __forceinline__ void put(int r, bool hi, int u, double2 ev, double2 od) {
+    const int k = (hi ? j2 : j1) + 64 * r;
+    const bool he = k > 0;
+    if (va) {
+      if (he) ya[2 * k - 1] = ev.x;
+      ya[2 * k] = od.x;
+    }
+    if (vb) {
+      if (he) yb[2 * k - 1] = ev.y;
+      yb[2 * k] = od.y;
+    }
+  }
+};
+
+constexpr int kB3Buf = 6;
+template <int N> constexpr size_t smem_bytes_b3() {
+  return 1024 + (size_t)kB3Buf * N * 64 + sizeof(double) * N + 16 * kB3Buf;
+}
+
+template <int N>
+__global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_constant__ CUtensorMap tm, ArgsB3 a) {
+  static_assert(N == 512, "three radix-8 stages");
+  constexpr int NBOX = N / wax::kBoxRows;
+  constexpr unsigned TILE_BYTES = (unsigned)(N * 8 * sizeof(double));
+  constexpr int TD2 = N * 4;   // double2 per tile
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  double2* tiles = reinterpret_cast<double2*>(base);
+  double* sn = reinterpret_cast<double*>(base + (size_t)kB3Buf * N * 64);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sn + N);
+  unsigned long long* done = full + kB3Buf;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) sn[j] = __ldg(a.sn + j);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
+    for (int b = 0; b < kB3Buf; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(done + b, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int ntiles_cta = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
+  if (warp == kCW) {
+    if (lane != 0) return;
+    for (int it = 0; it < ntiles_cta; ++it) {
+      const int b = it % kB3Buf;
+      if (it >= kB3Buf) mbar_sleep_wait(done + b, (unsigned)(((it - kB3Buf) / kB3Buf) & 1));
+      const int o = blockIdx.x + it * G;
+      mbar_expect(full + b, TILE_BYTES);
+#pragma unroll
+      for (int x = 0; x < NBOX; ++x) tma_load3(tiles + b * TD2 + x * wax::kBoxRows * 4, &tm, 0, x * wax::kBoxRows, o, full + b);
+    }
+    return;
+  }
+  const int q = warp & 3, grp = warp >> 2;
+  const LaneK K(lane, a.tw, a.scale);
+  const int m = a.m;
+  for (int it = grp; it < ntiles_cta; it += 2) {
+    const int b = it % kB3Buf;
+    double2* T = tiles + b * TD2;
+    const int o = blockIdx.x + it * G;
+    // o = (k1 * NT + lt) * idiv + r2
+    const int o2 = o / a.idiv, r2 = o - o2 * a.idiv;
+    const int k1 = o2 / a.nt, lt = o2 - k1 * a.nt;
+    const int t0 = lt * 8 + 2 * q;   // levels of lines 2q, 2q + 1
+    mbar_sleep_wait(full + b, (unsigned)((it / kB3Buf) & 1));
+    if (t0 + 1 >= a.nlev) {
+      // padding levels of the last level tile: zero them (their partner in the
+      // complex FFT is a valid level)
+      const bool za = t0 >= a.nlev, zb = t0 + 1 >= a.nlev;
+      for (int e = lane; e < N; e += 32) {
+        double2* p = at<Sw64>(T, e, q);
+        if (za) p->x = 0.0;
+        if (zb) p->y = 0.0;
+      }
+      __syncwarp();
+    }
+    // rows of y: level t, spatial line (k1, r2) -> y[((t * m + k1) * idiv + r2) * m + e]
+    const long long rowa = ((long long)((long long)t0 * m + k1) * a.idiv + r2) * m;
+    const long long rowb = rowa + (long long)m * m * a.idiv;
+    RowSink sink{a.y + rowa, a.y + rowb, t0 < a.nlev, t0 + 1 < a.nlev, K.j1, K.j2};
+    warp_dst512<Sw64>(T, q, K, sn, sink);
+    if (lane == 0) mbar_arrive_relaxed(done + b);
+  }
+}
+
+}  // namespace wax2
+}  // namespace bhcp

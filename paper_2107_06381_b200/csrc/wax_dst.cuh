@@ -63,15 +63,21 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // S sequences (LW = 2S lines, LW * 8 B per row chunk), T threads, NBUF tile
 // buffers of N * S complex slots (row e of the tile in slot e; the rows a box
 // covers past m are zero-filled by the TMA unit and never read), first radix R1.
+template <int N_, int S_, int T_, int NBUF_, int MINB_, int R1_, int R2_, int R3_>
+struct CfgWX {
+  static constexpr int N = N_, S = S_, T = T_, NBUF = NBUF_, MINB = MINB_, R1 = R1_;
+  template <class Lay> using F = Fft<N_, S_, T_, Lay, R1_, R2_, R3_>;
+};
+// Measured on c2 (N = 512): 128 B rows beat 64 B rows (0.53 vs 0.73-0.85 ms);
+// N = 512 now runs the warp-per-line-pair k_dst_wax2 (wax2_dst.cuh, 0.45 ms).
 template <int N> struct PlanWX;
-template <> struct PlanWX<256> { static constexpr int S = 16, T = 512, NBUF = 3, R1 = 4; template <class Lay> using F = Fft<256, 16, T, Lay, 4, 8, 8>; };
-template <> struct PlanWX<512> { static constexpr int S = 8, T = 512, NBUF = 3, R1 = 8; template <class Lay> using F = Fft<512, 8, T, Lay, 8, 8, 8>; };
-template <> struct PlanWX<1024> { static constexpr int S = 4, T = 512, NBUF = 3, R1 = 8; template <class Lay> using F = Fft<1024, 4, T, Lay, 8, 8, 16>; };
+template <> struct PlanWX<256> : CfgWX<256, 16, 512, 3, 1, 4, 8, 8> {};
+template <> struct PlanWX<1024> : CfgWX<1024, 4, 512, 3, 1, 8, 8, 16> {};
 
 constexpr int kBoxRows = 256;   // TMA box height (<= 256)
 
-template <int N> constexpr size_t smem_bytes() {
-  using P = PlanWX<N>;
+template <class P> constexpr size_t smem_bytes() {
+  constexpr int N = P::N;
   return sizeof(double2) * (size_t)P::NBUF * N * P::S + sizeof(double) * (N + 2 * (P::T / 32) * P::S) +
          sizeof(unsigned long long) * P::NBUF + 128;
 }
@@ -87,12 +93,12 @@ struct ArgsWX {
   // FFT with a valid line, so it is zeroed after the load:
   int vlast;           // valid levels in level tile NT - 1 (8: no padding)
   int nt;              // NT
-  long long lpl;       // axis 0: lines per level tile (lt = line / lpl); else 0 (lt = outer % NT)
+  int llast;           // axis 0: first line of level tile NT - 1; else -1 (level tile = outer % NT)
 };
 
-template <int N>
-__global__ void __launch_bounds__(PlanWX<N>::T, 1) k_dst_wax(const __grid_constant__ CUtensorMap tm, ArgsWX a) {
-  using P = PlanWX<N>;
+template <class P>
+__global__ void __launch_bounds__(P::T, P::MINB) k_dst_wax(const __grid_constant__ CUtensorMap tm, ArgsWX a) {
+  constexpr int N = P::N;
   constexpr int S = P::S, T = P::T, NBUF = P::NBUF, LW = 2 * S;
   constexpr int NW = T / 32;
   constexpr int KK = 32 / S;        // k values per warp step
@@ -141,14 +147,14 @@ __global__ void __launch_bounds__(PlanWX<N>::T, 1) k_dst_wax(const __grid_consta
     if (a.vlast < 8) {
       // does this tile hold lines of the last level tile? (uniform across the CTA)
       const int o = tile / a.lchunks, c = tile - o * a.lchunks;
-      const long long l0 = (long long)c * LW;
-      const bool last_lo = a.lpl ? (l0 / a.lpl == a.nt - 1) : (o % a.nt == a.nt - 1);
-      const bool last_hi = a.lpl ? ((l0 + LW - 1) / a.lpl == a.nt - 1) : last_lo;
+      const int l0 = c * LW;
+      const bool last_lo = a.llast >= 0 ? l0 >= a.llast : (o % a.nt == a.nt - 1);
+      const bool last_hi = a.llast >= 0 ? l0 + LW - 1 >= a.llast : last_lo;
       if (last_lo || last_hi) {
         double* bd = reinterpret_cast<double*>(buf);
         for (int i = threadIdx.x; i < N * LW; i += T) {
           const int l = i % LW;
-          const bool last = a.lpl ? ((l0 + l) / a.lpl == a.nt - 1) : last_lo;
+          const bool last = a.llast >= 0 ? l0 + l >= a.llast : last_lo;
           if (last && (l & 7) >= a.vlast) bd[i] = 0.0;
         }
         __syncthreads();

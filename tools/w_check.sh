@@ -1,0 +1,5 @@
+# quick check of the level passes on c2: bench, parity subset, ncu of k_dst_wax2 + k_dst_blk3
+out=gpurun_out/wc; mkdir -p $out
+timeout 300 python bench.py --quick --steps 30 --warmup 5 > $out/quick.json 2> $out/quick.err; echo "quick rc=$?"; cat $out/quick.json; tail -3 $out/quick.err
+timeout 600 python -m pytest tests -m gpu -q -x -k "${1:-c2 or full or emulated or 512}" > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 $out/pytest_gpu.log
+ncu --set full --clock-control none --import-source on -k regex:"k_dst_wax2|k_dst_blk3" -s 2 -c 2 -o $out/lv -f python tools/profile_step.py c2 1 > $out/ncu.log 2>&1; echo "ncu rc=$?"
