@@ -11,8 +11,10 @@ metric is space-time DOFs/s over all ranks.
 * e2e        -- the same solve through the C-ABI call with HOST buffers:
                 pinned g -> device, bhcp_pint_solve, full trajectory -> pinned
                 host, every step inside the timed region.
-* roofline   -- dominant kernel of the step, algorithmic bytes / its average
-                CUDA-event duration vs the measured HBM copy bandwidth.
+* roofline   -- dominant kernel of the step: algorithmic bytes (or, for the
+                FP64-bound pass A, algorithmic flops) / its average CUDA-event
+                duration vs the measured HBM copy bandwidth (FP64 FMA peak);
+                roofline_hbm / kernels give every kernel's HBM fraction.
 * cpu_baseline -- the reference 3-step algorithm (oracle port, bit-identical
                 to the reference on the golden vectors) on a bounded sample of
                 the same workload, 1 host core, rank 0 at N=1.
@@ -65,6 +67,27 @@ def peaks():
         d = json.loads(f.read_text())
         return float(d["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def fp64_peak():
+    """Dense FP64 FMA throughput measured on a B200 of this pool by tools/probe_fp64.cu
+    (profiles/fp64_peak.json), else the 37 TFLOP/s datasheet figure."""
+    f = ROOT / "profiles" / "fp64_peak.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["dfma_tflops"]), "measured (tools/probe_fp64.cu)"
+    return 37.0, "datasheet"
+
+
+def modes_alg_flops(dim: int, m: int, n: int) -> float:
+    """Algorithmic FP64 flops of pass A: per time FFT of length n the textbook
+    5 n log2 n, plus 7 flops per point for the shift generator 1/(s_j + mu); per
+    stored mode 8 flops per level (Re(gamma^-1 X) * ghat and the two residue
+    norms). 2D/3D: one FFT serves a mirror pair of modes (k1 <-> k2)."""
+    import math
+    modes = m ** dim
+    ffts = modes if dim == 1 else (m * (m + 1) // 2) * (m ** (dim - 2))
+    return ffts * (5.0 * n * math.log2(n) + 7.0 * n) + modes * 8.0 * n
 
 
 class ClockSampler:
@@ -274,26 +297,51 @@ def main():
         phase_ms /= args.steps
         names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"]
         if wax:
-            names += [f"k_dst_wax W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]
+            names += [("k_dst_wax2" if w.num_cells == 512 else "k_dst_wax") + f" W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]
             names += [f"k_dst_blk3 level pass (axis -1, W -> y)" if w.num_cells == 512 else "k_dst_blk2 level pass (axis -1, W -> y)"]
         else:
             names += [("k_dst_blk2" if a == 0 else "k_dst_cols3") + f" level pass {a} (axis -{a + 1})"
                       for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
-        # algorithmic bytes per launch of each kernel
+        # algorithmic bytes per launch of each kernel (DESIGN.md 3.4)
         dof = w.dof
         alg_bytes = [16.0 * nx, 8.0 * dof + 8.0 * nx] + [16.0 * dof] * w.dim
         hbm, peak_kind = peaks()
-        achieved = alg_bytes[dom] / (phase_ms[dom] * 1e-3) / 1e9
-        # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
-        traffic = None
+        # DRAM bytes per launch of each kernel from the committed ncu --set full capture
         tfile = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
-        if tfile.exists():
-            tmap = json.loads(tfile.read_text())
-            short = names[dom].split()[0]
+        tmap = json.loads(tfile.read_text()) if tfile.exists() else {}
+
+        def traffic_of(name):
+            short = name.split()[0]
             for key, val in tmap.items():
-                if key.split("::")[-1] == short:
-                    traffic = val
+                if key.split("::")[-1].split("<")[0] == short:
+                    return val
+            return None
+
+        kernels = []
+        for i, nm in enumerate(names):
+            gbs = alg_bytes[i] / (phase_ms[i] * 1e-3) / 1e9
+            kernels.append({"kernel": nm, "ms": float(phase_ms[i]), "alg_bytes": alg_bytes[i],
+                            "achieved_GBps": gbs, "hbm_frac": gbs / hbm, "traffic": traffic_of(nm)})
+        # the dominant HBM-bound kernel (the level passes); pass A is FP64-bound
+        mem_idx = [i for i in range(2, len(names))]
+        mdom = max(mem_idx, key=lambda i: phase_ms[i])
+        roof_hbm = {"bound": "hbm", "kernel": names[mdom], "achieved": kernels[mdom]["achieved_GBps"], "peak": hbm,
+                    "unit": "GB/s", "frac": kernels[mdom]["hbm_frac"], "traffic": kernels[mdom]["traffic"],
+                    "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes[mdom]}
+        if dom == 1:
+            fpk, fpk_kind = fp64_peak()
+            flops = modes_alg_flops(w.dim, w.num_cells - 1, n)
+            tf = flops / (phase_ms[1] * 1e-3) / 1e12
+            roofline = {"bound": "fp64", "kernel": names[1], "achieved": tf, "peak": fpk, "unit": "TFLOP/s",
+                        "frac": tf / fpk, "traffic": kernels[1]["traffic"], "peak_source": fpk_kind,
+                        "alg_flops_per_launch": flops,
+                        "hbm": {"achieved": kernels[1]["achieved_GBps"], "frac": kernels[1]["hbm_frac"],
+                                "alg_bytes_per_launch": alg_bytes[1]},
+                        "note": "pass A is the dominant kernel and is FP64-bound (one n-point time FFT per mirror "
+                                "pair of modes, 8 B/DOF written); roofline_hbm is the dominant HBM-bound kernel"}
+        else:
+            roofline = roof_hbm
         ms_per_step = total_ms / args.steps
         value = dof / (ms_per_step * 1e-3)
 
@@ -353,11 +401,11 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config construction)",
             "config": {"workload": f"{args.config}: 2D pint-mqbvm, 511^2 interior x 513 levels, alpha=1e-2",
                        "dof_per_solve": dof, "l2": "working set (W + y = 2.1 GB) larger than L2; no flush",
-                       "timing": "K replays of the CUDA graph of one step (7 kernels); phases_ms from an eager "
+                       "timing": f"K replays of the CUDA graph of one step ({launches_per_step} kernels); phases_ms from an eager "
                                  "pass of the same K steps with CUDA events"},
-            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": peak_kind,
-                         "alg_bytes_per_launch": alg_bytes[dom]},
+            "roofline": roofline,
+            "roofline_hbm": roof_hbm,
+            "kernels": kernels,
             "phases_ms": {nm: float(t) for nm, t in zip(names, phase_ms)},
             "pipeline_72B_per_dof": {"achieved_GBps": 72.0 * dof / (ms_per_step * 1e-3) / 1e9,
                                      "frac": 72.0 * dof / (ms_per_step * 1e-3) / 1e9 / hbm,

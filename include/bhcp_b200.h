@@ -209,7 +209,7 @@ int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, 
  *   place on the blocked W of `nlev` levels (single-slab layout, or a receive
  *   buffer whose k1 blocks sit at the uniform stride NT * m^(dim-1) * 8, which
  *   is what the slab layouts produce). TMA tensor loads/stores; needs dim 2/3
- *   and m + 1 in {256, 512, 1024} (bhcp_pint_w_passes_supported), W 16-byte
+ *   and m + 1 in {256, 512} (bhcp_pint_w_passes_supported), W 16-byte
  *   aligned.
  * bhcp_pint_levels / bhcp_pint_levels_blocked: all spatial passes, W (or the
  *   receive buffer) -> y. When bhcp_pint_w_passes_supported, the strided axes

@@ -828,7 +828,6 @@ void set_all_attributes() {
   allow_smem(gdst::k_dst_cols3<512>);
   allow_smem(gdst::k_dst_cols3<1024>);
   allow_smem(wax::k_dst_wax<wax::PlanWX<256>>);
-  allow_smem(wax::k_dst_wax<wax::PlanWX<1024>>);
   allow_smem(wax2::k_dst_wax2<512>);
   allow_smem(wax2::k_dst_blk3<512>);
 
@@ -1525,9 +1524,13 @@ int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long
   return BHCP_OK;
 }
 
+// Strided axes on W (k_dst_wax / k_dst_wax2) for m + 1 = 256 (c4) and 512 (c2).
+// m + 1 = 1024 (c3) keeps the y-side strided pass k_dst_cols3: with a 64 KB
+// tile budget its W tiles would have 64 B rows (8 lines), measured 7.45 ms
+// against 6.5 ms for k_dst_cols3.
 bool wax_ok(const bhcp_space_plan* sp) {
   const int L = 2 * (sp->m + 1);
-  return !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && (L == 512 || L == 1024 || L == 2048);
+  return !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && (L == 512 || L == 1024);
 }
 
 // In-place inverse DST of the blocked W (single-slab layout with NT level
@@ -1548,7 +1551,6 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
   switch (m + 1) {
     case 256: return wax_launch<wax::PlanWX<256>>(sp, W, Li, No, nlev, lpl, s);
     case 512: return wax2_launch<512>(sp, W, Li, No, nlev, lpl, s);   // warp per line pair (wax2_dst.cuh)
-    case 1024: return wax_launch<wax::PlanWX<1024>>(sp, W, Li, No, nlev, lpl, s);
   }
   return fail(BHCP_ERR_INVALID, "w_pass length");
 }

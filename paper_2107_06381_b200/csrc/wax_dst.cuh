@@ -69,10 +69,11 @@ struct CfgWX {
   template <class Lay> using F = Fft<N_, S_, T_, Lay, R1_, R2_, R3_>;
 };
 // Measured on c2 (N = 512): 128 B rows beat 64 B rows (0.53 vs 0.73-0.85 ms);
-// N = 512 now runs the warp-per-line-pair k_dst_wax2 (wax2_dst.cuh, 0.45 ms).
+// N = 512 now runs the warp-per-line-pair k_dst_wax2 (wax2_dst.cuh, 0.45 ms),
+// N = 1024 (c3) the y-side k_dst_cols3 (64 B rows here: 7.45 vs 6.5 ms).
+// N = 256 (c4): 32-line tiles (256 B rows), 17.8 ms per axis vs 20-22 ms.
 template <int N> struct PlanWX;
 template <> struct PlanWX<256> : CfgWX<256, 16, 512, 3, 1, 4, 8, 8> {};
-template <> struct PlanWX<1024> : CfgWX<1024, 4, 512, 3, 1, 8, 8, 16> {};
 
 constexpr int kBoxRows = 256;   // TMA box height (<= 256)
 

@@ -12,5 +12,5 @@ python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $out/bench_short_full.j
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches_full_bench.csv \
       python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $out/ncu_launch_full.log 2>&1; echo "ncu launches full rc=$?" | tee -a $out/rc.txt
 python tools/profile_step.py c2 1 > $out/profile_step.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"k_dst_blk2|k_modes_fast|k_dst_cols3" -s 4 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:"k_dst_blk3|k_modes_fast|k_dst_wax2" -s 3 -c 3 \
       -o $out/c2_full -f python tools/profile_step.py c2 2 > $out/ncu_full.log 2>&1; echo "ncu full rc=$?" | tee -a $out/rc.txt
