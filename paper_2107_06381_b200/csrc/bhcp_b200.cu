@@ -830,6 +830,7 @@ void set_all_attributes() {
   allow_smem(wax::k_dst_wax<wax::PlanWX<256>>);
   allow_smem(wax2::k_dst_wax2<512>);
   allow_smem(wax2::k_dst_blk3<512>);
+  allow_smem(wax2::k_dst_blk3<256>);
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
@@ -1404,7 +1405,7 @@ int level_pass(const bhcp_space_plan* sp, const double* in, const long long* kof
   const long long P1 = ipow(m, d - 1);
   if (pass >= 1)
     return launch_cols(sp, y, y, 0, ipow(m, pass), nlev * ipow(m, d - 1 - pass), pass, 0, nullptr, nullptr, s);
-  if (!g_disable_fast && L == 1024 && d <= 3 && !koff) return blk3_launch(sp, in, y, nlev, s);
+  if (!g_disable_fast && (L == 512 || L == 1024) && d <= 3 && !koff) return blk3_launch(sp, in, y, nlev, s);
   if (!g_disable_fast && (L == 512 || L == 1024 || L == 2048)) {
     gdst::ArgsB2 b{};
     b.in = in; b.out = y; b.tw = sp->twN; b.sn = sp->snN; b.scale = sqrt(2.0 / (m + 1));
@@ -1500,9 +1501,9 @@ int wax2_launch(const bhcp_space_plan* sp, double* W, long long Li, long long No
   return BHCP_OK;
 }
 
-// last spatial axis, blocked W -> y, N = 512 (k_dst_blk3, wax2_dst.cuh)
-int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s) {
-  constexpr int N = 512;
+// last spatial axis, blocked W -> y, N = m + 1 in {256, 512} (k_dst_blk3, wax2_dst.cuh)
+template <int N>
+int blk3_launch_n(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s) {
   const long long m = sp->m, d = sp->dim;
   const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
   const long long idiv = ipow(m, d - 2);
@@ -1522,6 +1523,14 @@ int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long
   wax2::k_dst_blk3<N><<<(unsigned)grid, threads, sm, s>>>(tm, a);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk3 launch");
   return BHCP_OK;
+}
+
+int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s) {
+  switch (sp->m + 1) {
+    case 256: return blk3_launch_n<256>(sp, W, y, nlev, s);
+    case 512: return blk3_launch_n<512>(sp, W, y, nlev, s);
+  }
+  return fail(BHCP_ERR_INVALID, "blk3 length");
 }
 
 // Strided axes on W (k_dst_wax / k_dst_wax2) for m + 1 = 256 (c4) and 512 (c2).
@@ -1549,6 +1558,8 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
   if (axis == 0) { Li = NT * P1 * fastk::kTBL; No = 1; lpl = P1 * fastk::kTBL; }
   else { Li = ipow(m, d - 1 - axis) * fastk::kTBL; No = m * NT * ipow(m, axis - 1); lpl = 0; }
   switch (m + 1) {
+    // N = 256 (c4): the CTA-synchronous 32-line tiles (256 B rows) measured faster than
+    // k_dst_wax2<256> with 16-line tiles (17.8 / 17.5 vs 19.4 / 18.3 ms per axis)
     case 256: return wax_launch<wax::PlanWX<256>>(sp, W, Li, No, nlev, lpl, s);
     case 512: return wax2_launch<512>(sp, W, Li, No, nlev, lpl, s);   // warp per line pair (wax2_dst.cuh)
   }
@@ -1566,7 +1577,7 @@ int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, doub
       int rc = w_pass(sp, W, nlev, a, s);
       if (rc) return rc;
     }
-    if (sp->m + 1 == 512) return blk3_launch(sp, W, y, nlev, s);   // k1 blocks at the uniform stride
+    return blk3_launch(sp, W, y, nlev, s);   // k1 blocks at the uniform stride
     return level_pass(sp, W, koff, y, nlev, 0, s);
   }
   for (int p = 0; p < sp->dim; ++p) {

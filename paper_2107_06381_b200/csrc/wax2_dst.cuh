@@ -39,11 +39,12 @@ using wax::tma_load3;
 using wax::tma_store3;
 
 constexpr int kCW = 8;      // consumer warps = line pairs per tile
-constexpr int kNBUF = 3;    // tile buffers
 constexpr int kLW = 16;     // lines per tile (128 B rows)
 
+// tile buffers: 192 KB of 16-line tiles (N * 128 bytes each)
+template <int N> constexpr int nbuf_wax() { return (192 * 1024) / (N * 128); }
 template <int N> constexpr size_t smem_bytes() {
-  return 1024 /* alignment slack */ + (size_t)kNBUF * N * 128 + sizeof(double) * N + 16 * kNBUF;
+  return 1024 /* alignment slack */ + (size_t)nbuf_wax<N>() * N * 128 + sizeof(double) * N + 16 * nbuf_wax<N>();
 }
 
 // try_wait with a suspend-time hint: the thread sleeps in hardware until the
@@ -262,10 +263,187 @@ __device__ __forceinline__ void warp_dst512(double2* T, int q, const LaneK& K, c
     }
 }
 
+// Per-lane constants of warp_dst256 (N = 256 = 4^4, four radix-4 stages).
+struct LaneK256 {
+  int u, j1, j2;          // lane; butterflies of stages 1 and 4 (u, 64 - u; lane 0: 0, 32)
+  double2 w2, w3, w4a, w4b;   // stage twiddles w^(16 (j%4)), w^(4 (j%16)), w^j1, w^j2
+  double mup[5], mdn[5];
+  double scale;
+  __device__ __forceinline__ LaneK256(int lane, const double2* tw, double sc) {
+    u = lane; j1 = lane; j2 = lane == 0 ? 32 : 64 - lane;
+    w2 = __ldg(tw + 16 * (lane & 3));
+    w3 = __ldg(tw + 4 * (lane & 15));
+    w4a = __ldg(tw + j1); w4b = __ldg(tw + j2);
+    scale = sc;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      mup[s] = lane >= (1 << s) ? 1.0 : 0.0;
+      mdn[s] = lane + (1 << s) < 32 ? 1.0 : 0.0;
+    }
+  }
+};
+
+// N = 256 version of warp_dst512: pre-step + four radix-4 Stockham stages
+// (butterfly j reads j + 64 r, writes (j - j%Ns) 4 + j%Ns + Ns r) + split.
+// Stage 1 and 4 pair butterflies u / 64 - u as before. Two in-octet row
+// permutations keep stages 1 -> 2 and 2 -> 3 conflict-free:
+//   after stage 1: index i at row (i & ~7) | ((i & 7) ^ ((i >> 3) & 3))
+//   after stage 2: index i at row (i & ~7) | ((i & 7) ^ (((i >> 4) & 1) << 2))
+// Output e (scaled) ends in row e, through the sink.
+__device__ __forceinline__ int perm1(int i) { return (i & ~7) | ((i & 7) ^ ((i >> 3) & 3)); }
+__device__ __forceinline__ int perm2(int i) { return (i & ~7) | ((i & 7) ^ (((i >> 4) & 1) << 2)); }
+
+template <class L, class Sink>
+__device__ __forceinline__ void warp_dst256(double2* T, int q, const LaneK256& K, const double* sn, Sink& sink) {
+  constexpr int N = 256;
+  constexpr int R64 = 64 * L::RS;
+  const int u = K.u, j1 = K.j1, j2 = K.j2, lane = u;
+  const double scale = K.scale;
+  double2 A[4], B[4];
+  {
+    // ---- stage 1 inputs: x_i (row i - 1) for i = j1 + 64 r, j2 + 64 r; lane 0's x_0
+    // from row N - 1 (zero-filled by the TMA unit)
+    double2 xa[4], xb[4];
+    const double2* pa0 = at<L>(T, u == 0 ? N - 1 : j1 - 1, q);
+    const double2* pa1 = at<L>(T, j1 + 63, q) - R64;
+    const double2* pb = at<L>(T, j2 - 1, q);
+    xa[0] = *pa0;
+#pragma unroll
+    for (int r = 1; r < 4; ++r) xa[r] = pa1[R64 * r];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) xb[r] = pb[R64 * r];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      // partner of j1 + 64 r: u >= 1 -> j2 + 64 (3 - r); u == 0 -> j1 + 64 (4 - r) (mod N)
+      const double2 pa = u == 0 ? xa[(4 - r) & 3] : xb[3 - r];
+      const double2 pb2 = u == 0 ? xb[3 - r] : xa[3 - r];
+      const double sa = sn[j1 + 64 * r], sb = sn[j2 + 64 * r];
+      A[r] = make_double2(fma(sa, xa[r].x + pa.x, 0.5 * (xa[r].x - pa.x)), fma(sa, xa[r].y + pa.y, 0.5 * (xa[r].y - pa.y)));
+      B[r] = make_double2(fma(sb, xb[r].x + pb2.x, 0.5 * (xb[r].x - pb2.x)), fma(sb, xb[r].y + pb2.y, 0.5 * (xb[r].y - pb2.y)));
+    }
+  }
+  Cod<4>::run(A);
+  Cod<4>::run(B);
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    *at<L>(T, perm1(4 * j1 + r), q) = A[r];
+    *at<L>(T, perm1(4 * j2 + r), q) = B[r];
+  }
+  __syncwarp();
+  // ---- stage 2 (Ns = 4) and stage 3 (Ns = 16): butterflies j = lane, lane + 32
+  {
+    double2 v[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      // index j + 64 r: (i >> 3) & 3 and i & 7 do not depend on r
+      const double2* p = at<L>(T, perm1(j), q);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[h][r] = p[R64 * r];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      apply_twiddles<4>(v[h], K.w2);
+      Cod<4>::run(v[h]);
+      const int base = 16 * (j >> 2) + (j & 3);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) *at<L>(T, perm2(base + 4 * r), q) = v[h][r];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      const double2* p = at<L>(T, perm2(j), q);   // (i >> 4) & 1 and i & 7 do not depend on r
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v[h][r] = p[R64 * r];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = lane + 32 * h;
+      apply_twiddles<4>(v[h], K.w3);
+      Cod<4>::run(v[h]);
+      double2* p = at<L>(T, 64 * (j >> 4) + (j & 15), q);   // rows base + 16 r: key fixed
+#pragma unroll
+      for (int r = 0; r < 4; ++r) p[16 * L::RS * r] = v[h][r];
+    }
+  }
+  __syncwarp();
+  // ---- stage 4 (Ns = 64): butterflies j1, j2, outputs U_{j + 64 r}
+  {
+    const double2* pa = at<L>(T, j1, q);
+    const double2* pb = at<L>(T, j2, q);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      A[r] = pa[R64 * r];
+      B[r] = pb[R64 * r];
+    }
+  }
+  apply_twiddles<4>(A, K.w4a);
+  apply_twiddles<4>(B, K.w4b);
+  Cod<4>::run(A);
+  Cod<4>::run(B);
+  __syncwarp();
+  // ---- split (k < N/2: blocks r = 0, 1; lo k = j1 + 64 r, hi k = j2 + 64 r)
+  const double2 U0 = make_double2(__shfl_sync(0xffffffffu, A[0].x, 0), __shfl_sync(0xffffffffu, A[0].y, 0));
+  double offa = -0.5 * U0.x, offb = -0.5 * U0.y;
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const double2 P = A[r], Q = u == 0 ? A[(4 - r) & 3] : B[3 - r];
+    const double2 Ph = B[r], Qh = u == 0 ? B[3 - r] : A[3 - r];
+    double la = 0.5 * (P.x + Q.x), lb = 0.5 * (P.y + Q.y);
+    double ha = 0.5 * (Ph.x + Qh.x), hb = 0.5 * (Ph.y + Qh.y);
+    const double ela = -0.5 * (P.y - Q.y), elb = 0.5 * (P.x - Q.x);
+    const double eha = -0.5 * (Ph.y - Qh.y), ehb = 0.5 * (Ph.x - Qh.x);
+    const double h0a = __shfl_sync(0xffffffffu, ha, 0), h0b = __shfl_sync(0xffffffffu, hb, 0);
+    if (u == 0) { ha = 0.0; hb = 0.0; }
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int off = 1 << s;
+      const double va = __shfl_up_sync(0xffffffffu, la, off), vb = __shfl_up_sync(0xffffffffu, lb, off);
+      const double wa = __shfl_down_sync(0xffffffffu, ha, off), wb = __shfl_down_sync(0xffffffffu, hb, off);
+      la = fma(K.mup[s], va, la);
+      lb = fma(K.mup[s], vb, lb);
+      ha = fma(K.mdn[s], wa, ha);
+      hb = fma(K.mdn[s], wb, hb);
+    }
+    const double tla = __shfl_sync(0xffffffffu, la, 31), tlb = __shfl_sync(0xffffffffu, lb, 31);
+    const double tha = __shfl_sync(0xffffffffu, ha, 0), thb = __shfl_sync(0xffffffffu, hb, 0);
+    const double mida = tla + h0a, midb = tlb + h0b;
+    const double oloa = offa + la, olob = offb + lb;
+    const double ohia = offa + mida + (u == 0 ? 0.0 : ha), ohib = offb + midb + (u == 0 ? 0.0 : hb);
+    offa += mida + tha;
+    offb += midb + thb;
+    sink.put(r, false, u, make_double2(scale * ela, scale * elb), make_double2(scale * oloa, scale * olob));
+    sink.put(r, true, u, make_double2(scale * eha, scale * ehb), make_double2(scale * ohia, scale * ohib));
+  }
+}
+
+// per-N dispatch of the column DST
+template <int N> struct ColDst;
+template <> struct ColDst<512> {
+  using K = LaneK;
+  template <class L, class Sink>
+  static __device__ __forceinline__ void run(double2* T, int q, const K& k, const double* sn, Sink& s) {
+    warp_dst512<L>(T, q, k, sn, s);
+  }
+};
+template <> struct ColDst<256> {
+  using K = LaneK256;
+  template <class L, class Sink>
+  static __device__ __forceinline__ void run(double2* T, int q, const K& k, const double* sn, Sink& s) {
+    warp_dst256<L>(T, q, k, sn, s);
+  }
+};
+
 template <int N>
 __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_wax2(const __grid_constant__ CUtensorMap tm,
                                                                  wax::ArgsWX a) {
-  static_assert(N == 512, "three radix-8 stages");
+  static_assert(N == 512 || N == 256, "column DST lengths");
+  constexpr int kNBUF = nbuf_wax<N>();
   constexpr int NBOX = N / wax::kBoxRows;
   constexpr unsigned TILE_BYTES = (unsigned)(N * kLW * sizeof(double));
   extern __shared__ unsigned char smem_raw[];
@@ -326,7 +504,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_wax2(const __grid_con
 
   // -------------------------------------------------------------- consumers
   const int q = warp;   // line pair (lines 2q, 2q+1) of every tile
-  const LaneK K(lane, a.tw, a.scale);
+  const typename ColDst<N>::K K(lane, a.tw, a.scale);
   // tile = blockIdx.x + it * G as (outer o, chunk c), advanced incrementally
   const int dG_o = G / a.lchunks, dG_c = G - dG_o * a.lchunks;
   int to = (int)blockIdx.x / a.lchunks, tc = (int)blockIdx.x - to * a.lchunks;
@@ -354,7 +532,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_wax2(const __grid_con
       }
     }
     ColumnSink<Sw128> sink(T, q, K.u, K.j1, K.j2);
-    warp_dst512<Sw128>(T, q, K, sn, sink);
+    ColDst<N>::template run<Sw128>(T, q, K, sn, sink);
     // hand the buffer to the producer (its TMA store reads it through the async proxy)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
@@ -403,14 +581,16 @@ struct RowSink {
   }
 };
 
-constexpr int kB3Buf = 6;
+// tile buffers: 192 KB of W blocks (N * 64 bytes each)
+template <int N> constexpr int nbuf_b3() { return (192 * 1024) / (N * 64); }
 template <int N> constexpr size_t smem_bytes_b3() {
-  return 1024 + (size_t)kB3Buf * N * 64 + sizeof(double) * N + 16 * kB3Buf;
+  return 1024 + (size_t)nbuf_b3<N>() * N * 64 + sizeof(double) * N + 16 * nbuf_b3<N>();
 }
 
 template <int N>
 __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_constant__ CUtensorMap tm, ArgsB3 a) {
-  static_assert(N == 512, "three radix-8 stages");
+  static_assert(N == 512 || N == 256, "column DST lengths");
+  constexpr int kB3Buf = nbuf_b3<N>();
   constexpr int NBOX = N / wax::kBoxRows;
   constexpr unsigned TILE_BYTES = (unsigned)(N * 8 * sizeof(double));
   constexpr int TD2 = N * 4;   // double2 per tile
@@ -446,7 +626,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_con
     return;
   }
   const int q = warp & 3, grp = warp >> 2;
-  const LaneK K(lane, a.tw, a.scale);
+  const typename ColDst<N>::K K(lane, a.tw, a.scale);
   const int m = a.m;
   for (int it = grp; it < ntiles_cta; it += 2) {
     const int b = it % kB3Buf;
@@ -472,7 +652,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_con
     const long long rowa = ((long long)((long long)t0 * m + k1) * a.idiv + r2) * m;
     const long long rowb = rowa + (long long)m * m * a.idiv;
     RowSink sink{a.y + rowa, a.y + rowb, t0 < a.nlev, t0 + 1 < a.nlev, K.j1, K.j2};
-    warp_dst512<Sw64>(T, q, K, sn, sink);
+    ColDst<N>::template run<Sw64>(T, q, K, sn, sink);
     if (lane == 0) mbar_arrive_relaxed(done + b);
   }
 }
