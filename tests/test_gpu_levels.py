@@ -1,0 +1,118 @@
+"""Device parity of the spatial level passes of the fused solve (B200 only).
+
+The fused solve ends with y[t, :] = Phi W[t, :] (pint.py:94-99 with the
+inverse DST moved after the time transform). For m + 1 in
+{256, 512} the strided axes run in place on the blocked W (k_dst_wax /
+k_dst_wax2, TMA tiles) and the last axis moves W -> y (k_dst_blk3). These
+tests feed seeded random blocked W -- with NaN in the padding levels of the
+last level tile, which pass A never writes -- through every entry point that
+runs those kernels and compare with the oracle's orthonormal DST
+(oracle.fused_pass_b, scipy.fft.dst type 1) at 1e-13 relative L2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2107_06381_b200 as B
+from oracle import bhcp_oracle as O
+from paper_2107_06381_b200 import _lib, plans
+from paper_2107_06381_b200.space import plan_for
+
+pytestmark = pytest.mark.gpu
+
+TB = 8   # levels per W block (fastk::kTBL)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def blocked(F, dim, m):
+    """Level-major F (L, m^dim) -> blocked W (k1, level tile, rest, 8 levels), NaN padding."""
+    L = F.shape[0]
+    nt = (L + TB - 1) // TB
+    P1 = m ** (dim - 1)
+    W = np.full((m, nt, P1, TB), np.nan)
+    Fr = F.reshape(L, m, P1)
+    for t in range(L):
+        W[:, t // TB, :, t % TB] = Fr[t]
+    return W.reshape(-1)
+
+
+def run_levels(sp, W_host, L, dim, m, how):
+    lib = _lib.lib()
+    sh = plans.stream_handle()
+    W = torch.from_numpy(W_host).cuda()
+    y = torch.full((L, m ** dim), np.nan, dtype=torch.float64, device="cuda")
+    if how == "levels":
+        _lib.check(lib.bhcp_pint_levels(sp, plans.ptr(W), plans.ptr(y), L, sh), "levels")
+    elif how == "passes":
+        # the bench's phase-by-phase order: strided axes on W, then the last axis
+        for a in range(dim - 1):
+            _lib.check(lib.bhcp_pint_w_pass(sp, plans.ptr(W), L, a, sh), "w pass")
+        _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, 0, sh), "level pass 0")
+    else:
+        # an all-to-all receive buffer: k1 blocks at koff[k1] (block_tables' uniform stride)
+        nt = (L + TB - 1) // TB
+        koff = torch.arange(m, dtype=torch.int64, device="cuda") * (nt * m ** (dim - 1) * TB)
+        _lib.check(lib.bhcp_pint_levels_blocked(sp, plans.ptr(W), plans.ptr(koff), plans.ptr(y), L, sh),
+                   "levels_blocked")
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("dim,cells,L", [(2, 512, 1), (2, 512, 7), (2, 512, 8), (2, 512, 9), (2, 512, 13),
+                                         (2, 512, 16), (2, 256, 5), (2, 256, 8), (2, 256, 11), (3, 256, 1),
+                                         (3, 256, 3)])
+def test_level_passes_vs_oracle(dim, cells, L):
+    grid = B.build_grid(dim, 1.0, cells)
+    m = cells - 1
+    plan = plan_for(grid)
+    lib = _lib.lib()
+    assert lib.bhcp_pint_w_passes_supported(plan.handle) == 1
+    rng = np.random.default_rng(1000 * dim + 10 * cells + L)
+    F = rng.standard_normal((L, m ** dim))
+    ref = O.fused_pass_b(F, dim, m)
+    W = blocked(F, dim, m)
+    y = run_levels(plan.handle, W, L, dim, m, "levels")
+    assert np.isfinite(y).all(), "padding NaN leaked into a valid level"
+    err = rel(y, ref)
+    assert err <= 1e-13, f"rel-L2 {err:.2e}"
+    # the same kernels driven pass by pass (bench order) and through the
+    # all-to-all receive-buffer entry point give the same bits
+    assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "passes"), y)
+    assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "blocked"), y)
+
+
+@pytest.mark.parametrize("dim,cells", [(2, 512), (3, 256)])
+def test_w_pass_single_axis_vs_oracle(dim, cells):
+    """bhcp_pint_w_pass alone: the DST along spatial axis a of every level, in place on W."""
+    import scipy.fft as sf
+
+    grid = B.build_grid(dim, 1.0, cells)
+    m = cells - 1
+    plan = plan_for(grid)
+    lib = _lib.lib()
+    L = 10 if dim == 2 else 2
+    rng = np.random.default_rng(7 + dim)
+    F = rng.standard_normal((L, m ** dim))
+    for a in range(dim - 1):
+        W = torch.from_numpy(blocked(F, dim, m)).cuda()
+        _lib.check(lib.bhcp_pint_w_pass(plan.handle, plans.ptr(W), L, a, plans.stream_handle()), "w pass")
+        torch.cuda.synchronize()
+        nt = (L + TB - 1) // TB
+        Wd = W.cpu().numpy().reshape(m, nt, m ** (dim - 1), TB)
+        got = np.stack([Wd[:, t // TB, :, t % TB].reshape(-1) for t in range(L)])
+        ref = sf.dst(F.reshape((L,) + (m,) * dim), type=1, norm="ortho", axis=1 + a).reshape(L, -1)
+        assert rel(got, ref) <= 1e-13
+
+
+def test_w_pass_rejects_unsupported():
+    lib = _lib.lib()
+    plan = plan_for(B.build_grid(2, 1.0, 1024))   # c3 keeps the y-side strided pass
+    assert lib.bhcp_pint_w_passes_supported(plan.handle) == 0
+    W = torch.zeros(8 * 1023 * 1023, dtype=torch.float64, device="cuda")
+    assert lib.bhcp_pint_w_pass(plan.handle, plans.ptr(W), 1, 0, plans.stream_handle()) == _lib.BHCP_ERR_INVALID
+    plan2 = plan_for(B.build_grid(2, 1.0, 512))
+    assert lib.bhcp_pint_w_pass(plan2.handle, plans.ptr(W), 1, 1, plans.stream_handle()) == _lib.BHCP_ERR_INVALID
