@@ -121,21 +121,21 @@ struct LaneK {
 // pre-step + three radix-8 Stockham stages + even/odd split with the
 // odd-output prefix sum. Output e (scaled) is left in row e.
 // Default output sink: rows 2k - 1 / 2k of the column (conflict-free order).
-template <class L>
+template <class L, int KS = 64>
 struct ColumnSink {
   double2 *lo_ev, *lo_od, *hi_ev, *hi_od;
-  __device__ __forceinline__ ColumnSink(double2* T, int q, int u, int j1, int j2) {
-    // output rows 2k - 1, 2k of k = j + 64 r: chunk independent of r (rows step 128)
-    lo_ev = at<L>(T, u == 0 ? 127 : 2 * j1 - 1, q) - (u == 0 ? 128 * L::RS : 0);   // lane 0: row 128 r - 1 (r >= 1)
+  __device__ __forceinline__ ColumnSink(double2* T, int q, int v, int j1, int j2) {
+    // output rows 2k - 1, 2k of k = j + KS r: chunk independent of r (rows step 2 KS)
+    lo_ev = at<L>(T, v == 0 ? 2 * KS - 1 : 2 * j1 - 1, q) - (v == 0 ? 2 * KS * L::RS : 0);   // unit 0: row 2 KS r - 1 (r >= 1)
     lo_od = at<L>(T, 2 * j1, q);
     hi_ev = at<L>(T, 2 * j2 - 1, q);
     hi_od = at<L>(T, 2 * j2, q);
   }
-  // k = j1 + 64 r (hi = false) or j2 + 64 r (hi = true); ev = S_{2k} -> element 2k - 1, od = S_{2k+1} -> 2k
-  __device__ __forceinline__ void put(int r, bool hi, int u, double2 ev, double2 od) {
-    const bool sw = (u & 4) != 0;
-    if (!hi) store_pair(sw, lo_ev + 128 * L::RS * r, ev, lo_od + 128 * L::RS * r, od, (u | r) != 0);
-    else store_pair(sw, hi_ev + 128 * L::RS * r, ev, hi_od + 128 * L::RS * r, od, true);
+  // k = j1 + KS r (hi = false) or j2 + KS r (hi = true); ev = S_{2k} -> element 2k - 1, od = S_{2k+1} -> 2k
+  __device__ __forceinline__ void put(int r, bool hi, int v, double2 ev, double2 od) {
+    const bool sw = (v & 4) != 0;
+    if (!hi) store_pair(sw, lo_ev + 2 * KS * L::RS * r, ev, lo_od + 2 * KS * L::RS * r, od, (v | r) != 0);
+    else store_pair(sw, hi_ev + 2 * KS * L::RS * r, ev, hi_od + 2 * KS * L::RS * r, od, true);
   }
 };
 
@@ -422,6 +422,161 @@ __device__ __forceinline__ void warp_dst256(double2* T, int q, const LaneK256& K
   }
 }
 
+// ---------------------------------------------------------------------------
+// N = 1024 (c3): the column is 1024 rows, too many for one warp's registers at
+// the in-place read-all / write-all points, so TWO warps share a line pair.
+// Unit v = 32 h + lane (h = warp half) owns butterflies v and 128 - v (unit 0:
+// 0 and 64) in the radix-8 stages 1 and 3 (stride 128) and butterfly v in the
+// radix-16 stage 2; the two warps meet at a 64-thread named barrier around
+// every in-place write and exchange block totals for the prefix sum.
+struct LaneK1024 {
+  int u, v, j1, j2;
+  double2 w2, w3a, w3b;   // w^(8 (v%8)), w^j1, w^j2
+  double mup[5], mdn[5];
+  double scale;
+  __device__ __forceinline__ LaneK1024(int lane, int h, const double2* tw, double sc) {
+    u = lane; v = 32 * h + lane; j1 = v; j2 = v == 0 ? 64 : 128 - v;
+    w2 = __ldg(tw + 8 * (v & 7));
+    w3a = __ldg(tw + j1); w3b = __ldg(tw + j2);
+    scale = sc;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      mup[s] = lane >= (1 << s) ? 1.0 : 0.0;
+      mdn[s] = lane + (1 << s) < 32 ? 1.0 : 0.0;
+    }
+  }
+};
+
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
+
+// xch: 42 doubles per line pair (block totals and U_0 exchanged between the two warps)
+template <class L, class Sink>
+__device__ __forceinline__ void warp_dst1024(double2* T, int q, int h, const LaneK1024& K, const double* sn,
+                                             double* xch, int bar, Sink& sink) {
+  constexpr int N = 1024;
+  constexpr int R128 = 128 * L::RS, R64 = 64 * L::RS;
+  const int u = K.u, v = K.v, j1 = K.j1, j2 = K.j2;
+  const double scale = K.scale;
+  double2 A[8], B[8];
+  {
+    double2 xa[8], xb[8];
+    const double2* pa0 = at<L>(T, v == 0 ? N - 1 : j1 - 1, q);
+    const double2* pa1 = at<L>(T, j1 + 127, q) - R128;
+    const double2* pb = at<L>(T, j2 - 1, q);
+    xa[0] = *pa0;
+#pragma unroll
+    for (int r = 1; r < 8; ++r) xa[r] = pa1[R128 * r];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) xb[r] = pb[R128 * r];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const double2 pa = v == 0 ? xa[(8 - r) & 7] : xb[7 - r];
+      const double2 pb2 = v == 0 ? xb[7 - r] : xa[7 - r];
+      const double sa = sn[j1 + 128 * r], sb = sn[j2 + 128 * r];
+      A[r] = make_double2(fma(sa, xa[r].x + pa.x, 0.5 * (xa[r].x - pa.x)), fma(sa, xa[r].y + pa.y, 0.5 * (xa[r].y - pa.y)));
+      B[r] = make_double2(fma(sb, xb[r].x + pb2.x, 0.5 * (xb[r].x - pb2.x)), fma(sb, xb[r].y + pb2.y, 0.5 * (xb[r].y - pb2.y)));
+    }
+  }
+  Cod<8>::run(A);
+  Cod<8>::run(B);
+  pair_sync(bar);   // both warps have read their inputs
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    *at<L>(T, 8 * j1 + ((j1 + r) & 7), q) = A[r];
+    *at<L>(T, 8 * j2 + ((j2 + r) & 7), q) = B[r];
+  }
+  pair_sync(bar);
+  // ---- stage 2: radix 16, Ns = 8, butterfly j = v: reads index j + 64 r (rotated rows)
+  {
+    double2 w[16];
+    const int j = v;
+    const double2* p = at<L>(T, 8 * (j >> 3) + (((j >> 3) + (j & 7)) & 7), q);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) w[r] = p[R64 * r];
+    apply_twiddles<16>(w, K.w2);
+    Cod<16>::run(w);
+    pair_sync(bar);
+    double2* o = at<L>(T, 128 * (j >> 3) + (j & 7), q);   // rows base + 8 r: key fixed
+#pragma unroll
+    for (int r = 0; r < 16; ++r) o[8 * L::RS * r] = w[r];
+  }
+  pair_sync(bar);
+  // ---- stage 3: radix 8, Ns = 128: butterflies j1, j2, outputs U_{j + 128 r}
+  {
+    const double2* pa = at<L>(T, j1, q);
+    const double2* pb = at<L>(T, j2, q);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      A[r] = pa[R128 * r];
+      B[r] = pb[R128 * r];
+    }
+  }
+  apply_twiddles<8>(A, K.w3a);
+  apply_twiddles<8>(B, K.w3b);
+  Cod<8>::run(A);
+  Cod<8>::run(B);
+  // ---- split: blocks r = 0..3 of 128 positions; unit v holds position v (lo,
+  // k = j1 + 128 r) and 128 - v (hi, k = j2 + 128 r; unit 0: position 64)
+  double la[4], lb[4], ha[4], hb[4], ela[4], elb[4], eha[4], ehb[4], h0a[4], h0b[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const double2 P = A[r], Q = v == 0 ? A[(8 - r) & 7] : B[7 - r];
+    const double2 Ph = B[r], Qh = v == 0 ? B[7 - r] : A[7 - r];
+    la[r] = 0.5 * (P.x + Q.x); lb[r] = 0.5 * (P.y + Q.y);
+    ha[r] = 0.5 * (Ph.x + Qh.x); hb[r] = 0.5 * (Ph.y + Qh.y);
+    ela[r] = -0.5 * (P.y - Q.y); elb[r] = 0.5 * (P.x - Q.x);
+    eha[r] = -0.5 * (Ph.y - Qh.y); ehb[r] = 0.5 * (Ph.x - Qh.x);
+    h0a[r] = ha[r]; h0b[r] = hb[r];   // unit 0's value is read from warp 0 lane 0 below
+    if (v == 0) { ha[r] = 0.0; hb[r] = 0.0; }
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const int off = 1 << s;
+      const double va = __shfl_up_sync(0xffffffffu, la[r], off), vb = __shfl_up_sync(0xffffffffu, lb[r], off);
+      const double wa = __shfl_down_sync(0xffffffffu, ha[r], off), wb = __shfl_down_sync(0xffffffffu, hb[r], off);
+      la[r] = fma(K.mup[s], va, la[r]);
+      lb[r] = fma(K.mup[s], vb, lb[r]);
+      ha[r] = fma(K.mdn[s], wa, ha[r]);
+      hb[r] = fma(K.mdn[s], wb, hb[r]);
+    }
+  }
+  // exchange: warp h publishes its lo totals (lane 31) and hi totals (lane 0);
+  // warp 0 also publishes unit 0's hi value. xch[h][r][{la, lb, ha, hb}], xch[2][r][{h0a, h0b}]
+  if (u == 31) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) { xch[(h * 4 + r) * 4 + 0] = la[r]; xch[(h * 4 + r) * 4 + 1] = lb[r]; }
+  }
+  if (u == 0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      xch[(h * 4 + r) * 4 + 2] = ha[r]; xch[(h * 4 + r) * 4 + 3] = hb[r];
+      if (h == 0) { xch[32 + r * 2] = h0a[r]; xch[32 + r * 2 + 1] = h0b[r]; }
+    }
+    if (h == 0) { xch[40] = A[0].x; xch[41] = A[0].y; }   // U_0 (unit 0 holds butterfly 0)
+  }
+  pair_sync(bar);   // totals visible; all stage-3 reads of the column done
+  double offa = -0.5 * xch[40], offb = -0.5 * xch[41];   // running block offsets minus Re U_0 / 2
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const double lo0a = xch[(0 * 4 + r) * 4 + 0], lo0b = xch[(0 * 4 + r) * 4 + 1];
+    const double lo1a = xch[(1 * 4 + r) * 4 + 0], lo1b = xch[(1 * 4 + r) * 4 + 1];
+    const double hi0a = xch[(0 * 4 + r) * 4 + 2], hi0b = xch[(0 * 4 + r) * 4 + 3];
+    const double hi1a = xch[(1 * 4 + r) * 4 + 2], hi1b = xch[(1 * 4 + r) * 4 + 3];
+    const double c0a = xch[32 + r * 2], c0b = xch[32 + r * 2 + 1];
+    // prefix through position v (lo): own scan + warp 0's lo total for warp 1
+    const double pla = la[r] + (h ? lo0a : 0.0), plb = lb[r] + (h ? lo0b : 0.0);
+    // prefix through position 64: all lo + unit 0's hi
+    const double mida = lo0a + lo1a + c0a, midb = lo0b + lo1b + c0b;
+    // suffix over units v..63 of hi: own suffix + warp 1's hi total for warp 0
+    const double sha = ha[r] + (h ? 0.0 : hi1a), shb = hb[r] + (h ? 0.0 : hi1b);
+    const double oloa = offa + pla, olob = offb + plb;
+    const double ohia = offa + mida + (v == 0 ? 0.0 : sha), ohib = offb + midb + (v == 0 ? 0.0 : shb);
+    offa += mida + hi0a + hi1a;
+    offb += midb + hi0b + hi1b;
+    sink.put(r, false, v, make_double2(scale * ela[r], scale * elb[r]), make_double2(scale * oloa, scale * olob));
+    sink.put(r, true, v, make_double2(scale * eha[r], scale * ehb[r]), make_double2(scale * ohia, scale * ohib));
+  }
+}
+
 // per-N dispatch of the column DST
 template <int N> struct ColDst;
 template <> struct ColDst<512> {
@@ -562,13 +717,14 @@ struct ArgsB3 {
 
 // Output sink of k_dst_blk3: the two y rows of the line pair, straight from
 // registers (elements 2k - 1 and 2k of every k the lane holds).
+template <int KS = 64>
 struct RowSink {
   double* ya;
   double* yb;
   bool va, vb;
   int j1, j2;
-  __device__ __forceinline__ void put(int r, bool hi, int u, double2 ev, double2 od) {
-    const int k = (hi ? j2 : j1) + 64 * r;
+  __device__ __forceinline__ void put(int r, bool hi, int v, double2 ev, double2 od) {
+    const int k = (hi ? j2 : j1) + KS * r;
     const bool he = k > 0;
     if (va) {
       if (he) ya[2 * k - 1] = ev.x;
@@ -651,9 +807,134 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_con
     // rows of y: level t, spatial line (k1, r2) -> y[((t * m + k1) * idiv + r2) * m + e]
     const long long rowa = ((long long)((long long)t0 * m + k1) * a.idiv + r2) * m;
     const long long rowb = rowa + (long long)m * m * a.idiv;
-    RowSink sink{a.y + rowa, a.y + rowb, t0 < a.nlev, t0 + 1 < a.nlev, K.j1, K.j2};
+    RowSink<> sink{a.y + rowa, a.y + rowb, t0 < a.nlev, t0 + 1 < a.nlev, K.j1, K.j2};
     ColDst<N>::template run<Sw64>(T, q, K, sn, sink);
     if (lane == 0) mbar_arrive_relaxed(done + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// N = 1024 (c3) kernels: 64 B rows (4 line pairs) x 1024 rows = 64 KB tiles,
+// 64-byte swizzle, two warps per line pair (warp w: pair w & 3, half w >> 2),
+// 3 buffers; a producer warp as in k_dst_wax2.
+//   k_dst_q4<true>:  the last axis, W -> y (TMA load, y rows from registers)
+//   k_dst_q4<false>: a strided axis in place on W (TMA load + store); measured
+//                    7.5 ms on c3 against 6.6 ms for k_dst_cols3 on y (64 B rows
+//                    at an 8 MB stride), so the solve does not launch it.
+constexpr int kNB4 = 3;
+constexpr size_t smem_bytes_4() { return 1024 + (size_t)kNB4 * 1024 * 64 + sizeof(double) * (1024 + 4 * 42) + 16 * kNB4; }
+
+template <bool TO_Y>
+__global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_q4(const __grid_constant__ CUtensorMap tm, wax::ArgsWX a,
+                                                            ArgsB3 b3) {
+  constexpr int N = 1024, NBOX = N / wax::kBoxRows, TD2 = N * 4;
+  constexpr unsigned TILE_BYTES = (unsigned)(N * 8 * sizeof(double));
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024 - (su32(smem_raw) & 1023)) & 1023);
+  double2* tiles = reinterpret_cast<double2*>(base);
+  double* sn = reinterpret_cast<double*>(base + (size_t)kNB4 * TD2 * 16);
+  double* xch = sn + N;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(xch + 4 * 42);
+  unsigned long long* done = full + kNB4;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) sn[j] = __ldg((TO_Y ? b3.sn : a.sn) + j);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
+    for (int b = 0; b < kNB4; ++b) {
+      mbar_init(full + b, 1);
+      mbar_init(done + b, kCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int G = gridDim.x;
+  const int ntiles = TO_Y ? b3.ntiles : a.ntiles;
+  const int ntiles_cta = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
+  // tile -> TMA coordinates: wax: (o, chunk c) of the 3D line view; blk: block o
+  auto coords = [&](int it, int& c0, int& c2) {
+    const int tile = blockIdx.x + it * G;
+    if (TO_Y) { c0 = 0; c2 = tile; }
+    else { c2 = tile / a.lchunks; c0 = (tile - c2 * a.lchunks) * 8; }
+  };
+  if (warp == kCW) {
+    if (lane != 0) return;
+    auto load = [&](int it, int b) {
+      int c0, c2;
+      coords(it, c0, c2);
+      mbar_expect(full + b, TILE_BYTES);
+#pragma unroll
+      for (int x = 0; x < NBOX; ++x) tma_load3(tiles + b * TD2 + x * wax::kBoxRows * 4, &tm, c0, x * wax::kBoxRows, c2, full + b);
+    };
+    auto store = [&](int it, int b) {
+      mbar_sleep_wait(done + b, (unsigned)((it / kNB4) & 1));
+      if (!TO_Y) {
+        int c0, c2;
+        coords(it, c0, c2);
+#pragma unroll
+        for (int x = 0; x < NBOX; ++x) tma_store3(&tm, c0, x * wax::kBoxRows, c2, tiles + b * TD2 + x * wax::kBoxRows * 4);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    };
+    for (int it = 0; it < ntiles_cta; ++it) {
+      const int b = it % kNB4;
+      if (it >= kNB4) {
+        store(it - kNB4, b);
+        if (!TO_Y) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+      }
+      load(it, b);
+    }
+    if (!TO_Y) {
+      for (int it = ntiles_cta - kNB4 < 0 ? 0 : ntiles_cta - kNB4; it < ntiles_cta; ++it) store(it, it % kNB4);
+      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    }
+    return;
+  }
+  const int q = warp & 3, h = warp >> 2, bar = 1 + q;
+  const LaneK1024 K(lane, h, TO_Y ? b3.tw : a.tw, TO_Y ? b3.scale : a.scale);
+  for (int it = 0; it < ntiles_cta; ++it) {
+    const int b = it % kNB4;
+    double2* T = tiles + b * TD2;
+    const int tile = blockIdx.x + it * G;
+    mbar_sleep_wait(full + b, (unsigned)((it / kNB4) & 1));
+    // padding levels of the last level tile: zero the line(s) of this pair
+    bool za = false, zb = false;
+    if (TO_Y) {
+      const int o2 = tile / b3.idiv, k1 = o2 / b3.nt, lt = o2 - k1 * b3.nt;
+      const int t0 = lt * 8 + 2 * q;
+      za = t0 >= b3.nlev; zb = t0 + 1 >= b3.nlev;
+    } else if (a.vlast < 8) {
+      const int o = tile / a.lchunks, c = tile - o * a.lchunks;
+      const int l0 = c * 8 + 2 * q;
+      const bool lastA = a.llast >= 0 ? l0 >= a.llast : (o % a.nt == a.nt - 1);
+      const bool lastB = a.llast >= 0 ? l0 + 1 >= a.llast : lastA;
+      za = lastA && (l0 & 7) >= a.vlast; zb = lastB && ((l0 + 1) & 7) >= a.vlast;
+    }
+    if (za || zb) {
+      for (int e = h * 32 + lane; e < N; e += 64) {
+        double2* p = at<Sw64>(T, e, q);
+        if (za) p->x = 0.0;
+        if (zb) p->y = 0.0;
+      }
+      pair_sync(bar);
+    }
+    if (TO_Y) {
+      const int o2 = tile / b3.idiv, r2 = tile - o2 * b3.idiv;
+      const int k1 = o2 / b3.nt, lt = o2 - k1 * b3.nt;
+      const int t0 = lt * 8 + 2 * q;
+      const long long m = b3.m;
+      const long long rowa = ((long long)((long long)t0 * m + k1) * b3.idiv + r2) * m;
+      const long long rowb = rowa + m * m * b3.idiv;
+      RowSink<128> sink{b3.y + rowa, b3.y + rowb, t0 < b3.nlev, t0 + 1 < b3.nlev, K.j1, K.j2};
+      warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_relaxed(done + b);
+    } else {
+      ColumnSink<Sw64, 128> sink(T, q, K.v, K.j1, K.j2);
+      warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(done + b);
+    }
   }
 }
 

@@ -3,7 +3,9 @@
 The fused solve ends with y[t, :] = Phi W[t, :] (pint.py:94-99 with the
 inverse DST moved after the time transform). For m + 1 in
 {256, 512} the strided axes run in place on the blocked W (k_dst_wax /
-k_dst_wax2, TMA tiles) and the last axis moves W -> y (k_dst_blk3). These
+k_dst_wax2, TMA tiles) and the last axis moves W -> y (k_dst_blk3); for 1024
+the last axis moves W -> y first (k_dst_q4, two warps per line pair) and the
+strided axis runs on y (k_dst_cols3). These
 tests feed seeded random blocked W -- with NaN in the padding levels of the
 last level tile, which pass A never writes -- through every entry point that
 runs those kernels and compare with the oracle's orthonormal DST
@@ -49,9 +51,14 @@ def run_levels(sp, W_host, L, dim, m, how):
         _lib.check(lib.bhcp_pint_levels(sp, plans.ptr(W), plans.ptr(y), L, sh), "levels")
     elif how == "passes":
         # the bench's phase-by-phase order: strided axes on W, then the last axis
-        for a in range(dim - 1):
-            _lib.check(lib.bhcp_pint_w_pass(sp, plans.ptr(W), L, a, sh), "w pass")
-        _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, 0, sh), "level pass 0")
+        # (m + 1 = 1024: the last axis W -> y, then the strided axes on y)
+        if lib.bhcp_pint_w_passes_supported(sp):
+            for a in range(dim - 1):
+                _lib.check(lib.bhcp_pint_w_pass(sp, plans.ptr(W), L, a, sh), "w pass")
+            _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, 0, sh), "level pass 0")
+        else:
+            for p in range(dim):
+                _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, p, sh), "level pass")
     else:
         # an all-to-all receive buffer: k1 blocks at koff[k1] (block_tables' uniform stride)
         nt = (L + TB - 1) // TB
@@ -64,13 +71,14 @@ def run_levels(sp, W_host, L, dim, m, how):
 
 @pytest.mark.parametrize("dim,cells,L", [(2, 512, 1), (2, 512, 7), (2, 512, 8), (2, 512, 9), (2, 512, 13),
                                          (2, 512, 16), (2, 256, 5), (2, 256, 8), (2, 256, 11), (3, 256, 1),
-                                         (3, 256, 3)])
+                                         (3, 256, 3), (2, 1024, 1), (2, 1024, 6), (2, 1024, 9), (2, 1024, 16)])
 def test_level_passes_vs_oracle(dim, cells, L):
     grid = B.build_grid(dim, 1.0, cells)
     m = cells - 1
     plan = plan_for(grid)
     lib = _lib.lib()
-    assert lib.bhcp_pint_w_passes_supported(plan.handle) == 1
+    wside = lib.bhcp_pint_w_passes_supported(plan.handle) == 1
+    assert wside == (cells in (256, 512))
     rng = np.random.default_rng(1000 * dim + 10 * cells + L)
     F = rng.standard_normal((L, m ** dim))
     ref = O.fused_pass_b(F, dim, m)
