@@ -10,7 +10,8 @@ metric is space-time DOFs/s over all ranks.
                 barrier + synchronize on both sides, max over ranks.
 * e2e        -- the same solve through the C-ABI call with HOST buffers:
                 pinned g -> device, bhcp_pint_solve, full trajectory -> pinned
-                host, every step inside the timed region.
+                host, every step inside the timed region (the trajectory copy of
+                step k overlaps step k+1 on a second stream).
 * roofline   -- dominant kernel of the step: algorithmic bytes (or, for the
                 FP64-bound pass A, algorithmic flops) / its average CUDA-event
                 duration vs the measured HBM copy bandwidth (FP64 FMA peak);
@@ -350,28 +351,45 @@ def main():
             print(json.dumps({"config": args.config, "ms_per_step": ms_per_step, "value": value,
                               "phases_ms": {nm: float(t) for nm, t in zip(names, phase_ms)}}), flush=True)
             return
-        # ---- e2e through the C-ABI with host buffers
+        # ---- e2e through the C-ABI with host buffers. Every step: pinned g -> device
+        # (compute stream), bhcp_pint_solve, full trajectory -> pinned host on a copy
+        # stream. Two trajectory buffers let step k's device->host copy overlap step
+        # k+1's H2D + solve; the timed region ends when the last copy has landed.
         g_host = torch.from_numpy(w.g_delta).pin_memory()
-        y_host = torch.empty((n, nx), dtype=torch.float64).pin_memory()
+        y_hosts = [torch.empty((n, nx), dtype=torch.float64).pin_memory() for _ in range(2)]
+        ys = [y, torch.empty_like(y)]
         g_e2e = torch.empty_like(g_dev)
         wsb = plan.ws_bytes
+        copy_stream = torch.cuda.Stream()
+        solved = [torch.cuda.Event() for _ in range(2)]
+        copied = [None, None]
 
-        def e2e_step():
+        def e2e_step(k):
+            b = k % 2
+            if copied[b] is not None:
+                stream.wait_event(copied[b])           # y buffer b's previous copy has read it
             g_e2e.copy_(g_host, non_blocking=True)
-            _lib.check(lib.bhcp_pint_solve(sp, tp, plans.ptr(g_e2e), divisor, plans.ptr(y), ctypes.c_void_p(wsp),
+            _lib.check(lib.bhcp_pint_solve(sp, tp, plans.ptr(g_e2e), divisor, plans.ptr(ys[b]), ctypes.c_void_p(wsp),
                                            wsb, sh), "solve")
-            y_host.copy_(y, non_blocking=True)
+            solved[b].record(stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(solved[b])
+                y_hosts[b].copy_(ys[b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                copied[b] = ev
 
         e2e_steps = max(3, min(args.steps, 10))
-        for _ in range(2):
-            e2e_step()
+        for k in range(2):
+            e2e_step(k)
         torch.cuda.synchronize()
         a0 = torch.cuda.Event(enable_timing=True)
         a1 = torch.cuda.Event(enable_timing=True)
-        a0.record()
-        for _ in range(e2e_steps):
-            e2e_step()
-        a1.record()
+        a0.record(stream)
+        for k in range(e2e_steps):
+            e2e_step(k)
+        stream.wait_stream(copy_stream)
+        a1.record(stream)
         torch.cuda.synchronize()
         plan.check_status()
         e2e_ms = a0.elapsed_time(a1) / e2e_steps
