@@ -24,7 +24,7 @@ start = next(i for i, x in enumerate(rows) if x and x[0] == "Address")
 ix = {k: i for i, k in enumerate(rows[start])}
 c = collections.Counter()
 for x in rows[start + 1:]:
-    if len(x) <= ix["Instructions Executed"]:
+    if len(x) <= ix["Instructions Executed"] or x[0] == "Address":
         continue
     n = int(x[ix["Instructions Executed"]] or 0)
     op = x[ix["Source"]].strip().split()

@@ -12,7 +12,7 @@ start = next(i for i, l in enumerate(lines) if l.startswith('"Address"'))
 rows = list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 h = rows[0]
 ix = {k: h.index(k) for k in h}
-data = rows[1:]
+data = [r for r in rows[1:] if r and r[0] != "Address" and len(r) == len(h)]
 tot = sum(int(r[ix["Warp Stall Sampling (All Samples)"]] or 0) for r in data)
 exc = sum(int(r[ix["L1 Wavefronts Shared Excessive"]] or 0) for r in data)
 print("total samples", tot, "excess smem wavefronts", exc)
