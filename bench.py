@@ -302,7 +302,7 @@ def main():
                       f" W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]
             names += ["k_dst_blk3 level pass (axis -1, W -> y)"]
         else:
-            names += [(("k_dst_q4" if w.num_cells == 1024 else "k_dst_blk2") if a == 0 else "k_dst_cols3") +
+            names += [(("k_dst_blk4" if w.num_cells == 1024 else "k_dst_blk2") if a == 0 else "k_dst_cols3") +
                       f" level pass {a} (axis -{a + 1})" for a in range(w.dim)]
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel

@@ -831,7 +831,7 @@ void set_all_attributes() {
   allow_smem(wax2::k_dst_wax2<512>);
   allow_smem(wax2::k_dst_blk3<512>);
   allow_smem(wax2::k_dst_blk3<256>);
-  allow_smem(wax2::k_dst_q4<true>);
+  allow_smem(wax2::k_dst_blk4);
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
@@ -1538,7 +1538,7 @@ int blk3_launch(const bhcp_space_plan* sp, const double* W, double* y, long long
 }
 
 // Strided axes on W: k_dst_wax (m + 1 = 256, c4), k_dst_wax2 (512, c2).
-// m + 1 = 1024 (c3) last axis: k_dst_q4 (two warps per line pair, 64 B row tiles)
+// m + 1 = 1024 (c3) last axis: k_dst_blk4 (two warps per line pair, 64 B row tiles)
 int q4_blk_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, cudaStream_t s) {
   constexpr int N = 1024;
   const long long m = sp->m, d = sp->dim;
@@ -1552,20 +1552,19 @@ int q4_blk_launch(const bhcp_space_plan* sp, const double* W, double* y, long lo
   int rc = tensor_map_3d(&tm, const_cast<double*>(W), fastk::kTBL, m, No, fastk::kTBL, fastk::kTBL * m,
                          fastk::kTBL, 64);
   if (rc) return rc;
-  wax::ArgsWX a{};
   wax2::ArgsB3 b3{sp->twN, sp->snN, sqrt(2.0 / N), y, (int)No, (int)NT, (int)idiv, (int)nlev, (int)m};
   const size_t sm = wax2::smem_bytes_4();
   const int threads = (wax2::kCW + 1) * 32;
-  const long long grid = std::min<long long>(No, resident_ctas(wax2::k_dst_q4<true>, threads, sm));
-  wax2::k_dst_q4<true><<<(unsigned)grid, threads, sm, s>>>(tm, a, b3);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_q4 (y) launch");
+  const long long grid = std::min<long long>(No, resident_ctas(wax2::k_dst_blk4, threads, sm));
+  wax2::k_dst_blk4<<<(unsigned)grid, threads, sm, s>>>(tm, b3);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_blk4 launch");
   return BHCP_OK;
 }
 
 // m + 1 = 1024 (c3) keeps the strided axis on y (k_dst_cols3, 6.6 ms): a W-side
-// tile of that length fits the smem budget only with 64 B rows, and
-// k_dst_q4<false> measured 7.5 ms (DRAM efficiency of 64 B rows at an 8 MB
-// stride). Its last axis runs k_dst_q4<true> (3.8 ms vs 5.4 for k_dst_blk2).
+// tile of that length fits the smem budget only with 64 B rows, which measured
+// 7.5 ms (DRAM efficiency of 64 B rows at an 8 MB stride). Its last axis runs
+// k_dst_blk4 (3.8 ms vs 5.4 for k_dst_blk2).
 bool wax_ok(const bhcp_space_plan* sp) {
   const int L = 2 * (sp->m + 1);
   return !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && (L == 512 || L == 1024);
@@ -1610,9 +1609,9 @@ int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, doub
     return level_pass(sp, W, koff, y, nlev, 0, s);
   }
   for (int p = 0; p < sp->dim; ++p) {
-    // m + 1 = 1024: the last axis by k_dst_q4 (k1 blocks at the uniform stride), then y-side passes
-    const bool q4 = p == 0 && !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && sp->m + 1 == 1024;
-    int rc = q4 ? blk3_launch(sp, W, y, nlev, s) : level_pass(sp, W, koff, y, nlev, p, s);
+    // m + 1 = 1024: the last axis by k_dst_blk4 (k1 blocks at the uniform stride), then y-side passes
+    const bool blk4 = p == 0 && !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && sp->m + 1 == 1024;
+    int rc = blk4 ? blk3_launch(sp, W, y, nlev, s) : level_pass(sp, W, koff, y, nlev, p, s);
     if (rc) return rc;
   }
   return BHCP_OK;

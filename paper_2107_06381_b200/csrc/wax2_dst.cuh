@@ -814,19 +814,17 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_con
 }
 
 // ---------------------------------------------------------------------------
-// N = 1024 (c3) kernels: 64 B rows (4 line pairs) x 1024 rows = 64 KB tiles,
-// 64-byte swizzle, two warps per line pair (warp w: pair w & 3, half w >> 2),
-// 3 buffers; a producer warp as in k_dst_wax2.
-//   k_dst_q4<true>:  the last axis, W -> y (TMA load, y rows from registers)
-//   k_dst_q4<false>: a strided axis in place on W (TMA load + store); measured
-//                    7.5 ms on c3 against 6.6 ms for k_dst_cols3 on y (64 B rows
-//                    at an 8 MB stride), so the solve does not launch it.
+// k_dst_blk4: the last axis W -> y for m + 1 = 1024 (c3). A tile is one 64 KB W
+// block (8 levels x 1024 rows, 64 B rows, 64-byte swizzle); two warps per line
+// pair (warp w: pair w & 3, half w >> 2) run warp_dst1024 and write the y rows
+// from registers; a producer warp streams 3 buffers.
+// (A W-side strided variant of the same tiles, TMA load + store, measured 7.5 ms
+// on c3 against 6.6 ms for k_dst_cols3 on y -- 64 B rows at an 8 MB stride --
+// so c3's strided axis stays on y.)
 constexpr int kNB4 = 3;
 constexpr size_t smem_bytes_4() { return 1024 + (size_t)kNB4 * 1024 * 64 + sizeof(double) * (1024 + 4 * 42) + 16 * kNB4; }
 
-template <bool TO_Y>
-__global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_q4(const __grid_constant__ CUtensorMap tm, wax::ArgsWX a,
-                                                            ArgsB3 b3) {
+__global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk4(const __grid_constant__ CUtensorMap tm, ArgsB3 b3) {
   constexpr int N = 1024, NBOX = N / wax::kBoxRows, TD2 = N * 4;
   constexpr unsigned TILE_BYTES = (unsigned)(N * 8 * sizeof(double));
   extern __shared__ unsigned char smem_raw[];
@@ -836,7 +834,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_q4(const __grid_const
   double* xch = sn + N;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(xch + 4 * 42);
   unsigned long long* done = full + kNB4;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) sn[j] = __ldg((TO_Y ? b3.sn : a.sn) + j);
+  for (int j = threadIdx.x; j < N; j += blockDim.x) sn[j] = __ldg(b3.sn + j);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm) : "memory");
@@ -848,68 +846,34 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_q4(const __grid_const
   }
   __syncthreads();
   const int G = gridDim.x;
-  const int ntiles = TO_Y ? b3.ntiles : a.ntiles;
-  const int ntiles_cta = ntiles > (int)blockIdx.x ? (ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
-  // tile -> TMA coordinates: wax: (o, chunk c) of the 3D line view; blk: block o
-  auto coords = [&](int it, int& c0, int& c2) {
-    const int tile = blockIdx.x + it * G;
-    if (TO_Y) { c0 = 0; c2 = tile; }
-    else { c2 = tile / a.lchunks; c0 = (tile - c2 * a.lchunks) * 8; }
-  };
+  const int ntiles_cta = b3.ntiles > (int)blockIdx.x ? (b3.ntiles - 1 - (int)blockIdx.x) / G + 1 : 0;
   if (warp == kCW) {
     if (lane != 0) return;
-    auto load = [&](int it, int b) {
-      int c0, c2;
-      coords(it, c0, c2);
-      mbar_expect(full + b, TILE_BYTES);
-#pragma unroll
-      for (int x = 0; x < NBOX; ++x) tma_load3(tiles + b * TD2 + x * wax::kBoxRows * 4, &tm, c0, x * wax::kBoxRows, c2, full + b);
-    };
-    auto store = [&](int it, int b) {
-      mbar_sleep_wait(done + b, (unsigned)((it / kNB4) & 1));
-      if (!TO_Y) {
-        int c0, c2;
-        coords(it, c0, c2);
-#pragma unroll
-        for (int x = 0; x < NBOX; ++x) tma_store3(&tm, c0, x * wax::kBoxRows, c2, tiles + b * TD2 + x * wax::kBoxRows * 4);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-      }
-    };
     for (int it = 0; it < ntiles_cta; ++it) {
       const int b = it % kNB4;
-      if (it >= kNB4) {
-        store(it - kNB4, b);
-        if (!TO_Y) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-      }
-      load(it, b);
-    }
-    if (!TO_Y) {
-      for (int it = ntiles_cta - kNB4 < 0 ? 0 : ntiles_cta - kNB4; it < ntiles_cta; ++it) store(it, it % kNB4);
-      asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+      if (it >= kNB4) mbar_sleep_wait(done + b, (unsigned)(((it - kNB4) / kNB4) & 1));
+      const int o = blockIdx.x + it * G;
+      mbar_expect(full + b, TILE_BYTES);
+#pragma unroll
+      for (int x = 0; x < NBOX; ++x) tma_load3(tiles + b * TD2 + x * wax::kBoxRows * 4, &tm, 0, x * wax::kBoxRows, o, full + b);
     }
     return;
   }
   const int q = warp & 3, h = warp >> 2, bar = 1 + q;
-  const LaneK1024 K(lane, h, TO_Y ? b3.tw : a.tw, TO_Y ? b3.scale : a.scale);
+  const LaneK1024 K(lane, h, b3.tw, b3.scale);
+  const long long m = b3.m;
   for (int it = 0; it < ntiles_cta; ++it) {
     const int b = it % kNB4;
     double2* T = tiles + b * TD2;
-    const int tile = blockIdx.x + it * G;
+    const int o = blockIdx.x + it * G;
+    // o = (k1 * NT + lt) * idiv + r2
+    const int o2 = o / b3.idiv, r2 = o - o2 * b3.idiv;
+    const int k1 = o2 / b3.nt, lt = o2 - k1 * b3.nt;
+    const int t0 = lt * 8 + 2 * q;   // levels of lines 2q, 2q + 1
     mbar_sleep_wait(full + b, (unsigned)((it / kNB4) & 1));
-    // padding levels of the last level tile: zero the line(s) of this pair
-    bool za = false, zb = false;
-    if (TO_Y) {
-      const int o2 = tile / b3.idiv, k1 = o2 / b3.nt, lt = o2 - k1 * b3.nt;
-      const int t0 = lt * 8 + 2 * q;
-      za = t0 >= b3.nlev; zb = t0 + 1 >= b3.nlev;
-    } else if (a.vlast < 8) {
-      const int o = tile / a.lchunks, c = tile - o * a.lchunks;
-      const int l0 = c * 8 + 2 * q;
-      const bool lastA = a.llast >= 0 ? l0 >= a.llast : (o % a.nt == a.nt - 1);
-      const bool lastB = a.llast >= 0 ? l0 + 1 >= a.llast : lastA;
-      za = lastA && (l0 & 7) >= a.vlast; zb = lastB && ((l0 + 1) & 7) >= a.vlast;
-    }
+    const bool za = t0 >= b3.nlev, zb = t0 + 1 >= b3.nlev;
     if (za || zb) {
+      // padding levels of the last level tile: zero them (they share the complex FFT)
       for (int e = h * 32 + lane; e < N; e += 64) {
         double2* p = at<Sw64>(T, e, q);
         if (za) p->x = 0.0;
@@ -917,24 +881,12 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_q4(const __grid_const
       }
       pair_sync(bar);
     }
-    if (TO_Y) {
-      const int o2 = tile / b3.idiv, r2 = tile - o2 * b3.idiv;
-      const int k1 = o2 / b3.nt, lt = o2 - k1 * b3.nt;
-      const int t0 = lt * 8 + 2 * q;
-      const long long m = b3.m;
-      const long long rowa = ((long long)((long long)t0 * m + k1) * b3.idiv + r2) * m;
-      const long long rowb = rowa + m * m * b3.idiv;
-      RowSink<128> sink{b3.y + rowa, b3.y + rowb, t0 < b3.nlev, t0 + 1 < b3.nlev, K.j1, K.j2};
-      warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
-      __syncwarp();
-      if (lane == 0) mbar_arrive_relaxed(done + b);
-    } else {
-      ColumnSink<Sw64, 128> sink(T, q, K.v, K.j1, K.j2);
-      warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(done + b);
-    }
+    const long long rowa = ((long long)((long long)t0 * m + k1) * b3.idiv + r2) * m;
+    const long long rowb = rowa + m * m * b3.idiv;
+    RowSink<128> sink{b3.y + rowa, b3.y + rowb, !za, !zb, K.j1, K.j2};
+    warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_relaxed(done + b);
   }
 }
 

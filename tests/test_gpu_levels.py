@@ -4,7 +4,7 @@ The fused solve ends with y[t, :] = Phi W[t, :] (pint.py:94-99 with the
 inverse DST moved after the time transform). For m + 1 in
 {256, 512} the strided axes run in place on the blocked W (k_dst_wax /
 k_dst_wax2, TMA tiles) and the last axis moves W -> y (k_dst_blk3); for 1024
-the last axis moves W -> y first (k_dst_q4, two warps per line pair) and the
+the last axis moves W -> y first (k_dst_blk4, two warps per line pair) and the
 strided axis runs on y (k_dst_cols3). These
 tests feed seeded random blocked W -- with NaN in the padding levels of the
 last level tile, which pass A never writes -- through every entry point that
