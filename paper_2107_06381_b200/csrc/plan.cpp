@@ -2,6 +2,9 @@
 // Bluestein chirp/filter tables, all computed in long double and rounded once.
 #include "plan.h"
 
+#include <map>
+#include <mutex>
+
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -136,28 +139,45 @@ bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
   for (size_t i = 0; i < rad.size(); ++i) p.d.radix[i] = rad[i];
   p.ld = (Lc % 2 == 0) ? Lc + 1 : Lc;
 
-  // Host tables
-  std::vector<double2> tw(Lc), chirp, bhat;
-  for (int k = 0; k < Lc; ++k) {
-    long double ang = -2.0L * kPi * (long double)k / (long double)Lc;
-    tw[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+  // Host tables (depend on L only: computed once per length and cached; the
+  // long-double DFT of the Bluestein kernel is O(Lc^2))
+  struct Tabs { std::vector<double2> tw, chirp, bhat; };
+  static std::mutex tabs_mutex;
+  static std::map<std::pair<int, int>, Tabs> tabs_cache;
+  Tabs tb;
+  {
+    std::lock_guard<std::mutex> lk(tabs_mutex);
+    auto it = tabs_cache.find({L, Lc});
+    if (it != tabs_cache.end()) tb = it->second;
   }
-  if (blue) {
-    chirp.resize(L);
-    std::vector<cld> cl(L);
-    for (int j = 0; j < L; ++j) {
-      long long e = ((long long)j * j) % (2LL * L);
-      long double ang = -kPi * (long double)e / (long double)L;
-      cl[j] = cld(cosl(ang), sinl(ang));
-      chirp[j] = to_d2(cl[j]);
+  if (tb.tw.empty()) {
+    tb.tw.resize(Lc);
+    for (int k = 0; k < Lc; ++k) {
+      long double ang = -2.0L * kPi * (long double)k / (long double)Lc;
+      tb.tw[k] = make_double2((double)cosl(ang), (double)sinl(ang));
     }
-    std::vector<cld> b(Lc, cld(0, 0));
-    for (int j = 0; j < L; ++j) b[j] = std::conj(cl[j]);
-    for (int j = 1; j < L; ++j) b[Lc - j] = std::conj(cl[j]);
-    host_dft(b);
-    bhat.resize(Lc);
-    for (int k = 0; k < Lc; ++k) bhat[k] = to_d2(b[k] / (long double)Lc);
+    if (blue) {
+      tb.chirp.resize(L);
+      std::vector<cld> cl(L);
+      for (int j = 0; j < L; ++j) {
+        long long e = ((long long)j * j) % (2LL * L);
+        long double ang = -kPi * (long double)e / (long double)L;
+        cl[j] = cld(cosl(ang), sinl(ang));
+        tb.chirp[j] = to_d2(cl[j]);
+      }
+      std::vector<cld> b(Lc, cld(0, 0));
+      for (int j = 0; j < L; ++j) b[j] = std::conj(cl[j]);
+      for (int j = 1; j < L; ++j) b[Lc - j] = std::conj(cl[j]);
+      host_dft(b);
+      tb.bhat.resize(Lc);
+      for (int k = 0; k < Lc; ++k) tb.bhat[k] = to_d2(b[k] / (long double)Lc);
+    }
+    std::lock_guard<std::mutex> lk(tabs_mutex);
+    tabs_cache[{L, Lc}] = tb;
   }
+  const std::vector<double2>& tw = tb.tw;
+  const std::vector<double2>& chirp = tb.chirp;
+  const std::vector<double2>& bhat = tb.bhat;
   size_t bytes = (tw.size() + chirp.size() + bhat.size()) * sizeof(double2);
   cudaGetLastError();  // clear any stale error before checking our own calls
   if (cudaMalloc(&p.mem, bytes) != cudaSuccess) { *err = "cudaMalloc failed for FFT plan"; return false; }
@@ -178,7 +198,23 @@ bool build_fft_plan(int L, FftPlanHost* out, std::string* err) {
 
 // Power-of-two Bluestein tables for n = 2^p + 1 (see fastk::k_modes_blue):
 // tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1).
+bool build_blue_tables_uncached(int n, std::vector<double2>* out, std::string* err);
+
 bool build_blue_tables(int n, std::vector<double2>* out, std::string* err) {
+  static std::mutex mu;
+  static std::map<int, std::vector<double2>> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(n);
+    if (it != cache.end()) { *out = it->second; return true; }
+  }
+  if (!build_blue_tables_uncached(n, out, err)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[n] = *out;
+  return true;
+}
+
+bool build_blue_tables_uncached(int n, std::vector<double2>* out, std::string* err) {
   const int M = n - 1, L = 2 * M;
   if (M < 2 || (M & (M - 1))) { *err = "n - 1 must be a power of two"; return false; }
   out->assign(2 * L + 2 * n, make_double2(0.0, 0.0));

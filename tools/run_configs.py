@@ -64,6 +64,21 @@ for name in names:
             del y, plan, graph
             torch.cuda.empty_cache()
     out[name] = {"dof": w.dof, "gen_s": gen_s, "results": res}
+    if name == "c5":
+        # the full error-vs-alpha curve: 64 alpha x 2 kinds, every e_h against the oracle's
+        from paper_2107_06381_b200 import sweep
+        sw = sweep.alpha_sweep(grid, tg, w.g_delta, w.z0, w.kinds, w.alphas)
+        dev = []
+        for p in sw.points:
+            ref0 = O.spectral_oracle(p.kind, p.alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
+                                     w.g_delta, levels=np.array([0]))
+            e_ref = workloads.l2_error(ref0[0], w.z0, grid.h, w.dim)
+            dev.append(abs(p.e_h - e_ref) / e_ref)
+        out[name]["sweep"] = {
+            "solves": len(sw.points), "wall_s": sw.wall_s, "device_ms_total": sum(p.ms for p in sw.points),
+            "max_rel_dev_e_h": max(dev), "ok_3_sig_digits": bool(max(dev) <= 5e-4),
+            "best": {k: {"alpha": sw.best(k).alpha, "e_h": sw.best(k).e_h} for k in w.kinds},
+            "curve": {k: [[float(a), float(e)] for a, e in zip(*sw.curve(k))] for k in w.kinds}}
     if cpu:
         kind, alpha = w.kinds[0], w.alphas[0]
         dof_eq, secs = O.solve_pint_sample(kind, alpha, w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
