@@ -84,6 +84,14 @@ class PintPlan:
         self.ws_bytes = int(lib.bhcp_pint_workspace_bytes(self.sp.handle, self.tp.handle))
         self._ws: Optional[torch.Tensor] = None
 
+    def use_workspace(self, ws: torch.Tensor) -> None:
+        """Share a workspace between plans of the same grid and level count (their
+        sizes agree; e.g. the plans of an alpha sweep). The caller serialises the
+        solves that use it."""
+        if ws.numel() < self.ws_bytes or ws.dtype != torch.uint8:
+            raise ValueError(f"workspace of {ws.numel()} bytes, this plan needs {self.ws_bytes}")
+        self._ws = ws
+
     def workspace(self) -> torch.Tensor:
         if self._ws is None:
             self._ws = torch.empty(self.ws_bytes, dtype=torch.uint8,

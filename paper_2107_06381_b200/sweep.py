@@ -118,7 +118,7 @@ def alpha_sweep(grid, timegrid, g_delta, z0, kinds: Sequence[str], alphas: Seque
         plan, div = built.pop((kind, alpha))
         if ws_shared[0] is None:
             ws_shared[0] = plan.workspace()
-        plan._ws = ws_shared[0]          # every (kind, alpha) plan has the same workspace size
+        plan.use_workspace(ws_shared[0])   # every (kind, alpha) plan has the same workspace size
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         plan.solve_device(g_dev, div, out=y)

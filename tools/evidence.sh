@@ -9,7 +9,7 @@ mkdir -p $out
 python -m pytest tests -m gpu -q -x > $out/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $out/rc.txt
 python bench.py > $out/bench_c2.json 2> $out/bench_c2.err; echo "bench rc=$?" | tee -a $out/rc.txt
 python bench.py --impl reference --steps 3 --warmup 1 > $out/bench_ref.json 2> $out/bench_ref.err; echo "ref rc=$?" | tee -a $out/rc.txt
-python tools/run_configs.py > $out/configs.json 2> $out/configs.err; echo "configs rc=$?" | tee -a $out/rc.txt
+python tools/run_configs.py --cpu > $out/configs.json 2> $out/configs.err; echo "configs rc=$?" | tee -a $out/rc.txt
 # launch list of the timed step (--quick: device step only) and of the whole bench command
 python bench.py --quick --steps 3 --warmup 3 > $out/bench_short.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches.csv \
