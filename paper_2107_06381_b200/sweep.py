@@ -18,7 +18,7 @@ from __future__ import annotations
 
 import time
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence, Tuple
+from typing import Callable, List, Sequence, Tuple
 
 import numpy as np
 
@@ -46,8 +46,8 @@ class SweepResult:
 
 
 def assign(n_pairs: int, rank: int, world: int) -> List[int]:
-    """Pairs of this rank: i = rank, rank + world, ... (round robin keeps the
-    cheap and expensive alphas -- all alphas cost the same here -- balanced)."""
+    """Pairs of this rank: i = rank, rank + world, ... (round robin; every
+    solve costs the same, so the ranks are balanced to one solve)."""
     if not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside world {world}")
     return list(range(rank, n_pairs, world))
