@@ -496,7 +496,7 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     alg = [8.0 * local_dof_a, 0.0, 32.0 * local_dof_b]
     dom = 0 if ph[0] >= ph[2] else 2
     achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
-    launches = 6 + 2 * grid.dim  # status reset, ghat (dim passes + scale), modes, level passes (x2 kernels max)
+    launches = 1 + (grid.dim + 1) + 1 + grid.dim  # status reset, ghat (dim passes + scale), modes, level passes
     if rank != 0:
         return None
     return {
