@@ -367,7 +367,10 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
       const long long local = valid ? kl : 0;
       if (wl.mode_major) { k1d = (int)(local / wl.P1); rd = local - (long long)k1d * wl.P1; }
     }
-    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    // 2D symmetric tiles know (k1, k2): mu1[k1] + mu1[k2] directly (the same sum
+    // mode_mu forms, without its 64-bit division of the flat index)
+    const double mu = SYM ? (valid ? __ldg(a.mu1 + k1d) + __ldg(a.mu1 + rd) : __ldg(a.mu1) + __ldg(a.mu1))
+                          : mode_mu(a.mu1, a.m, a.dim, kd);
     const double c = valid ? __ldg(a.ghat + kd) * a.cscale : 0.0;
     const double c2 = (SYM && km >= 0) ? __ldg(a.ghat + km) * a.cscale : 0.0;
     {
