@@ -65,7 +65,10 @@ __device__ __forceinline__ void flag_singular(StatusDev* st, long long col) {
 }
 
 // mu for flattened mode index (C order, first axis outermost) -- same
-// association as numpy add.outer (space.py:215; 3D restated as ((a+b)+c)).
+// association as numpy add.outer (space.py:215). 3D (no reference; restated):
+// the sum of the sorted triple, (mu1[lo] + mu1[mid]) + mu1[hi], so all six
+// permutations of a mode share one bit-identical mu (one time FFT serves them,
+// k_modes_rader sym6); within an ulp of the C-order sum.
 __device__ __forceinline__ double mode_mu(const double* __restrict__ mu1, int m, int dim, long long k) {
   if (dim == 1) return __ldg(mu1 + k);
   if (dim == 2) {
@@ -73,9 +76,12 @@ __device__ __forceinline__ double mode_mu(const double* __restrict__ mu1, int m,
     return __ldg(mu1 + k1) + __ldg(mu1 + k2);
   }
   const long long mm = (long long)m * m;
-  const int k1 = (int)(k / mm);
+  int k1 = (int)(k / mm);
   const long long r = k - k1 * mm;
-  const int k2 = (int)(r / m), k3 = (int)(r - (long long)k2 * m);
+  int k2 = (int)(r / m), k3 = (int)(r - (long long)k2 * m);
+  if (k1 > k2) { const int t = k1; k1 = k2; k2 = t; }
+  if (k2 > k3) { const int t = k2; k2 = k3; k3 = t; }
+  if (k1 > k2) { const int t = k1; k1 = k2; k2 = t; }
   return (__ldg(mu1 + k1) + __ldg(mu1 + k2)) + __ldg(mu1 + k3);
 }
 
@@ -1075,17 +1081,25 @@ struct SymRange {
   long long begin = 0, end = -1;
 };
 
-const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count) {
+// six = true (3D): tiles (k1, k2, k3a) of sorted triples k1 <= k2 <= k3, k3 in
+// [k3a, k3a + S) with k3a stepping from k2 rounded down to S (k_modes_rader's
+// one-FFT-per-permutation-class work list)
+const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count, bool six = false) {
   auto* sp = const_cast<bhcp_space_plan*>(sp_c);
   std::lock_guard<std::mutex> lk(g_tile_mutex);
+  const int key = six ? S + 1000 : S;
   int slot = 0;
-  while (slot < 9 && sp->seg_tiles[slot] && sp->seg_len[slot] != S) ++slot;
+  while (slot < 9 && sp->seg_tiles[slot] && sp->seg_len[slot] != key) ++slot;
   if (slot >= 9 || S < 1) return nullptr;
   if (!sp->seg_tiles[slot]) {
-    sp->seg_len[slot] = S;
+    sp->seg_len[slot] = key;
     std::vector<int4> t;
     const int m = sp->m;
-    if (sp->dim == 2) {
+    if (six && sp->dim == 3) {
+      for (int k1 = 0; k1 < m; ++k1)
+        for (int k2 = k1; k2 < m; ++k2)
+          for (int k3a = k2 - k2 % S; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
+    } else if (sp->dim == 2) {
       for (int k1 = 0; k1 < m; ++k1)
         for (int k2a = k1 - k1 % S; k2a < m; k2a += S) t.push_back(make_int4(k1, k2a, 0, 0));
     } else {
@@ -1187,7 +1201,8 @@ int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doubl
   const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
   if (sym) {
     long long cnt = 0;
-    a.tiles = seg_tiles(sp, Pl::S, &cnt);
+    a.sym6 = sp->dim == 3 ? 1 : 0;
+    a.tiles = seg_tiles(sp, Pl::S, &cnt, a.sym6 != 0);
     if (!a.tiles) return cuda_fail("seg tiles");
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
@@ -2006,7 +2021,7 @@ int64_t bhcp_pint_sym_tiles(const bhcp_space_plan* sp, const bhcp_time_plan* tp)
   DeviceGuard g(sp->device);
   long long cnt = 0;
   const int4* t = nullptr;
-  if (tp->rader && tp->n == 257) t = seg_tiles(sp, fastk::RaderPlan<257>::S, &cnt);
+  if (tp->rader && tp->n == 257) t = seg_tiles(sp, fastk::RaderPlan<257>::S, &cnt, sp->dim == 3);
   else if (tp->gt && tp->n == 1025) t = seg_tiles(sp, fastk::GtPlan::S, &cnt);
   else if (tp->pf && tp->n == 4097) t = seg_tiles(sp, 1, &cnt);
   else if (tp->blue && tp->n == 4097) t = seg_tiles(sp, fastk::BluePlan<4097>::S, &cnt);

@@ -667,6 +667,7 @@ struct RaderModesArgs {
   WLayout wl;
   const int4* tiles;    // SYM: seg tiles of S modes (see k_modes_blue)
   long long ntiles;
+  int sym6;             // 3D: tiles of sorted triples k1 <= k2 <= k3, one FFT for all their permutations
 };
 
 template <int NL, bool SYM>
@@ -722,6 +723,15 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
         hm = valid && k2 != k1;
         km = (long long)k2 * a.m + k1;
         k1d = k1; rd = k2; k1m = k2; rm = k1;
+      } else if (a.sym6) {
+        // sorted triple (k1 <= k2 <= k3): every permutation of it has the same
+        // mu = (mu1[k1] + mu1[k2]) + mu1[k3] (the sum in sorted order; within an
+        // ulp of the C-order sum of the other permutations), so one FFT serves
+        // all of them
+        const int k1 = tb.x, k2 = tb.y, k3 = tb.z + warp;
+        valid = k3 < a.m && k3 >= k2;
+        kd = ((long long)k1 * a.m + k2) * a.m + k3;
+        k1d = k1; rd = (long long)k2 * a.m + k3; k1m = k2; rm = (long long)k1 * a.m + k3;
       } else {
         const int k1 = tb.x, k2 = tb.y, k3 = tb.z + warp;
         valid = k3 < a.m;
@@ -740,7 +750,14 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
       else rd = local;
     }
     if (!valid) continue;
-    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    const bool six = SYM && a.sym6;
+    double mu;
+    if (six) {
+      const int4 tb = __ldg(a.tiles + tile);
+      mu = (__ldg(a.mu1 + tb.x) + __ldg(a.mu1 + tb.y)) + __ldg(a.mu1 + tb.z + warp);
+    } else {
+      mu = mode_mu(a.mu1, a.m, a.dim, kd);
+    }
     const double c = __ldg(a.ghat + kd) * a.cscale;
     const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
     // 1 / (s + mu) with the singular test of space.py:237-240 (column j reported)
@@ -765,6 +782,49 @@ __global__ void __launch_bounds__(RaderPlan<NL>::T, RaderPlan<NL>::MINB) k_modes
     // store: t along lanes; X_0 = v0 + A0, X_t = v0 + conv_{qidx[t]}
     const int nsl = wl.mode_major ? wl.nsl : 1;
     double zr2 = 0.0, zi2 = 0.0;
+    if (six) {
+      // the distinct permutations (p1, p2, p3) of the sorted triple (x, y, z):
+      // 0 (x,y,z) 1 (x,z,y) 2 (y,x,z) 3 (y,z,x) 4 (z,x,y) 5 (z,y,x)
+      const int4 tb = __ldg(a.tiles + tile);
+      const int x = tb.x, yv = tb.y, z = tb.z + warp;
+      const unsigned mask = (x == yv && yv == z) ? 0x01u : (x == yv) ? 0x13u : (yv == z) ? 0x0du : 0x3fu;
+      const int P1[6] = {x, x, yv, yv, z, z}, P2[6] = {yv, z, x, z, x, yv}, P3[6] = {z, yv, z, x, yv, x};
+      double cf[6];
+      double cc = 0.0;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        cf[p] = ((mask >> p) & 1u) ? __ldg(a.ghat + ((long long)P1[p] * a.m + P2[p]) * a.m + P3[p]) * a.cscale : 0.0;
+        cc = fma(cf[p], cf[p], cc);
+      }
+      for (int sl = 0; sl < nsl; ++sl) {
+        const int t0 = wl.sl_c[sl], t1 = wl.sl_c[sl + 1];
+        const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
+        const long long step = 4 * wl.P1 * kTBL;
+        double* w6[6];
+#pragma unroll
+        for (int p = 0; p < 6; ++p)
+          w6[p] = wl.sl_base[sl] + wl.row_off(sl, P1[p]) + ((long long)P2[p] * a.m + P3[p]) * kTBL + lo;
+        for (int t = t0 + lane; t < t1; t += 32) {
+          double2 X;
+          if (t == 0) X = cadd(v0, A0);
+          else X = cadd(v0, cconj(buf[WF::pi(s_q[t])]));
+          const double2 g = s_gi[t];
+          const double zr = X.x * g.x - X.y * g.y;
+          const double zi = X.x * g.y + X.y * g.x;
+          zr2 = fma(zr, zr, zr2);
+          zi2 = fma(zi, zi, zi2);
+#pragma unroll
+          for (int p = 0; p < 6; ++p) {
+            if ((mask >> p) & 1u) *w6[p] = cf[p] * zr;
+            w6[p] += step;
+          }
+        }
+      }
+      sre = fma(cc, zr2, sre);
+      sim = fma(cc, zi2, sim);
+      __syncwarp();
+      continue;
+    }
     for (int sl = 0; sl < nsl; ++sl) {
       const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
       const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
