@@ -80,7 +80,10 @@ const char* bhcp_last_error(void);
  * {1,2,3} (3 is this library's extension; the reference stops at 2,
  * space.py:42-43). mu1_host holds the m = num_cells-1 one-dimensional
  * eigenvalues (4/h^2) sin^2(k pi / 2M) computed by the caller with the
- * reference expression (space.py:209-211), so shifts match bit for bit. */
+ * reference expression (space.py:209-211), so shifts match bit for bit.
+ * 2D mode eigenvalues are mu1[k1] + mu1[k2] (numpy add.outer, space.py:215);
+ * 3D ones (no reference) are the sum of the sorted triple,
+ * (mu1[lo] + mu1[mid]) + mu1[hi], shared bit for bit by all permutations. */
 int bhcp_space_plan_create(int device, int dim, int num_cells,
                            const double* mu1_host, bhcp_space_plan** out);
 void bhcp_space_plan_destroy(bhcp_space_plan* plan);
@@ -170,10 +173,10 @@ int bhcp_pint_modes_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, cons
 
 /* Symmetric pass A for the multi-GPU solve. The modes kernels compute one
  * mode of every mirror pair (k1,k2) / (k2,k1) (2D) or (k1,k2,k3) /
- * (k2,k1,k3) (3D), whose shifted spectra are bit-identical, from a tile
- * list. bhcp_pint_sym_tiles returns the list length for (sp, tp), or 0 when
+ * (k2,k1,k3) (3D; for n = 257 every permutation of a sorted triple), whose
+ * shifted spectra are bit-identical, from a tile list. bhcp_pint_sym_tiles returns the list length for (sp, tp), or 0 when
  * that time length has no symmetric kernel. bhcp_pint_modes_sym_to
- * computes tiles [tile_begin, tile_end) and stores both modes of each pair
+ * computes tiles [tile_begin, tile_end) and stores every mode of each class
  * into every level slab s: at slab_dst[s] + slab_koff[s][k1] +
  * ((t - b[s]) / 8 * P1 + r) * 8 + (t - b[s]) % 8, where slab_koff[s] is the
  * device int64 block table (length m) of slab s's receiver, as for
