@@ -1,7 +1,12 @@
-// wax2_dst.cuh -- strided spatial axes in place on the blocked W, one warp
-// per line pair, no CTA barriers (N = 512: c2).
+// wax2_dst.cuh -- the level passes of the fused solve with one warp (or two)
+// per line pair and no CTA barriers. Kernels:
+//   k_dst_wax2<512>  strided axis in place on the blocked W (c2)
+//   k_dst_blk3<N>    last axis, W -> y, N = 256 (c4) and 512 (c2)
+//   k_dst_blk4       last axis, W -> y, N = 1024 (c3; two warps per line pair)
+// Column DSTs: warp_dst512 (three radix-8 stages), warp_dst256 (four radix-4
+// stages), warp_dst1024 (radix 8, 16, 8 over two warps with named barriers).
 //
-// Same job and tiling as k_dst_wax (wax_dst.cuh): a tile is 16 adjacent
+// k_dst_wax2 does the job of k_dst_wax (wax_dst.cuh): a tile is 16 adjacent
 // lines x 511 elements of a 3D view of W, moved by TMA tensor loads/stores.
 // The difference is who works on it:
 //   * the tile lands 128B-swizzled (16-byte chunk q of row e at chunk
