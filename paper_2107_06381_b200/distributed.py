@@ -338,7 +338,13 @@ class DeviceOps:
     def tables(self, layout: SlabLayout, rank: int):
         key = (layout.world, rank)
         if key not in self._tables:
-            self._tables[key] = self.torch.from_numpy(layout.block_tables(rank)).to(self.g.device)
+            koff = layout.block_tables(rank)
+            # the TMA level passes view the receive buffer with one k1 stride
+            # (bhcp_pint_levels_blocked); the slab layouts always produce it
+            stride = layout.tiles(rank) * layout.plane * TB
+            if not np.array_equal(koff, np.arange(layout.m, dtype=np.int64) * stride):
+                raise ValueError("receive-buffer block table is not uniform")
+            self._tables[key] = self.torch.from_numpy(koff).to(self.g.device)
         return self._tables[key]
 
     def levels_blocked(self, recv, koff, L: int):
