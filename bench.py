@@ -70,6 +70,10 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def describe(name, w, kind, alpha) -> str:
+    return f"{name}: {w.dim}D {kind}, {w.num_cells - 1}^{w.dim} interior x {w.n_levels} levels, alpha={alpha:g}"
+
+
 def fp64_peak():
     """Dense FP64 FMA throughput measured on a B200 of this pool by tools/probe_fp64.cu
     (profiles/fp64_peak.json), else the 37 TFLOP/s datasheet figure."""
@@ -180,8 +184,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
-        "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, alpha=1e-2",
-                   "dof_per_solve": w.dof},
+        "config": {"workload": describe(args.config, w, kind, alpha), "dof_per_solve": w.dof},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -418,8 +421,9 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config construction)",
-            "config": {"workload": f"{args.config}: 2D pint-mqbvm, 511^2 interior x 513 levels, alpha=1e-2",
-                       "dof_per_solve": dof, "l2": "working set (W + y = 2.1 GB) larger than L2; no flush",
+            "config": {"workload": describe(args.config, w, kind, alpha),
+                       "dof_per_solve": dof,
+                       "l2": f"working set (W + y = {2 * 8 * dof / 1e9:.1f} GB) larger than L2; no flush",
                        "timing": f"K replays of the CUDA graph of one step ({launches_per_step} kernels); phases_ms from an eager "
                                  "pass of the same K steps with CUDA events"},
             "roofline": roofline,

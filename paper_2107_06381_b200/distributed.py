@@ -509,7 +509,8 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
-        "config": {"workload": f"{args.config}: 2D pint-mqbvm 511^2 x 513 levels, slab-decomposed over {world} GPUs",
+        "config": {"workload": f"{args.config}: {grid.dim}D {system.method.kind.value} {grid.num_cells - 1}^{grid.dim} x "
+                               f"{tg.n_levels} levels, slab-decomposed over {world} GPUs",
                    "dof_per_solve": w.dof, "transport": transport,
                    "parallelism": (f"pass A over 1/P of the mirror-pair tiles (or a k1 slab) storing into the "
                                    f"level-slab owners over NVLink peer memory -> level slabs, P={world}")
