@@ -264,7 +264,7 @@ def main():
                     if record:
                         record[3 + a].record()
 
-        launches_per_step = 1 + (w.dim + 1) + 1 + w.dim  # reset, ghat passes + scale, modes, level passes
+        launches_per_step = 1 + w.dim + 1 + w.dim  # graph of bhcp_pint_solve: reset, ghat passes, modes, level passes
         sampler = ClockSampler(local)
         sampler.start()
         time.sleep(0.5)  # let nvidia-smi start sampling before the GPU is loaded

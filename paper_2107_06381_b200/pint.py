@@ -112,6 +112,12 @@ class PintPlan:
         stream = plans.stream_handle()
         wsp = ws.data_ptr()
         status = ctypes.c_void_p(lib.bhcp_pint_status_ptr(self.sp.handle, self.tp.handle, ctypes.c_void_p(wsp)))
+        if not events:
+            # one call: status reset, ghat, pass A (the 1/(divisor n) scale folded into
+            # its coefficients) and the level passes
+            _lib.check(lib.bhcp_pint_solve(self.sp.handle, self.tp.handle, plans.ptr(g), divisor, plans.ptr(y),
+                                           ctypes.c_void_p(wsp), self.ws_bytes, stream), "bhcp_pint_solve")
+            return y
         ghat = ctypes.c_void_p(wsp + 256)
         W = ctypes.c_void_p(wsp + 256 + ((8 * nx + 255) // 256) * 256)
         if events:
