@@ -10,8 +10,10 @@
 //     a_p = y_{g^p}, FFT240 = radix 4 x 4 x 5 x 3;
 //   17-point DFTs down the 241 columns (direct odd codelet).
 // About 0.55x the FLOPs of the 8192-point Bluestein pair; 65.5 KB of shared
-// memory per mode, so three CTAs share an SM. Every stage runs in place: a
-// thread loads all of its butterflies, the CTA synchronises, then it stores.
+// memory per mode, so two CTAs share an SM. The 17 rows go one per warp
+// (warp-synchronous in-place stages: a lane loads its butterflies, the warp
+// synchronises, then it stores); CTA barriers only separate the row, column
+// and store phases of a mode.
 #pragma once
 
 namespace bhcp {
@@ -37,48 +39,45 @@ struct PfModesArgs {
   long long ntiles;
 };
 
-struct PfPlan { static constexpr int T = 256, MINB = 2; };   // the 17-point column codelet needs ~140 registers
+// 9 warps (at most two of the 17 rows each) and two CTAs per SM: 96
+// registers, some spills, but measured faster (c5: 464 us) than 8 warps with
+// a rotating third row (507 us) or 17 warps, one CTA per SM (490 us)
+struct PfPlan { static constexpr int T = 288, MINB = 2; };
 
-// One in-place Stockham stage of radix R over slots 1..240 of all 17 rows:
-// butterfly (row, b), b < 240/R, reads slots 1 + b + (240/R) r, twiddles
-// w240^{TWS k r} (k = b % Ns), writes slots 1 + (b - k) R + k + Ns r. Rounds
-// of whole rows (one butterfly per thread): a round's loads finish (CTA
-// barrier) before its stores, and different rounds touch different rows.
+// One in-place Stockham stage of radix R over slots 1..240 of one row, run by
+// one warp: butterfly b < 240/R (lanes b = lane + 32 i) reads slots
+// 1 + b + (240/R) r and twiddles them by w240^{TWS k r} (k = b % Ns); the warp
+// synchronises, then store(q, x) takes output q = (b - k) R + k + Ns r.
 template <int R, int Ns, class Store>
-__device__ __forceinline__ void pf_row_stage(double2* buf, const double2* __restrict__ w240, Store&& store) {
-  constexpr int NB = kPfNp / R, T = PfPlan::T, RPR = T / NB;
-  constexpr int TWS = kPfNp / (Ns * R);
-  static_assert(RPR >= 1, "one row per round at least");
-  const int lr = threadIdx.x / NB, b = threadIdx.x - lr * NB;
-  const int k = b % Ns;
-  double2 tw[R];
-  if (Ns > 1) {
+__device__ __forceinline__ void pf_warp_stage(const double2* rowp, int lane, const double2* __restrict__ w240,
+                                              Store&& store) {
+  constexpr int NB = kPfNp / R, PER = (NB + 31) / 32, TWS = kPfNp / (Ns * R);
+  double2 v[PER][R];
 #pragma unroll
-    for (int r = 1; r < R; ++r) tw[r] = w240[(TWS * k * r) % kPfNp];
-  }
-#pragma unroll 1
-  for (int r0 = 0; r0 < kPfRows; r0 += RPR) {
-    const int row = r0 + lr;
-    const bool act = lr < RPR && row < kPfRows;
-    double2 v[R];
-    double2* rowp = buf + row * kPfLen + 1;
-    if (act) {
+  for (int i = 0; i < PER; ++i) {
+    const int b = lane + 32 * i;
+    if (b < NB) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = rowp[b + NB * r];
+      for (int r = 0; r < R; ++r) v[i][r] = rowp[b + NB * r];
       if (Ns > 1) {
+        const int k = b % Ns;
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], tw[r]);
+        for (int r = 1; r < R; ++r) v[i][r] = cmul(v[i][r], w240[(TWS * k * r) % kPfNp]);
       }
-      sfft::Cod<R>::run(v);
-    }
-    __syncthreads();
-    if (act) {
-      const int base = (b - k) * R + k;
-#pragma unroll
-      for (int r = 0; r < R; ++r) store(rowp, base + Ns * r, v[r]);
+      sfft::Cod<R>::run(v[i]);
     }
   }
-  __syncthreads();
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int b = lane + 32 * i;
+    if (b < NB) {
+      const int k = b % Ns, base = (b - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) store(base + Ns * r, v[i][r]);
+    }
+  }
+  __syncwarp();
 }
 
 template <bool SYM>
@@ -134,40 +133,39 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
     const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
     const double c = __ldg(a.ghat + kd) * a.cscale;
     const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
-    // 1. generator in prime-factor order (slot 0: j2 = 0; slot 1 + p: j2 = g^p)
-    for (int i = threadIdx.x; i < NL; i += T) {
-      const double2 s = __ldg(a.shg + i);
-      const double dr = s.x + mu, di = s.y;
-      const double den2 = dr * dr + di * di;
-      if (den2 <= __ldg(a.thrg + i)) flag_singular(st, __ldg(a.jg + i));
-      const double inv = fast_rcp(den2);
-      buf[i] = make_double2(dr * inv, -di * inv);
+    // 1-4. rows, one warp per row (warp-synchronous, no CTA barrier): the
+    // generator in prime-factor order (slot 0: j2 = 0; slot 1 + p: j2 = g^p),
+    // A = FFT240(a), Y(row, 0) = y0 + A_0 kept aside, slots <- conj(A_k bhat_k),
+    // FFT240 again with the last stage storing y0 + conj(out_q) at slot
+    // t2 = g^-q.
+    for (int row = warp; row < kPfRows; row += T / 32) {
+      double2* rowb = buf + row * kPfLen;
+      double2* rowp = rowb + 1;
+#pragma unroll
+      for (int sl = lane; sl < kPfLen; sl += 32) {
+        const int i = row * kPfLen + sl;
+        const double2 s = __ldg(a.shg + i);
+        const double dr = s.x + mu, di = s.y;
+        const double den2 = dr * dr + di * di;
+        if (den2 <= __ldg(a.thrg + i)) flag_singular(st, __ldg(a.jg + i));
+        const double inv = fast_rcp(den2);
+        rowb[sl] = make_double2(dr * inv, -di * inv);
+      }
+      __syncwarp();
+      auto natural = [&](int q, double2 x) { rowp[q] = x; };
+      pf_warp_stage<4, 1>(rowp, lane, s_w, natural);
+      pf_warp_stage<4, 4>(rowp, lane, s_w, natural);
+      pf_warp_stage<5, 16>(rowp, lane, s_w, natural);
+      pf_warp_stage<3, 80>(rowp, lane, s_w, [&](int q, double2 x) {
+        if (q == 0) s_x0[row] = cadd(rowb[0], x);
+        rowp[q] = cconj(cmul(x, s_bh[q]));
+      });
+      pf_warp_stage<4, 1>(rowp, lane, s_w, natural);
+      pf_warp_stage<4, 4>(rowp, lane, s_w, natural);
+      pf_warp_stage<5, 16>(rowp, lane, s_w, natural);
+      pf_warp_stage<3, 80>(rowp, lane, s_w, [&](int q, double2 x) { rowp[s_tq[q] - 1] = cadd(rowb[0], cconj(x)); });
+      if (lane == 0) rowb[0] = s_x0[row];
     }
-    __syncthreads();
-    // 2. A = FFT240(a) per row
-    auto natural = [](double2* rowp, int q, double2 x) { rowp[q] = x; };
-    pf_row_stage<4, 1>(buf, s_w, natural);
-    pf_row_stage<4, 4>(buf, s_w, natural);
-    pf_row_stage<5, 16>(buf, s_w, natural);
-    pf_row_stage<3, 80>(buf, s_w, natural);
-    // 3. Y(row, 0) = y0 + A_0 kept aside; slots <- conj(A_k * bhat_k)
-    for (int i = threadIdx.x; i < kPfRows * kPfNp; i += T) {
-      const int row = i / kPfNp, k = i - row * kPfNp;
-      double2* p = buf + row * kPfLen + 1 + k;
-      const double2 A = *p;
-      if (k == 0) s_x0[row] = cadd(buf[row * kPfLen], A);
-      *p = cconj(cmul(A, s_bh[k]));
-    }
-    __syncthreads();
-    // 4. FFT240 again; the last stage stores y0 + conj(out_q) at slot t2 = g^-q
-    pf_row_stage<4, 1>(buf, s_w, natural);
-    pf_row_stage<4, 4>(buf, s_w, natural);
-    pf_row_stage<5, 16>(buf, s_w, natural);
-    {
-      // last stage: all loads of the CTA complete before the permuted stores
-      pf_row_stage<3, 80>(buf, s_w, [&](double2* rowp, int q, double2 x) { rowp[s_tq[q] - 1] = cadd(rowp[-1], cconj(x)); });
-    }
-    if (threadIdx.x < kPfRows) buf[threadIdx.x * kPfLen] = s_x0[threadIdx.x];
     __syncthreads();
     // 5. 17-point DFT down each of the 241 columns (one per thread), the
     //    symmetric odd-prime codelet with outputs stored as they are formed
@@ -226,6 +224,7 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
       }
       double* __restrict__ wd = wl.sl_base[sl] + pd;
       double* __restrict__ wmr = wl.sl_base[sl] + pm;
+#pragma unroll 4
       for (int t = t0 + threadIdx.x; t < t1; t += T, wd += step, wmr += step) {
         const double2 X = buf[(t % kPfRows) * kPfLen + (t % kPfLen)];
         const double2 g = __ldg(a.gaminv + t);
@@ -242,8 +241,6 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
     sim = fma(cc, zi2, sim);
     __syncthreads();   // buf is rewritten by the next mode
   }
-  (void)warp;
-  (void)lane;
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
     atomicAdd(&a.st->sum_re2, sre);
