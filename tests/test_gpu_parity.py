@@ -238,9 +238,11 @@ def test_result_semantics():
 
 @pytest.mark.parametrize("dim,cells,steps", [(1, 64, 63), (1, 100, 40), (2, 16, 16), (2, 20, 33), (3, 8, 8),
                                              (3, 12, 10),
-                                             # the specialised pass-A kernels: n = 257 (Rader), 513, 1025 / 4097 (Bluestein)
+                                             # the specialised pass-A kernels: n = 257 (Rader), 513 (Stockham),
+                                             # 1025 (Good-Thomas + Rader), 4097 (prime factor + Rader); 2D / 3D
+                                             # run their symmetric (mirror / permutation-class) tile lists
                                              (1, 32, 256), (2, 12, 256), (3, 6, 256), (2, 10, 512), (2, 8, 1024),
-                                             (1, 16, 4096)])
+                                             (3, 5, 1024), (1, 16, 4096), (2, 6, 4096), (3, 4, 4096)])
 @pytest.mark.parametrize("alpha", [1e-1, 1e-3, 1e-6])
 def test_solve_pint_sizes_vs_oracle(dim, cells, steps, alpha):
     w = workloads.make_small(dim, cells, steps, seed=cells + steps)
