@@ -1716,7 +1716,7 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
     cudaMemcpy(sp->snN, sn.data(), sizeof(double) * N, cudaMemcpyHostToDevice);
   }
   if (dim == 2) {
-    const int mt = (sp->m + 3) / 4;
+    const int mt = (sp->m + fastk::kSymTile - 1) / fastk::kSymTile;
     std::vector<int2> tiles;
     for (int a = 0; a < mt; ++a)
       for (int b = a; b < mt; ++b) tiles.push_back(make_int2(a, b));

@@ -40,6 +40,8 @@ struct GtModesArgs {
   long long ntiles;
 };
 
+// 12 warps at 168 registers; 8 warps (no spills, 231 registers) measured 12.2 ms
+// against 10.0 on c3
 struct GtPlan { static constexpr int S = 12, T = 384; };
 
 template <bool SYM>
