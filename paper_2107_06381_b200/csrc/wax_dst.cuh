@@ -73,7 +73,10 @@ struct CfgWX {
 // N = 1024 (c3) the y-side k_dst_cols3 (64 B rows here: 7.45 vs 6.5 ms).
 // N = 256 (c4): 32-line tiles (256 B rows), 17.8 ms per axis vs 20-22 ms.
 template <int N> struct PlanWX;
-template <> struct PlanWX<256> : CfgWX<256, 16, 512, 3, 1, 4, 8, 8> {};
+// c4, per pass: 256 threads (156 registers, no spills) 14.9-15.2 ms; 512 threads
+// (106 registers) 16.6-16.9; 128 / 384 / 1024 threads 16.8 / 17.3 / 22.8;
+// 16-line tiles at 2 CTAs per SM 17.4-18.6
+template <> struct PlanWX<256> : CfgWX<256, 16, 256, 3, 1, 4, 8, 8> {};
 
 constexpr int kBoxRows = 256;   // TMA box height (<= 256)
 
