@@ -2,9 +2,10 @@
 
 Contract (see the task statement): ``python bench.py --gpus N --steps K
 --warmup W`` prints ONE JSON line on rank 0. A "step" is one complete solve
-of BASELINE.json config 2 (2D pint-mqbvm, 511^2 interior, N = 512 steps,
-133,955,073 space-time DOFs) with the data g already resident in HBM; the
-metric is space-time DOFs/s over all ranks.
+of BASELINE.json config 3 -- the largest config that fits one GPU (2D
+pint-qbvm, 1023^2 interior, N = 1024 steps, 1,072,692,225 space-time DOFs) --
+with the data g already resident in HBM; the metric is space-time DOFs/s over
+all ranks. ``--config c1|c2|c4|c5`` runs the others.
 
 * value      -- K solves timed with CUDA events on the launching stream,
                 barrier + synchronize on both sides, max over ranks.
@@ -18,11 +19,13 @@ metric is space-time DOFs/s over all ranks.
                 roofline_hbm / kernels give every kernel's HBM fraction.
 * cpu_baseline -- the reference 3-step algorithm (oracle port, bit-identical
                 to the reference on the golden vectors) on a bounded sample of
-                the same workload, 1 host core, rank 0 at N=1.
+                the same workload (a fraction f of every per-unit operation,
+                extrapolated as elapsed / f), 1 host core = the reference's
+                default workers=None, rank 0 at N=1.
 * ``--impl reference`` times that CPU path with all host threads instead.
 
 N > 1: slab decomposition (mode slabs -> NCCL all-to-all -> level slabs),
-strong scaling of the one c2 problem over the ranks.
+strong scaling of the one problem over the ranks.
 """
 
 from __future__ import annotations
@@ -43,7 +46,12 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG_NAME = "c2"
+CONFIG_NAME = "c3"
+# fraction of every per-unit operation in the CPU samples: about 10-30 s of
+# one host core (cpu_baseline) and about 1-3 s of all host threads per
+# --impl reference step
+CPU_FRACTION = {"c1": 1.0, "c2": 1.0, "c3": 0.05, "c4": 0.01, "c5": 1.0}
+REF_FRACTION = {"c1": 1.0, "c2": 0.1, "c3": 0.03, "c4": 0.005, "c5": 0.5}
 METRIC = "space-time DOFs/s of QBVM/MQBVM all-at-once solve; % of HBM roofline"
 UNIT = "DOF/s"
 
@@ -55,8 +63,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=10)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default=CONFIG_NAME)
-    p.add_argument("--cpu-fraction", type=float, default=1.0,
-                   help="fraction of every per-unit operation in the CPU-baseline sample")
+    p.add_argument("--cpu-fraction", type=float, default=None,
+                   help="fraction of every per-unit operation in the CPU-baseline sample (default per config)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--quick", action="store_true", help="device timing only (no e2e / unfused / CPU legs)")
     return p.parse_args()
@@ -72,6 +80,12 @@ def peaks():
 
 def describe(name, w, kind, alpha) -> str:
     return f"{name}: {w.dim}D {kind}, {w.num_cells - 1}^{w.dim} interior x {w.n_levels} levels, alpha={alpha:g}"
+
+
+def config_of(name, w, kind, alpha) -> dict:
+    """The `config` object of both arms' lines (identical, so the driver can pair them)."""
+    return {"workload": describe(name, w, kind, alpha), "dof_per_solve": w.dof,
+            "l2": f"working set (W + y = {2 * 8 * w.dof / 1e9:.2f} GB) larger than the 126 MB L2; no flush"}
 
 
 def fp64_peak():
@@ -168,7 +182,7 @@ def run_reference(args, rank, world):
     w = workloads.make(args.config)
     kind, alpha = w.kinds[0], w.alphas[0]
     cores = os.cpu_count() or 1
-    frac = min(args.cpu_fraction, 0.1)  # each reference step: a 10% sample (~0.6 s on 16 threads)
+    frac = args.cpu_fraction if args.cpu_fraction is not None else REF_FRACTION.get(args.config, 0.05)
     for _ in range(args.warmup):
         cpu_sample(w, kind, alpha, frac / 4, cores)
     total_dof, total_s = 0.0, 0.0
@@ -177,14 +191,16 @@ def run_reference(args, rank, world):
         total_dof += dof
         total_s += s
     value = total_dof / total_s
-    sample = (f"{args.config}: per step, fraction {frac} of every per-unit op of the 3-step solve "
-              f"(time FFTs of {frac:.0%} of rows, shifted solves of {frac:.0%} of levels on {cores} threads)")
+    sample = (f"{args.config}: per step, fraction {frac} of every per-unit op of the reference 3-step solve "
+              f"(time FFTs of {frac:.1%} of the spatial rows, shifted solves incl. the singular-shift scan of "
+              f"{frac:.1%} of the levels on a {cores}-thread pool, back transform + residue + transposed copy of "
+              f"{frac:.1%} of the rows); DOF/s = {frac} * DOF / elapsed (every op is linear in rows/levels)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
-        "config": {"workload": describe(args.config, w, kind, alpha), "dof_per_solve": w.dof},
+        "config": config_of(args.config, w, kind, alpha),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -359,7 +375,9 @@ def main():
         # stream. Two trajectory buffers let step k's device->host copy overlap step
         # k+1's H2D + solve; the timed region ends when the last copy has landed.
         g_host = torch.from_numpy(w.g_delta).pin_memory()
-        y_hosts = [torch.empty((n, nx), dtype=torch.float64).pin_memory() for _ in range(2)]
+        # one pinned host trajectory (the copies serialise on copy_stream anyway)
+        y_host = torch.empty((n, nx), dtype=torch.float64).pin_memory()
+        y_hosts = [y_host, y_host]
         ys = [y, torch.empty_like(y)]
         g_e2e = torch.empty_like(g_dev)
         wsb = plan.ws_bytes
@@ -398,34 +416,42 @@ def main():
         e2e_ms = a0.elapsed_time(a1) / e2e_steps
         e2e_value = dof / (e2e_ms * 1e-3)
 
-        # ---- unfused literal 3-step dataflow for comparison (same kernels family)
-        yu, wsu = plan.solve_unfused_device(g_dev, divisor)
-        torch.cuda.synchronize()
-        u0 = torch.cuda.Event(enable_timing=True)
-        u1 = torch.cuda.Event(enable_timing=True)
-        u0.record()
-        for _ in range(3):
-            plan.solve_unfused_device(g_dev, divisor, out=yu)
-        u1.record()
-        torch.cuda.synchronize()
-        unfused_ms = u0.elapsed_time(u1) / 3
-        del yu, wsu
+        # ---- unfused literal 3-step dataflow for comparison (same kernels family;
+        # two complex (n, nx) intermediates: skipped above 2e9 DOF)
+        del y_hosts, y_host
+        unfused_ms = None
+        if dof <= 2e9:
+            yu, wsu = plan.solve_unfused_device(g_dev, divisor)
+            torch.cuda.synchronize()
+            u0 = torch.cuda.Event(enable_timing=True)
+            u1 = torch.cuda.Event(enable_timing=True)
+            u0.record()
+            for _ in range(3):
+                plan.solve_unfused_device(g_dev, divisor, out=yu)
+            u1.record()
+            torch.cuda.synchronize()
+            unfused_ms = u0.elapsed_time(u1) / 3
+            del yu, wsu
 
         cpu = None
         if not args.no_cpu_baseline:
-            dof_s, secs = cpu_sample(w, kind, alpha, args.cpu_fraction, None)
+            frac = args.cpu_fraction if args.cpu_fraction is not None else CPU_FRACTION.get(args.config, 0.05)
+            dof_s, secs = cpu_sample(w, kind, alpha, frac, None)
             cpu = {"value": dof_s / secs, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"{args.config}, fraction {args.cpu_fraction} of every per-unit op of the reference "
-                             f"3-step solve ({secs:.1f} s, single thread = reference default workers=None)"}
+                   "sample": f"{args.config}, fraction {frac} of every per-unit op of the reference 3-step solve "
+                             f"(time FFTs of {frac:.1%} of the spatial rows, shifted solves incl. the singular-shift "
+                             f"scan of {frac:.1%} of the levels, back transform + residue + transposed copy of "
+                             f"{frac:.1%} of the rows) in {secs:.1f} s on one thread (the reference default "
+                             f"workers=None); value = {frac} * DOF / elapsed, i.e. extrapolated linearly to the "
+                             f"full solve ({secs / frac:.0f} s)",
+                   "fraction": frac, "elapsed_s": secs, "extrapolated_full_solve_s": secs / frac}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json config construction)",
-            "config": {"workload": describe(args.config, w, kind, alpha),
-                       "dof_per_solve": dof,
-                       "l2": f"working set (W + y = {2 * 8 * dof / 1e9:.1f} GB) larger than L2; no flush",
-                       "timing": f"K replays of the CUDA graph of one step ({launches_per_step} kernels); phases_ms from an eager "
-                                 "pass of the same K steps with CUDA events"},
+            "config": config_of(args.config, w, kind, alpha),
+            "timing": f"K replays of the CUDA graph of one step ({launches_per_step} kernels); phases_ms from an eager "
+                      "pass of the same K steps with CUDA events",
             "roofline": roofline,
             "roofline_hbm": roof_hbm,
             "kernels": kernels,
@@ -444,7 +470,7 @@ def main():
         return
 
     # ---------------- N > 1: slab-decomposed solve
-    line = D.bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, METRIC, UNIT)
+    line = D.bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, METRIC, UNIT, config_of)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     dist.barrier()

@@ -215,10 +215,16 @@ int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, 
  *   and m + 1 in {256, 512} (bhcp_pint_w_passes_supported), W 16-byte
  *   aligned.
  * bhcp_pint_levels / bhcp_pint_levels_blocked: all spatial passes, W (or the
- *   receive buffer) -> y. When bhcp_pint_w_passes_supported, the strided axes
- *   run first in place on the input (which is therefore overwritten), then
- *   pass 0; otherwise passes 0..dim-1 as above and the input is untouched.
- *   levels_blocked needs dim >= 2. */
+ *   receive buffer) -> y. levels_blocked needs dim >= 2; its koff_dev is
+ *   either NULL -- k1 blocks at the uniform stride NT * P1 * 8, the layout
+ *   bhcp_pint_modes / _modes_to / _modes_sym_to write for one level slab --
+ *   or a device int64 table of m block offsets, which may be arbitrary.
+ *   Uniform input (bhcp_pint_levels, or koff_dev NULL): when
+ *   bhcp_pint_w_passes_supported, the strided axes run first in place on the
+ *   input (which is therefore overwritten), then the last axis into y, all on
+ *   TMA views of the one stride. An explicit table runs the general passes
+ *   (pass 0 into y, then the strided axes on y) and leaves the input
+ *   untouched. */
 int bhcp_pint_ghat(const bhcp_space_plan* sp, const double* g_dev, double scale,
                    double* ghat_dev, void* stream);
 int bhcp_pint_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp,

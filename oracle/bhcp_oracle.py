@@ -313,11 +313,21 @@ def solve_pint_sample(kind, alpha, dim, length, num_cells, horizon, num_steps, d
     """Time the reference 3-step solve (pint.py:89-99) on a bounded sample.
 
     The sample performs a fraction ``f`` of every per-unit operation of the
-    full solve: step (a) time transforms of ceil(f*N_x) spatial rows
-    (circulant.py:106), step (b) shifted solves of ceil(f*N_t) columns
-    (pint.py:59-65, with a ThreadPoolExecutor of ``workers`` threads exactly
-    like the reference's optional pool), step (c) back transforms + residue of
-    ceil(f*N_x) rows (circulant.py:115, 182-190). Returns
+    full solve, with the reference's own memory layouts:
+
+    * step (a): the rhs rows (methods.py:158-162) and the time transforms of
+      ceil(f*N_x) spatial rows (circulant.py:99-106);
+    * step (b): ceil(f*N_t) columns j, each read as a strided column of the
+      (N_x, cols) S1 block and written back as one (pint.py:52-61), each with
+      the per-column singular-shift scan (space.py:234-246, 273) and the
+      spectral solve (space.py:276-278); a ThreadPoolExecutor of ``workers``
+      threads exactly like the reference's optional pool (pint.py:62-65);
+    * step (c): the back transform of ceil(f*N_x) rows, both residue norms,
+      the real part (circulant.py:108-115, 182-190) and the transposed
+      contiguous copy of the trajectory rows (pint.py:99).
+
+    Every operation is linear in the number of rows or columns it touches, so
+    the full-solve time is extrapolated as elapsed / f. Returns
     (dof_equivalent, seconds) with dof_equivalent = f * N_t * N_x.
     """
     import time
@@ -333,17 +343,21 @@ def solve_pint_sample(kind, alpha, dim, length, num_cells, horizon, num_steps, d
     mu = mode_eigenvalues(dim, length, num_cells)
     rows = max(1, int(np.ceil(fraction * nx)))
     cols = max(1, int(np.ceil(fraction * n)))
+    # S1 columns: column j of S1 is rhs_0 / sqrt(n) (the exact step-(a) output;
+    # the values do not change the work)
+    col = (data / condition_divisor(kind, alpha, tau) / np.sqrt(n)).astype(np.complex128)
+    s1 = np.empty((nx, cols), dtype=np.complex128)
+    s1[:] = col[:, None]
     start = time.perf_counter()
     # (a) rhs block rows (methods.py:158-162) and their time transform
     rhs_rows = np.zeros((rows, n))
     rhs_rows[:, 0] = data[:rows] / condition_divisor(kind, alpha, tau)
     s1_rows = to_eigenspace(rhs_rows, gamma)
-    # (b) full spatial columns; column j of S1 is rhs_0 / sqrt(n) (the values
-    # do not change the work; they are the exact step-(a) output)
-    col = (data / condition_divisor(kind, alpha, tau) / np.sqrt(n)).astype(np.complex128)
 
     def solve_column(j):
-        coeffs = sine_transform(col, dim, m)
+        if check_shifts(np.array([shifts[j]]), mu) >= 0:
+            raise SingularShift(f"column {j}")
+        coeffs = sine_transform(s1[:, j], dim, m)
         return sine_transform(coeffs / (shifts[j] + mu), dim, m)
 
     out = np.empty((nx, cols), dtype=np.complex128)
@@ -354,10 +368,10 @@ def solve_pint_sample(kind, alpha, dim, length, num_cells, horizon, num_steps, d
         with ThreadPoolExecutor(max_workers=workers) as pool:
             for j, c in enumerate(pool.map(solve_column, range(cols))):
                 out[:, j] = c
-    # (c) back transform of sample rows + residue norms
+    # (c) back transform of sample rows + residue norms + real part + transposed copy
     back = apply_basis(s1_rows, gamma)
     _ = np.linalg.norm(back), np.linalg.norm(back.imag)
-    _ = np.ascontiguousarray(back.real)
+    _ = np.ascontiguousarray(np.ascontiguousarray(back.real).T)
     elapsed = time.perf_counter() - start
     return fraction * n * nx, elapsed
 

@@ -1068,7 +1068,6 @@ int launch_time(const bhcp_time_plan* tp, int mode, const double* in, int in_cpl
   return BHCP_OK;
 }
 
-std::mutex g_tile_mutex;
 
 // Symmetric work list of the Bluestein modes kernel: 2D tiles (k1, k2a) cover
 // k2 in [k2a, k2a+S) with k2 >= k1; 3D tiles (k1, k2, k3a) with k1 <= k2 cover
@@ -1084,35 +1083,82 @@ struct SymRange {
 // six = true (3D): tiles (k1, k2, k3a) of sorted triples k1 <= k2 <= k3, k3 in
 // [k3a, k3a + S) with k3a stepping from k2 rounded down to S (k_modes_rader's
 // one-FFT-per-permutation-class work list)
-const int4* seg_tiles(const bhcp_space_plan* sp_c, int S, long long* count, bool six = false) {
-  auto* sp = const_cast<bhcp_space_plan*>(sp_c);
-  std::lock_guard<std::mutex> lk(g_tile_mutex);
-  const int key = six ? S + 1000 : S;
-  int slot = 0;
-  while (slot < 9 && sp->seg_tiles[slot] && sp->seg_len[slot] != key) ++slot;
-  if (slot >= 9 || S < 1) return nullptr;
-  if (!sp->seg_tiles[slot]) {
-    sp->seg_len[slot] = key;
-    std::vector<int4> t;
-    const int m = sp->m;
-    if (six && sp->dim == 3) {
-      for (int k1 = 0; k1 < m; ++k1)
-        for (int k2 = k1; k2 < m; ++k2)
-          for (int k3a = k2 - k2 % S; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
-    } else if (sp->dim == 2) {
-      for (int k1 = 0; k1 < m; ++k1)
-        for (int k2a = k1 - k1 % S; k2a < m; k2a += S) t.push_back(make_int4(k1, k2a, 0, 0));
-    } else {
-      for (int k1 = 0; k1 < m; ++k1)
-        for (int k2 = k1; k2 < m; ++k2)
-          for (int k3a = 0; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
-    }
-    if (cudaMalloc(&sp->seg_tiles[slot], sizeof(int4) * t.size()) != cudaSuccess) return nullptr;
-    cudaMemcpy(sp->seg_tiles[slot], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice);
-    sp->seg_count[slot] = (long long)t.size();
+std::vector<int4> seg_list(int dim, int m, int S, bool six) {
+  std::vector<int4> t;
+  if (six && dim == 3) {
+    for (int k1 = 0; k1 < m; ++k1)
+      for (int k2 = k1; k2 < m; ++k2)
+        for (int k3a = k2 - k2 % S; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
+  } else if (dim == 2) {
+    for (int k1 = 0; k1 < m; ++k1)
+      for (int k2a = k1 - k1 % S; k2a < m; k2a += S) t.push_back(make_int4(k1, k2a, 0, 0));
+  } else {
+    for (int k1 = 0; k1 < m; ++k1)
+      for (int k2 = k1; k2 < m; ++k2)
+        for (int k3a = 0; k3a < m; k3a += S) t.push_back(make_int4(k1, k2, k3a, 0));
   }
-  *count = sp->seg_count[slot];
-  return sp->seg_tiles[slot];
+  return t;
+}
+
+// Number of tiles of seg_list without building it.
+long long seg_list_count(int dim, int m, int S, bool six) {
+  long long c = 0;
+  if (six && dim == 3) {
+    for (int k1 = 0; k1 < m; ++k1)
+      for (int k2 = k1; k2 < m; ++k2) c += (m - (k2 - k2 % S) + S - 1) / S;
+  } else if (dim == 2) {
+    for (int k1 = 0; k1 < m; ++k1) c += (m - (k1 - k1 % S) + S - 1) / S;
+  } else {
+    c = (long long)m * (m + 1) / 2 * ((m + S - 1) / S);
+  }
+  return c;
+}
+
+// Symmetric work lists are built once, at space-plan creation (plans are
+// immutable afterwards: no allocation or synchronous copy on the enqueue path,
+// so a solve can be captured into a CUDA graph on a fresh plan). The segment
+// lengths are those of the symmetric pass-A kernels: Good-Thomas / Rader (12,
+// 3D Rader: sorted triples), prime-factor (1), Bluestein (8, 2, 1). A list
+// above kSegCapBytes is not built; its kernel then runs the non-symmetric
+// variant (every mode its own FFT).
+constexpr long long kSegCapBytes = 64LL << 20;
+struct SegKey { int S; bool six; };
+constexpr SegKey kSegKeys[] = {{12, false}, {12, true}, {1, false}, {8, false}, {2, false}};
+
+constexpr bool seg_key_listed(int S, bool six) {
+  for (const SegKey& k : kSegKeys)
+    if (k.S == S && k.six == six) return true;
+  return false;
+}
+
+int build_seg_tiles(bhcp_space_plan* sp) {
+  if (sp->dim < 2) return BHCP_OK;
+  int slot = 0;
+  for (const SegKey& k : kSegKeys) {
+    if (k.six && sp->dim != 3) continue;
+    if (slot >= 9) break;
+    if (seg_list_count(sp->dim, sp->m, k.S, k.six) * (long long)sizeof(int4) > kSegCapBytes) continue;
+    const std::vector<int4> t = seg_list(sp->dim, sp->m, k.S, k.six);
+    if (t.empty()) continue;
+    if (cudaMalloc(&sp->seg_tiles[slot], sizeof(int4) * t.size()) != cudaSuccess) return cuda_fail("cudaMalloc seg tiles");
+    if (cudaMemcpy(sp->seg_tiles[slot], t.data(), sizeof(int4) * t.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+      return cuda_fail("seg tiles upload");
+    sp->seg_len[slot] = k.six ? k.S + 1000 : k.S;
+    sp->seg_count[slot] = (long long)t.size();
+    ++slot;
+  }
+  return BHCP_OK;
+}
+
+// lookup only (built by build_seg_tiles); nullptr when the plan has no such list
+const int4* seg_tiles(const bhcp_space_plan* sp, int S, long long* count, bool six = false) {
+  const int key = six ? S + 1000 : S;
+  for (int slot = 0; slot < 9; ++slot)
+    if (sp->seg_tiles[slot] && sp->seg_len[slot] == key) {
+      *count = sp->seg_count[slot];
+      return sp->seg_tiles[slot];
+    }
+  return nullptr;
 }
 
 // apply a tile window to a symmetric work list
@@ -1131,6 +1177,12 @@ inline void window(const SymRange& sr, const int2*& tiles, long long& cnt) {
   cnt = e - b;
 }
 
+static_assert(seg_key_listed(fastk::GtPlan::S, false) && seg_key_listed(fastk::RaderPlan<257>::S, false) &&
+                  seg_key_listed(fastk::RaderPlan<257>::S, true) && seg_key_listed(1, false) &&
+                  seg_key_listed(fastk::BluePlan<257>::S, false) && seg_key_listed(fastk::BluePlan<1025>::S, false) &&
+                  seg_key_listed(fastk::BluePlan<4097>::S, false),
+              "every symmetric pass-A kernel's segment length has a prebuilt list");
+
 int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
              long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s,
              const SymRange& sr = SymRange()) {
@@ -1141,10 +1193,10 @@ int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
   a.st = st; a.wl = wl; a.tab = tp->gt; a.itab = tp->gt_idx;
   const size_t sm = gt_smem();
   const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
-  if (sym) {
-    long long cnt = 0;
-    a.tiles = seg_tiles(sp, GtPlan::S, &cnt);
-    if (!a.tiles) return cuda_fail("seg tiles");
+  long long cnt = 0;
+  a.tiles = sym ? seg_tiles(sp, GtPlan::S, &cnt) : nullptr;
+  if (sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
+  if (a.tiles) {
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
@@ -1169,10 +1221,10 @@ int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
   a.m = sp->m; a.dim = sp->dim; a.st = st; a.tab = tp->pf; a.tq = tp->pf_idx; a.wl = wl;
   const size_t sm = pf_smem();
   const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
-  if (sym) {
-    long long cnt = 0;
-    a.tiles = seg_tiles(sp, 1, &cnt);
-    if (!a.tiles) return cuda_fail("seg tiles");
+  long long cnt = 0;
+  a.tiles = sym ? seg_tiles(sp, 1, &cnt) : nullptr;
+  if (sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
+  if (a.tiles) {
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
@@ -1199,11 +1251,11 @@ int rader_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const doubl
   a.tw = tp->rader; a.bhat = tp->rader + Pl::NP; a.perm = tp->rader_idx; a.qidx = tp->rader_idx + Pl::NP;
   const size_t sm = rader_smem<NL>();
   const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
-  if (sym) {
-    long long cnt = 0;
-    a.sym6 = sp->dim == 3 ? 1 : 0;
-    a.tiles = seg_tiles(sp, Pl::S, &cnt, a.sym6 != 0);
-    if (!a.tiles) return cuda_fail("seg tiles");
+  long long cnt = 0;
+  a.sym6 = sp->dim == 3 ? 1 : 0;
+  a.tiles = sym ? seg_tiles(sp, Pl::S, &cnt, a.sym6 != 0) : nullptr;
+  if (sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
+  if (a.tiles) {
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
@@ -1233,10 +1285,10 @@ int blue_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double
   a.bt.cg = tp->blue + 2 * L + 2 * NL; a.bt.wg = tp->blue + 2 * L + 3 * NL; a.bt.thr = tp->blue + 2 * L + 4 * NL;
   const size_t sm = blue_smem<NL>();
   const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
-  if (sym) {
-    long long cnt = 0;
-    a.tiles = seg_tiles(sp, Pl::S, &cnt);
-    if (!a.tiles) return cuda_fail("seg tiles");
+  long long cnt = 0;
+  a.tiles = sym ? seg_tiles(sp, Pl::S, &cnt) : nullptr;
+  if (sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
+  if (a.tiles) {
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
@@ -1609,23 +1661,26 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
   return fail(BHCP_ERR_INVALID, "w_pass length");
 }
 
-// All spatial passes of the fused solve: W (blocked, consumed) -> y.
-// Fast lengths in 2D/3D: the strided axes in place on W (k_dst_wax), then
-// the last axis W -> y (k_dst_blk2). Otherwise pass 0 into y, then the
-// strided axes in place on y.
+// All spatial passes of the fused solve: W (blocked) -> y.
+// koff == null: k1 blocks at the uniform stride NT * P1 * 8 (the single-slab
+// W and every slab receive buffer). Fast lengths in 2D/3D then run the strided
+// axes in place on W (k_dst_wax / k_dst_wax2; W is consumed) and the last
+// axis W -> y (k_dst_blk3 / k_dst_blk4), all on TMA views that need that one
+// stride. koff != null: an explicit k1 -> block offset table, honoured by the
+// general passes (pass 0 into y by k_dst_blk2 / unpack + rows, then the
+// strided axes in place on y); W is left untouched.
 int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, double* y, long long nlev,
                cudaStream_t s) {
-  if (wax_ok(sp)) {
+  if (!koff && wax_ok(sp)) {
     for (int a = 0; a < sp->dim - 1; ++a) {
       int rc = w_pass(sp, W, nlev, a, s);
       if (rc) return rc;
     }
-    return blk3_launch(sp, W, y, nlev, s);   // k1 blocks at the uniform stride
-    return level_pass(sp, W, koff, y, nlev, 0, s);
+    return blk3_launch(sp, W, y, nlev, s);
   }
   for (int p = 0; p < sp->dim; ++p) {
-    // m + 1 = 1024: the last axis by k_dst_blk4 (k1 blocks at the uniform stride), then y-side passes
-    const bool blk4 = p == 0 && !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && sp->m + 1 == 1024;
+    // m + 1 = 1024: the last axis by k_dst_blk4 (uniform k1 stride), then y-side passes
+    const bool blk4 = p == 0 && !koff && !g_disable_fast && sp->dim >= 2 && sp->dim <= 3 && sp->m + 1 == 1024;
     int rc = blk4 ? blk3_launch(sp, W, y, nlev, s) : level_pass(sp, W, koff, y, nlev, p, s);
     if (rc) return rc;
   }
@@ -1725,6 +1780,11 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
       free_fft_plan(&sp->dst); cudaFree(sp->mu1_dev); delete sp; return cuda_fail("cudaMalloc tiles");
     }
     cudaMemcpy(sp->tiles_dev, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice);
+  }
+  if (const int rc = build_seg_tiles(sp); rc != BHCP_OK) {
+    const std::string msg = g_last_error;
+    bhcp_space_plan_destroy(sp);
+    return fail(rc, msg);
   }
   if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {   // a failed table upload
     bhcp_space_plan_destroy(sp);
@@ -2108,7 +2168,7 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
 
 int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev, const int64_t* koff_dev,
                              double* out_dev, int64_t batch, void* stream) {
-  if (!sp || !in_dev || !koff_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (!sp || !in_dev || !out_dev || batch < 0) return fail(BHCP_ERR_INVALID, "bad argument");
   if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
   DeviceGuard g(sp->device);
   return levels_all(sp, in_dev, (const long long*)koff_dev, out_dev, batch, as_stream(stream));

@@ -427,6 +427,7 @@ __global__ void __launch_bounds__(ModesPlan<N>::T, ModesPlan<N>::MINB) k_modes_f
     const double cc = c * c + c2 * c2;
     sre = fma(cc, zr2, sre);
     sim = fma(cc, zi2, sim);
+    __syncwarp();   // the store loop's trip count differs across lanes; buf is rewritten by the next mode
   }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {

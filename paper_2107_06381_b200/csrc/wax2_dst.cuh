@@ -76,14 +76,18 @@ __device__ __forceinline__ void store_pair(bool sw, double2* pe, double2 ev, dou
       "r"((unsigned)has_ev), "d"(od.x), "d"(od.y), "d"(ev.x), "d"(ev.y), "r"(su32(po)), "r"(su32(pe))
       : "memory");
 }
-// Relaxed arrive: orders nothing, so it does not wait for the warp's global
-// stores to drain. Used where the only hazard is the buffer's shared-memory
-// reads, which have completed (their values feed the stores issued before).
-__device__ __forceinline__ void mbar_arrive_relaxed(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
-}
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(bar)) : "memory");
+}
+// Hand a tile buffer back to the TMA producer after the warp rewrote it in
+// place through generic-proxy shared-memory stores (padding zeroing, Stockham
+// stages): the proxy fence orders those stores before the producer's next
+// async-proxy (cp.async.bulk.tensor) write into the buffer, and the release
+// arrive publishes them to the producer's acquiring wait.
+__device__ __forceinline__ void release_buffer(unsigned long long* bar, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
 }
 
 // TMA-swizzled tiles of 16-byte chunks (one chunk = one line pair):
@@ -814,7 +818,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk3(const __grid_con
     const long long rowb = rowa + (long long)m * m * a.idiv;
     RowSink<> sink{a.y + rowa, a.y + rowb, t0 < a.nlev, t0 + 1 < a.nlev, K.j1, K.j2};
     ColDst<N>::template run<Sw64>(T, q, K, sn, sink);
-    if (lane == 0) mbar_arrive_relaxed(done + b);
+    release_buffer(done + b, lane);
   }
 }
 
@@ -890,8 +894,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk4(const __grid_con
     const long long rowb = rowa + m * m * b3.idiv;
     RowSink<128> sink{b3.y + rowa, b3.y + rowb, !za, !zb, K.j1, K.j2};
     warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
-    __syncwarp();
-    if (lane == 0) mbar_arrive_relaxed(done + b);
+    release_buffer(done + b, lane);
   }
 }
 

@@ -352,7 +352,8 @@ class DeviceOps:
         if self._y is None or self._y.shape != (L, self.nx):
             self._y = torch.empty((L, self.nx), dtype=torch.float64, device=self.g.device)
         if L > 0:
-            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), p.ptr(koff),
+            # tables() verified koff is the uniform stride: pass NULL so the TMA passes run
+            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), None,
                                                               p.ptr(self._y), L, p.stream_handle()),
                             "levels_blocked")
         return self._y
@@ -420,7 +421,7 @@ def _nvlink_stats(nbytes: float, ms: float, transport: str) -> dict:
             "achieved_GBps": gbps, "peak_GBps": 770.0, "frac": gbps / 770.0}
 
 
-def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric, unit):
+def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric, unit, config_of):
     import torch
     import torch.distributed as dist
 
@@ -509,14 +510,12 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json config construction)",
-        "config": {"workload": f"{args.config}: {grid.dim}D {system.method.kind.value} {grid.num_cells - 1}^{grid.dim} x "
-                               f"{tg.n_levels} levels, slab-decomposed over {world} GPUs",
-                   "dof_per_solve": w.dof, "transport": transport,
-                   "parallelism": (f"pass A over 1/P of the mirror-pair tiles (or a k1 slab) storing into the "
-                                   f"level-slab owners over NVLink peer memory -> level slabs, P={world}")
-                                  if peer is not None else
-                                  f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
-                   "l2": "working set larger than L2; no flush"},
+        "config": config_of(args.config, w, system.method.kind.value, system.method.alpha),
+        "transport": transport,
+        "parallelism": (f"pass A over 1/P of the mirror-pair tiles (or a k1 slab) storing into the "
+                        f"level-slab owners over NVLink peer memory -> level slabs, P={world}")
+                       if peer is not None else
+                       f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
         "roofline": {"bound": "hbm", "kernel": ["pass A (k_modes_fast)", "", "pass B (level passes)"][dom],
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": kind},

@@ -139,9 +139,10 @@ class PintPlan:
     def capture(self, g: torch.Tensor, divisor: float, out: torch.Tensor) -> "torch.cuda.CUDAGraph":
         """Capture one fused solve (g -> out, fixed buffers) into a CUDA graph;
         ``graph.replay()`` then re-runs status reset, ghat, pass A and the level
-        passes with a single launch from the host. The solve runs once eagerly
-        first so every lazily built device table exists before capture."""
-        self.solve_device(g, divisor, out=out)
+        passes with a single launch from the host. Plans are immutable (every
+        device table, symmetric tile lists included, is built at plan
+        creation), so a fresh plan captures without an eager solve first."""
+        self.workspace()
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
         side = torch.cuda.Stream()
@@ -156,10 +157,16 @@ class PintPlan:
         ws = self.workspace()
         return ctypes.c_void_p(ws.data_ptr())
 
-    def check_status(self, tol: float = RESIDUE_TOL) -> _lib.Status:
+    def read_status(self, tol: float = RESIDUE_TOL) -> _lib.Status:
+        """The status block of the last solve (synchronises): code, first singular
+        column, ||Im Y|| (residue) and ||Y|| (norm) of circulant.py:182-185."""
         st = _lib.Status()
         _lib.check(_lib.lib().bhcp_read_status(self.status_ptr(), tol, ctypes.byref(st), plans.stream_handle()),
                    "bhcp_read_status")
+        return st
+
+    def check_status(self, tol: float = RESIDUE_TOL) -> _lib.Status:
+        st = self.read_status(tol)
         if st.code == _lib.BHCP_ERR_SINGULAR_SHIFT:
             j = int(st.bad_column)
             raise SingularShiftError(f"column {j}: {singular_message(complex(self.shifts[j]))}")
@@ -224,12 +231,14 @@ def solve_pint(system, backend: str = "spectral", workers: Optional[int] = None)
     g = plans.to_device(system.data, torch.float64)
     events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     y = plan.solve_device(g, divisor, events=events)
-    plan.check_status()  # synchronises
+    st = plan.check_status()  # synchronises; raises under circulant.py:182-189
     t_a = events[0].elapsed_time(events[1]) / 1e3
     t_b = events[1].elapsed_time(events[2]) / 1e3
     t_c = events[2].elapsed_time(events[3]) / 1e3
     timings = {"step_a": t_a, "step_b": t_b, "step_c": t_c, "total": t_a + t_b + t_c}
-    return SolveResult(system=system, trajectory=None, solver="pint", timings=timings, trajectory_device=y)
+    res = SolveResult(system=system, trajectory=None, solver="pint", timings=timings, trajectory_device=y)
+    res.residue_ratio = float(st.residue / st.norm) if st.norm > 0 else 0.0   # ||Im Y|| / ||Y||
+    return res
 
 
 def solve_pint_unfused(system) -> SolveResult:

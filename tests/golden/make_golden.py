@@ -17,6 +17,12 @@ reference's own code path on seeded inputs (names say which function):
   oracle_*      baseline.solve_spectral_oracle   (baseline.py:67-112)
   march_*       baseline.march_forward           (baseline.py:115-129)
   c1_*          BASELINE config 1 inputs/outputs (seeded, see workloads.py)
+  trip_*        the imaginary-residue tripwire of from_eigenspace (circulant.py:
+                182-189): the reference's raise / no-raise decision and its
+                residue ratio ||Im Y|| / ||Y|| for the noise-free ex1 rows that
+                the reference driver records as failed (pkg/test_output.txt:
+                118-119; alpha = the 1e-12 fallback of bench.py:49-83), and for
+                BASELINE c1 and c5 pint-qbvm at alpha = 1e-6 (no raise)
 """
 import sys
 from pathlib import Path
@@ -29,6 +35,12 @@ from bhcp.circulant import TimeGrid, diagonalize, from_eigenspace, to_eigenspace
 from bhcp.methods import MethodKind, assemble  # noqa: E402
 from bhcp.pint import solve_pint, step_b_parallel  # noqa: E402
 from bhcp.space import build_grid, laplacian_eigenvalues, shifted_solve, sine_transform  # noqa: E402
+from bhcp.analysis import get_problem  # noqa: E402
+from bhcp.bench import resolve_alpha  # noqa: E402
+from bhcp.circulant import ImaginaryResidueError  # noqa: E402
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+from paper_2107_06381_b200 import workloads  # noqa: E402  (host-side seeded input generator)
 
 OUT = Path(__file__).with_name("golden.npz")
 g = {}
@@ -126,6 +138,41 @@ g["c1_g"] = gclean
 g["c1_gdelta"] = gdelta
 g["c1_pint"] = res.trajectory
 g["c1_oracle"] = solve_spectral_oracle(MethodKind.PINT_QBVM, alpha, grid, tg, gdelta).trajectory
+
+
+
+# --- the imaginary-residue tripwire (circulant.py:182-189)
+def residue_case(key, kind, alpha, grid, tg, data):
+    """Run the reference solve_pint; record whether it raised and its ratio."""
+    sysm = assemble(kind, alpha, grid, tg, data)
+    try:
+        solve_pint(sysm)
+        raised = 0
+    except ImaginaryResidueError:
+        raised = 1
+    # the same quantity the reference tests: ||Im Y|| / ||Y|| of Y = apply_basis(S2)
+    diag = diagonalize(tg.n_levels, sysm.omega)
+    s1 = to_eigenspace(sysm.rhs().reshape(tg.n_levels, grid.n_interior).T, diag)
+    s2 = step_b_parallel(grid, s1, diag.eigenvalues / tg.tau)
+    out = diag.apply_basis(s2)
+    ratio = np.linalg.norm(out.imag) / max(np.linalg.norm(out), np.finfo(float).tiny)
+    g[f"trip_{key}_{kind.value}"] = np.array([raised, ratio, alpha])
+
+
+ex1 = get_problem("ex1")
+trip_meshes = [(8, 8), (16, 8), (16, 16), (32, 32), (64, 64)]
+for M, N in trip_meshes:
+    grid = build_grid(1, np.pi, M)
+    tg = TimeGrid(1.0, N)
+    data = ex1.final_on_grid(grid)
+    g[f"trip_ex1_{M}_{N}_data"] = data
+    for kind in (MethodKind.PINT_QBVM, MethodKind.PINT_MQBVM):
+        residue_case(f"ex1_{M}_{N}", kind, resolve_alpha("auto", kind, 0.0, tg.tau), grid, tg, data)
+residue_case("c1", MethodKind.PINT_QBVM, 1e-3, build_grid(1, np.pi, 256), TimeGrid(1.0, 256), gdelta)
+w5 = workloads.make("c5")
+for alpha in (1e-6, 1e-1):
+    for kind in (MethodKind.PINT_QBVM, MethodKind.PINT_MQBVM):
+        residue_case(f"c5_{alpha:g}", kind, alpha, build_grid(1, np.pi, 4096), TimeGrid(1.0, 4096), w5.g_delta)
 
 np.savez_compressed(OUT, **g)
 print(f"wrote {OUT} with {len(g)} arrays, {OUT.stat().st_size / 1e6:.2f} MB")

@@ -59,12 +59,18 @@ def run_levels(sp, W_host, L, dim, m, how):
         else:
             for p in range(dim):
                 _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, p, sh), "level pass")
+    elif how == "blocked":
+        # an all-to-all receive buffer at the uniform k1 stride (koff NULL): the TMA passes
+        _lib.check(lib.bhcp_pint_levels_blocked(sp, plans.ptr(W), None, plans.ptr(y), L, sh), "levels_blocked")
     else:
-        # an all-to-all receive buffer: k1 blocks at koff[k1] (block_tables' uniform stride)
+        # an explicit, non-uniform k1 -> block table: the k1 blocks stored in reverse
+        # order; the general passes honour it
         nt = (L + TB - 1) // TB
-        koff = torch.arange(m, dtype=torch.int64, device="cuda") * (nt * m ** (dim - 1) * TB)
-        _lib.check(lib.bhcp_pint_levels_blocked(sp, plans.ptr(W), plans.ptr(koff), plans.ptr(y), L, sh),
-                   "levels_blocked")
+        blk = nt * m ** (dim - 1) * TB
+        Wr = W.view(m, blk).flip(0).contiguous().view(-1)
+        koff = (m - 1 - torch.arange(m, dtype=torch.int64, device="cuda")) * blk
+        _lib.check(lib.bhcp_pint_levels_blocked(sp, plans.ptr(Wr), plans.ptr(koff), plans.ptr(y), L, sh),
+                   "levels_blocked table")
     torch.cuda.synchronize()
     return y.cpu().numpy()
 
@@ -91,6 +97,8 @@ def test_level_passes_vs_oracle(dim, cells, L):
     # all-to-all receive-buffer entry point give the same bits
     assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "passes"), y)
     assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "blocked"), y)
+    yt = run_levels(plan.handle, W, L, dim, m, "table")
+    assert rel(yt, ref) <= 1e-13, "explicit block table"
 
 
 @pytest.mark.parametrize("dim,cells", [(2, 512), (3, 256)])

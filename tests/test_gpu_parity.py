@@ -434,9 +434,12 @@ def test_zero_data_zero_trajectory_fast_kernels(dim, cells, steps):
     assert not res.trajectory_device.any().item()
 
 
-@pytest.mark.parametrize("dim,cells,steps", [(1, 256, 256), (2, 40, 30), (2, 64, 512)])
+@pytest.mark.parametrize("dim,cells,steps", [(1, 256, 256), (2, 40, 30), (2, 64, 512), (2, 40, 1024),
+                                             (3, 12, 256), (2, 24, 4096), (3, 10, 1024)])
 def test_graph_replay_matches_eager(dim, cells, steps):
-    """PintPlan.capture: the CUDA-graph replay of the fused solve gives the
+    """PintPlan.capture on a FRESH plan (no eager solve before the capture: the
+    symmetric tile lists of the Rader / Good-Thomas / prime-factor pass A are
+    built at plan creation): the CUDA-graph replay of the fused solve gives the
     eager bits, and a new g copied into the captured input buffer is used."""
     w = workloads.make_small(dim, cells, steps, seed=9)
     grid = B.build_grid(dim, w.length, cells)

@@ -137,3 +137,32 @@ def test_3d_pint_restatement_matches_closed_form():
         traj, _ = O.solve_pint(kind, 1e-2, 3, 1.0, cells, 0.05, steps, data)
         orc = O.spectral_oracle(kind, 1e-2, 3, 1.0, cells, 0.05, steps, data)
         assert rel(traj, orc) < 1e-12
+
+
+@pytest.mark.parametrize("mesh", [(8, 8), (16, 8), (16, 16), (32, 32), (64, 64)])
+@pytest.mark.parametrize("kind", [O.PINT_QBVM, O.PINT_MQBVM])
+def test_residue_tripwire_like_reference(golden, mesh, kind):
+    """circulant.py:182-189 on the reference's own noise-free ex1 rows (alpha =
+    1e-12 fallback): the oracle raises exactly where the reference raised and
+    reports the reference's residue ratio bit for bit."""
+    M, N = mesh
+    raised_ref, ratio_ref, alpha = golden[f"trip_ex1_{M}_{N}_{kind}"]
+    data = golden[f"trip_ex1_{M}_{N}_data"]
+    try:
+        _, ratio = O.solve_pint(kind, alpha, 1, np.pi, M, 1.0, N, data)
+        raised = False
+    except O.ResidueError:
+        raised = True
+    tau = 1.0 / N
+    gam, eig = O.diagonalize(N + 1, O.omega_of(kind, alpha, tau))
+    s1 = O.to_eigenspace(O.rhs_block(data, kind, alpha, tau, N + 1).T, gam)
+    s2 = O.step_b(s1, eig / tau, 1, np.pi, M)
+    assert raised == bool(raised_ref)
+    assert O.residue_ratio(s2, gam) == ratio_ref
+
+
+def test_residue_no_raise_cases(golden):
+    """BASELINE c1 does not trip the residue check (ratio 2e-13)."""
+    traj, ratio = O.solve_pint(O.PINT_QBVM, 1e-3, 1, np.pi, 256, 1.0, 256, golden["c1_gdelta"])
+    raised_ref, ratio_ref, _ = golden["trip_c1_pint-qbvm"]
+    assert not raised_ref and ratio == ratio_ref
