@@ -315,7 +315,8 @@ def main():
             for p in range(nph - 1):
                 phase_ms[p] += evs[k][p].elapsed_time(evs[k][p + 1])
         phase_ms /= args.steps
-        names = ["ghat (DST of g)", "k_modes_fast (shifts + time FFT + Gamma^-1 + Re)"]
+        modes_kernel = {257: "k_modes_rader", 513: "k_modes_fast", 1025: "k_modes_gt", 4097: "k_modes_pf"}.get(n, "k_modes")
+        names = ["ghat (DST of g)", f"{modes_kernel} (shifts + time FFT + Gamma^-1 + Re)"]
         if wax:
             names += [("k_dst_wax2" if w.num_cells == 512 else "k_dst_wax") +
                       f" W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]

@@ -132,7 +132,10 @@ int bhcp_from_eigenspace(const bhcp_time_plan* tp, const void* in, int64_t batch
                          int64_t out_sb, int64_t out_st, void* status_dev,
                          void* stream);
 
-/* Reset a status block (bad column = none, norms = 0). */
+/* Reset a status block (bad column = none, norms = 0, and the pass-A work
+ * counter that the kernels of bhcp_pint_modes / _modes_to / _modes_sym_to
+ * schedule their warps with -- a status block must be reset once before
+ * its first use; those kernels leave the counter at 0 when they finish). */
 int bhcp_status_reset(void* status_dev, void* stream);
 
 /* Synchronise `stream`, read the status block and apply the reference's
@@ -194,7 +197,9 @@ int bhcp_pint_modes_sym_to(const bhcp_space_plan* sp, const bhcp_time_plan* tp, 
  * bhcp_pint_ghat: ghat = DST(g) * scale (n_space float64), scale = 1/(divisor*n).
  * bhcp_pint_modes: for spatial modes [k_begin, k_end) write
  *   W(k, t) = ghat[k] * Re(gamma_inv_t * FFT_t(1/(s_j + mu_k)))
- *   and accumulate the residue norms / first singular column into status_dev.
+ *   and accumulate the residue norms / first singular column into status_dev
+ *   (reset with bhcp_status_reset before its first use: the pass-A kernels
+ *   also take their work from a counter in it).
  *   Layout of W (K = k_end - k_begin, k local, P1 = m^(dim-1)):
  *     dim 1 (nslabs = 0):  level-major, W[t * K + k]
  *     dim >= 2:            blocked by level slabs s (nslabs = 0: one slab

@@ -33,7 +33,9 @@ struct StatusDev {
   unsigned long long bad_col;  // first singular column, ULLONG_MAX if none
   double sum_re2;              // sum of (Re Y)^2
   double sum_im2;              // sum of (Im Y)^2
-  double pad[5];
+  unsigned long long work;     // pass-A work counter (dynamic scheduling; 0 between launches)
+  unsigned long long done;     // CTAs finished (the last one resets work and done)
+  double pad[3];
 };
 static_assert(sizeof(StatusDev) == 64, "status block is 64 bytes");
 
@@ -553,6 +555,8 @@ __global__ void k_status_reset(StatusDev* st) {
     st->bad_col = ~0ull;
     st->sum_re2 = 0.0;
     st->sum_im2 = 0.0;
+    st->work = 0;
+    st->done = 0;
   }
 }
 
@@ -740,6 +744,7 @@ struct bhcp_space_plan {
   long long ntiles;
   double2* twN;          // exp(-2 pi i k / N), N = m + 1 (half-length DST kernels)
   double* snN;           // sin(pi j / N)
+  double mu_lo, mu_hi;   // range of the mode eigenvalues: dim * mu1_min, dim * mu1_max (host)
   int4* seg_tiles[9];    // symmetric segment tiles of the Bluestein / Rader / Good-Thomas modes kernels,
   long long seg_count[9];   // one slot per segment length seg_len[slot]
   int seg_len[9];
@@ -752,8 +757,9 @@ struct bhcp_time_plan {
   double2* blue;         // n = 2^p + 1 fast path: tw (L) | chirp (n) | bhat (L) | wM (n), L = 2(n-1)
   double2* rader;        // prime n = 2^p + 1: tw (n-1) | bhat (n-1)
   int* rader_idx;        //                    perm (n-1) | qidx (n)
-  double2* gt;           // n = 1025: w40 | w25 | bhat40
-  int* gt_idx;           //           perm41 | tq41
+  double2* gt;           // n = 1025: plan.h kGt2* layout (generator shifts, twiddles, 1/gamma, bhat40)
+  int* gt_idx;           //           stage-C lane map | row slots | powers of g
+  std::vector<double2> shifts_h;   // host copy of the shifts (may_be_singular)
   double2* pf;           // n = 4097: w240 | bhat240 | shifts in prime-factor order (4097)
   double* pf_thr;        //           singular thresholds, prime-factor order (4097)
   int* pf_idx;           //           tq241 (240) | time index j per (row, slot) (4097)
@@ -841,8 +847,10 @@ void set_all_attributes() {
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
-  allow_smem(fastk::k_modes_gt<false>);
-  allow_smem(fastk::k_modes_gt<true>);
+  allow_smem(fastk::k_modes_gt<false, false>);
+  allow_smem(fastk::k_modes_gt<true, false>);
+  allow_smem(fastk::k_modes_gt<false, true>);
+  allow_smem(fastk::k_modes_gt<true, true>);
   allow_smem(fastk::k_modes_rader<257, false>);
   allow_smem(fastk::k_modes_rader<257, true>);
   allow_smem(fastk::k_modes_fast<513, false>);
@@ -1123,7 +1131,7 @@ long long seg_list_count(int dim, int m, int S, bool six) {
 // variant (every mode its own FFT).
 constexpr long long kSegCapBytes = 64LL << 20;
 struct SegKey { int S; bool six; };
-constexpr SegKey kSegKeys[] = {{12, false}, {12, true}, {1, false}, {8, false}, {2, false}};
+constexpr SegKey kSegKeys[] = {{12, false}, {12, true}, {10, false}, {1, false}, {8, false}, {2, false}};
 
 constexpr bool seg_key_listed(int S, bool six) {
   for (const SegKey& k : kSegKeys)
@@ -1183,12 +1191,41 @@ static_assert(seg_key_listed(fastk::GtPlan::S, false) && seg_key_listed(fastk::R
                   seg_key_listed(fastk::BluePlan<4097>::S, false),
               "every symmetric pass-A kernel's segment length has a prebuilt list");
 
+// Could some shift s_j lie within 1e-14 |s_j| of a mode eigenvalue of this
+// plan (space.py:237-240)? mu ranges over [dim mu1_min, dim mu1_max]; the
+// nearest point of that interval to -s_j is tested with a 2x margin for the
+// rounding of the device's den2. If not, the pass-A generator skips the test.
+bool may_be_singular(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
+  const double lo = sp->mu_lo * (1.0 - 1e-12), hi = sp->mu_hi * (1.0 + 1e-12);
+  for (const double2& s : tp->shifts_h) {
+    const double x = std::min(std::max(-s.x, lo), hi);
+    const double d = std::hypot(s.x + x, s.y);
+    if (d <= 2e-14 * std::hypot(s.x, s.y)) return true;
+  }
+  return false;
+}
+
+template <bool CHECK>
+int gt_launch(const fastk::GtModesArgs& a, bool sym, size_t sm, cudaStream_t s) {
+  using namespace fastk;
+  if (sym) {
+    const long long grid = std::min<long long>(a.ntiles, resident_ctas(k_modes_gt<true, CHECK>, GtPlan::T, sm));
+    k_modes_gt<true, CHECK><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+  } else {
+    const long long work = (a.k_count + GtPlan::S - 1) / GtPlan::S;
+    const long long grid = std::min<long long>(work, resident_ctas(k_modes_gt<false, CHECK>, GtPlan::T, sm));
+    k_modes_gt<false, CHECK><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_gt launch");
+  return BHCP_OK;
+}
+
 int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
              long long k_begin, long long k_end, double* W, const fastk::WLayout& wl, StatusDev* st, cudaStream_t s,
              const SymRange& sr = SymRange()) {
   using namespace fastk;
   GtModesArgs a{};
-  a.shifts = tp->tables + 2 * tp->n; a.gaminv = tp->tables + tp->n; a.mu1 = sp->mu1_dev; a.ghat = ghat;
+  a.mu1 = sp->mu1_dev; a.ghat = ghat;
   a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
   a.st = st; a.wl = wl; a.tab = tp->gt; a.itab = tp->gt_idx;
   const size_t sm = gt_smem();
@@ -1200,15 +1237,9 @@ int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
-    const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_gt<true>, GtPlan::T, sm));
-    k_modes_gt<true><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
-  } else {
-    const long long work = (a.k_count + GtPlan::S - 1) / GtPlan::S;
-    const long long grid = std::min<long long>(work, resident_ctas(k_modes_gt<false>, GtPlan::T, sm));
-    k_modes_gt<false><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
   }
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_gt launch");
-  return BHCP_OK;
+  return may_be_singular(sp, tp) ? gt_launch<true>(a, a.tiles != nullptr, sm, s)
+                                 : gt_launch<false>(a, a.tiles != nullptr, sm, s);
 }
 
 int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,
@@ -1751,6 +1782,8 @@ int bhcp_space_plan_create(int device, int dim, int num_cells, const double* mu1
     free_fft_plan(&sp->dst); delete sp; return cuda_fail("cudaMalloc mu1");
   }
   cudaMemcpy(sp->mu1_dev, mu1_host, sizeof(double) * sp->m, cudaMemcpyHostToDevice);
+  sp->mu_lo = dim * *std::min_element(mu1_host, mu1_host + sp->m);
+  sp->mu_hi = dim * *std::max_element(mu1_host, mu1_host + sp->m);
   sp->tiles_dev = nullptr;
   sp->ntiles = 0;
   for (int i = 0; i < 9; ++i) { sp->seg_tiles[i] = nullptr; sp->seg_count[i] = 0; sp->seg_len[i] = 0; }
@@ -1888,10 +1921,14 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
     cudaMemcpy(tp->pf_thr, thr.data(), sizeof(double) * thr.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(tp->pf_idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice);
   }
+  tp->shifts_h.resize(n_levels);
+  for (int j = 0; j < n_levels; ++j) tp->shifts_h[j] = make_double2(shifts_host[2 * j], shifts_host[2 * j + 1]);
   if (n_levels == 1025) {
     std::vector<double2> gc;
     std::vector<int> gi;
-    if (!build_gt_tables(&gc, &gi, &err)) { bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err); }
+    if (!build_gt2_tables(shifts_host, gamma_inv_host, &gc, &gi, &err)) {
+      bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err);
+    }
     if (cudaMalloc(&tp->gt, sizeof(double2) * gc.size()) != cudaSuccess ||
         cudaMalloc(&tp->gt_idx, sizeof(int) * gi.size()) != cudaSuccess) {
       bhcp_time_plan_destroy(tp); return cuda_fail("cudaMalloc gt tables");

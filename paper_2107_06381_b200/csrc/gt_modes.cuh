@@ -1,31 +1,41 @@
-// gt_modes.cuh -- pass A for n = 1025 time levels (BASELINE config 3) by the
-// prime-factor (Good-Thomas) algorithm, 1025 = 25 x 41, with Rader's
-// algorithm for the 41-point transforms. Included by bhcp_b200.cu.
+// gt_modes.cuh -- pass A for n = 1025 time levels (BASELINE config 3):
+// register-resident Cooley-Tukey 1025 = 41 x 25 with a Rader 41-point first
+// stage. Included by bhcp_b200.cu.
 //
-// X_t = sum_j v_j w^{jt}, w = exp(-2 pi i / 1025), v_j = 1 / (s_j + mu).
-// With the input map j = (41 j1 + 25 j2) mod 1025 and t1 = t mod 25,
-// t2 = t mod 41 the kernel is w25^{j1 t1} w41^{j2 t2}: a 25 x 41 2D DFT with
-// no twiddles between the two factors.
-//   * 41-point DFTs along j2 (one per row j1) by Rader: with j2 = g^p,
-//     t2 = g^-q (g a primitive root of 41),
-//       Y_0 = sum y,  Y_{g^-q} = y_0 + (a (*) b)_q,  a_p = y_{g^p}, b_m = w41^{g^-m},
-//     a length-40 cyclic convolution done as A = FFT40(a),
-//     conv = conj(FFT40(conj(A * bhat))) (bhat = FFT40(b) / 40), and Y_0 = y_0 + A_0.
-//   * 25-point DFTs along j1 (one per column t2), radix 5 x 5.
-// The per-mode work is about 0.6x the FLOPs of the 2048-point Bluestein
-// pair it replaces. One warp per mode (warp-synchronous stages over a
-// 25 x 41 region, in rounds of whole rows / columns so every stage can run in
-// place), persistent CTAs, symmetric seg tiles as in k_modes_blue.
+// X_t = sum_j v_j w^{jt}, w = exp(-2 pi i / 1025), v_j = 1 / (s_j + mu) (the
+// shifted divide of space.py:276-278 for one spatial mode, pint.py:52-61).
+// With j = 25 j1 + j2 and t = k1 + 41 k2 (j1, k1 in Z41; j2, k2 in Z25):
+//   Y(j2, k1) = sum_j1 v_{25 j1 + j2} w41^{j1 k1}                 (41-point, 25 rows)
+//   X_{k1 + 41 k2} = sum_j2 [Y(j2, k1) w1025^{j2 k1}] w25^{j2 k2}  (25-point, 41 columns)
+// The 41-point transforms use Rader (g a primitive root of 41):
+//   Y(j2, 0) = y0 + A_0,  Y(j2, g^-q) = y0 + conj(FFT40(conj(A * bhat)))_q,
+//   A = FFT40(a), a_p = v_{25 g^p + j2}, y0 = v_{j2}, bhat = FFT40(b) / 40,
+//   b_m = w41^{g^-m}; and FFT40 is the prime-factor 5 x 8 (no twiddles):
+//   position (x, y) in Z5 x Z8 holds input index (8x + 5y) mod 40 and output
+//   index K = CRT(x mod 5, y mod 8).
+//
+// One warp per mode; its 25 rows live in shared memory (row stride 43,
+// slot 5y + x for FFT40 position (x, y), slot 40 = y0, slot 41 = Y(j2, 0)),
+// and every small DFT runs in registers:
+//   R1  (4 rounds, pencils (x, j2)): generator 1/(s_j + mu) -> DFT8 over y
+//   R2  (7 rounds, pencils (y, j2)): DFT5 over x -> * bhat, conj -> DFT5
+//   R3  (4 rounds, pencils (x, j2)): DFT8 over y -> y0 + conj
+//   C   (2 rounds, lane = column k1): twiddle, DFT25 (5 x 5) over j2,
+//       Gamma^-1, Re, residue norms, and the store of W[t] straight from
+//       registers (t = k1 + 41 k2: consecutive lanes, consecutive levels).
+// Each stage reads what the previous one wrote through one shared-memory
+// pass (4 passes per mode instead of 16 in a stage-per-round layout); the
+// pencil orders and the stage-C lane positions make every 16-byte access
+// conflict-free. Persistent CTAs of 10 warps, no CTA barrier in the mode loop.
 #pragma once
 
 namespace bhcp {
 namespace fastk {
 
-constexpr int kGtRows = 25, kGtLen = 41, kGtN = kGtRows * kGtLen;   // row j1: 41 slots
+constexpr int kGtRS = 43;                 // row stride (odd: consecutive rows hit distinct banks)
+constexpr int kGtRowWords = 25 * kGtRS;   // one warp's mode: 25 rows
 
 struct GtModesArgs {
-  const double2* shifts;
-  const double2* gaminv;
   const double* mu1;
   const double* ghat;
   double cscale;
@@ -33,235 +43,304 @@ struct GtModesArgs {
   double* W;
   int m, dim;
   StatusDev* st;
-  const double2* tab;   // w40 (40) | w25 (25) | bhat40 (40)
-  const int* itab;      // perm (40): g^p mod 41 | tq (40): g^-q mod 41
+  const double2* tab;   // plan.h kGt2* layout
+  const int* itab;      // ck1 [41] | csl [41] | gpw [40]
   WLayout wl;
   const int4* tiles;
   long long ntiles;
 };
 
-// 12 warps at 168 registers; 8 warps (no spills, 231 registers) measured 12.2 ms
-// against 10.0 on c3
-struct GtPlan { static constexpr int S = 12, T = 384; };
+struct GtPlan { static constexpr int S = 10, T = 32 * S; };
+
+// w25^e = cos(2 pi e / 25) - i sin(2 pi e / 25), e = 0..16 (DFT25 internal twiddles)
+__constant__ double c_cos25[17] = {1.0, 0.96858316112863111949, 0.876306680043863587308, 0.728968627421411523147,
+                                   0.535826794978996618271, 0.309016994374947424102, 0.0627905195293133760762,
+                                   -0.187381314585724630543, -0.425779291565072648863, -0.637423989748689710177,
+                                   -0.809016994374947424102, -0.929776485888251403661, -0.99211470131447783105,
+                                   -0.99211470131447783105, -0.929776485888251403661, -0.809016994374947424102,
+                                   -0.637423989748689710177};
+__constant__ double c_sin25[17] = {0.0, 0.248689887164854788242, 0.481753674101715274987, 0.684547105928688673732,
+                                   0.844327925502015078549, 0.951056516295153572116, 0.998026728428271561952,
+                                   0.982287250728688681086, 0.904827052466019527714, 0.770513242775789230803,
+                                   0.587785252292473129169, 0.368124552684677959157, 0.125333233564304245373,
+                                   -0.125333233564304245373, -0.368124552684677959157, -0.587785252292473129169,
+                                   -0.770513242775789230803};
+
+__device__ __forceinline__ double2 cmulc(double2 a, double c, double s) {   // a * (c + i s)
+  return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+}
+
+// 1/(s + mu) with the singular-shift test of space.py:237-240 when CHECK
+template <bool CHECK>
+__device__ __forceinline__ double2 gen_inv(double2 s, double mu, StatusDev* st, long long j) {
+  const double dr = s.x + mu, di = s.y;
+  const double den2 = fma(dr, dr, di * di);
+  if (CHECK) {
+    if (den2 <= 1e-28 * fma(s.x, s.x, s.y * s.y)) flag_singular(st, j);
+  }
+  const double inv = fast_rcp(den2);
+  return make_double2(dr * inv, -di * inv);
+}
+
+// W address of level t for destination (row k1, in-row index r) of layout wl
+__device__ __forceinline__ double* w_level_ptr(const WLayout& wl, int k1, long long r, int t) {
+  if (!wl.mode_major) return wl.sl_base[0] + (long long)t * wl.w_ld + r;
+  int s = 0;
+  while (s + 1 < wl.nsl && t >= wl.sl_c[s + 1]) ++s;
+  const int tl = t - wl.sl_c[s];
+  return wl.sl_base[s] + wl.row_off(s, k1) + (((long long)(tl >> 3)) * wl.P1 + r) * kTBL + (tl & 7);
+}
+
+// One work item = one warp-mode: SYM (2D/3D mirror tiles): item = tile * S + w,
+// the w-th mode of tile `tile` (invalid off the triangle / past m: skipped);
+// otherwise item = local mode index.
+struct GtItem {
+  bool valid, hm;
+  long long kd, km, rd, rm;
+  int k1d, k1m;
+};
 
 template <bool SYM>
-__global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {   // 12 warps: 197 KB buffers
-  constexpr int NL = kGtN, S = GtPlan::S, T = GtPlan::T, RS = kGtLen;
-  static_assert(T == 32 * S, "one warp per mode");
-  extern __shared__ double2 smem[];
-  __shared__ double red[2 * (T / 32)];
-  __shared__ double2 s_t40[7][5], s_t25[4][5], s_bh[40];   // twiddles by (r-1, b)
-  __shared__ short s_tq[40];
-  // shifts and singular thresholds in the Good-Thomas input order (row j1, slot):
-  // the generator reads consecutive entries
-  __shared__ double2 s_shg[NL];
-  __shared__ double s_thrg[NL];
-  __shared__ short s_jg[NL];
-  __shared__ double2 s_x0[S][kGtRows];
-  for (int i = threadIdx.x; i < NL; i += T) {
-    const int row = i / RS, slot = i - row * RS;
-    const int j2 = slot ? __ldg(a.itab + slot - 1) : 0;
-    const int j = (41 * row + 25 * j2) % NL;
-    const double2 sh = __ldg(a.shifts + j);
-    s_shg[i] = sh;
-    s_thrg[i] = 1e-28 * (sh.x * sh.x + sh.y * sh.y);   // space.py:237-240
-    s_jg[i] = (short)j;
-    if (i < 40) {
-      s_bh[i] = __ldg(a.tab + 65 + i);
-      s_tq[i] = (short)__ldg(a.itab + 40 + i);
+__device__ __forceinline__ GtItem gt_decode(const GtModesArgs& a, long long item, int4 tb) {
+  GtItem it{};
+  constexpr int S = GtPlan::S;
+  if (SYM) {
+    const int w = (int)(item % S);
+    if (a.dim == 2) {
+      const int k1 = tb.x, k2 = tb.y + w;
+      it.valid = k2 < a.m && k2 >= k1;
+      it.kd = (long long)k1 * a.m + k2;
+      it.hm = it.valid && k2 != k1;
+      it.km = (long long)k2 * a.m + k1;
+      it.k1d = k1; it.rd = k2; it.k1m = k2; it.rm = k1;
+    } else {
+      const int k1 = tb.x, k2 = tb.y, k3 = tb.z + w;
+      it.valid = k3 < a.m;
+      it.kd = ((long long)k1 * a.m + k2) * a.m + k3;
+      it.hm = it.valid && k1 != k2;
+      it.km = ((long long)k2 * a.m + k1) * a.m + k3;
+      it.k1d = k1; it.rd = (long long)k2 * a.m + k3; it.k1m = k2; it.rm = (long long)k1 * a.m + k3;
     }
-    if (i < 35) s_t40[i / 5][i % 5] = __ldg(a.tab + ((i / 5 + 1) * (i % 5)) % 40);
-    if (i < 20) s_t25[i / 5][i % 5] = __ldg(a.tab + 40 + ((i / 5 + 1) * (i % 5)) % 25);
+  } else {
+    it.valid = item < a.k_count;
+    const long long local = it.valid ? item : 0;
+    it.kd = a.k_begin + local;
+    if (a.wl.mode_major) { it.k1d = (int)(local / a.wl.P1); it.rd = local - (long long)it.k1d * a.wl.P1; }
+    else it.rd = local;
+  }
+  return it;
+}
+
+template <bool SYM, bool CHECK>
+__global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
+  constexpr int S = GtPlan::S, T = GtPlan::T, RS = kGtRS;
+  extern __shared__ double2 smem[];
+  __shared__ double red[2 * S];
+  __shared__ int s_ck1[41], s_csl[41], s_gpw[40];
+  double2* s_sg = smem;                       // [8][128] + y0 [32]
+  double2* s_tw = smem + kGt2Tw;              // [25][41]
+  double2* s_gi = smem + kGt2Gi;              // [25][41]
+  double2* s_bh = smem + kGt2Bh;              // [8][5]
+  for (int i = threadIdx.x; i < kGt2Total; i += T) smem[i] = __ldg(a.tab + i);
+  for (int i = threadIdx.x; i < 41; i += T) {
+    s_ck1[i] = __ldg(a.itab + i);
+    s_csl[i] = __ldg(a.itab + 41 + i);
+    if (i < 40) s_gpw[i] = __ldg(a.itab + 82 + i);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* buf = smem + warp * NL;
-  double2* x0 = s_x0[warp];
+  double2* Y = smem + kGt2Total + warp * kGtRowWords;
   StatusDev* st = a.st;
   const WLayout& wl = a.wl;
+  const bool fast_store = wl.mode_major && wl.nsl == 1 && !wl.sl_koff[0];
   double sre = 0.0, sim = 0.0;
-  const long long ntiles = SYM ? a.ntiles : (a.k_count + S - 1) / S;
+  const long long nitems = SYM ? a.ntiles * S : a.k_count;
 
-  // In-place FFT40 over slots 1..40 of every row: radix 5 (Ns = 1) then
-  // radix 8 (Ns = 5). Rounds cover whole rows, so loads of a round finish
-  // (syncwarp) before its stores and no round reads what another wrote. Both
-  // stages touch consecutive slots across lanes (strides 1 and 5): no bank
-  // conflicts with the odd row stride 41. store_out(rowp, q, value) stores
-  // output q of the radix-8 stage.
-  auto fft40 = [&](auto&& store_out) {
-    // radix 5: 8 butterflies per row, 4 rows per round
-#pragma unroll 1
-    for (int r0 = 0; r0 < kGtRows; r0 += 4) {
-      const int row = r0 + (lane >> 3), b = lane & 7;
-      const bool act = row < kGtRows;
-      double2 v[5];
-      double2* rowp = buf + row * RS + 1;
-      if (act) {
-#pragma unroll
-        for (int r = 0; r < 5; ++r) v[r] = rowp[b + 8 * r];
-        sfft::Cod<5>::run(v);
-      }
-      __syncwarp();
-      if (act) {
-#pragma unroll
-        for (int r = 0; r < 5; ++r) rowp[5 * b + r] = v[r];
-      }
-      __syncwarp();
-    }
-    // radix 8 with twiddles w40^{b r} (k = b % 5 = b): 5 butterflies per row, 6 rows per round
-#pragma unroll 1
-    for (int r0 = 0; r0 < kGtRows; r0 += 6) {
-      const int row = r0 + lane / 5, b = lane % 5;
-      const bool act = lane < 30 && row < kGtRows;
-      double2 v[8];
-      double2* rowp = buf + row * RS + 1;
-      if (act) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) v[r] = rowp[b + 5 * r];
-#pragma unroll
-        for (int r = 1; r < 8; ++r) v[r] = cmul(v[r], s_t40[r - 1][b]);
-        sfft::Cod<8>::run(v);
-      }
-      __syncwarp();
-      if (act) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) store_out(rowp, b + 5 * r, v[r]);
-      }
-      __syncwarp();
-    }
+  // Dynamic per-warp scheduling (atomic counter in the status block, reset by the
+  // last CTA): warps finish together whatever their share of off-triangle items.
+  // Depth-2 prefetch: while mode i is transformed, item i+2 is claimed and item
+  // i+1's tile, mu and ghat loads are in flight.
+  auto claim = [&]() -> long long {
+    unsigned long long v = 0;
+    if (lane == 0) v = atomicAdd(&st->work, 1ull);
+    return (long long)__shfl_sync(0xffffffffu, v, 0);
   };
+  long long cur = claim();
+  long long nxt = claim();
+  int4 tb_cur = make_int4(0, 0, 0, 0);
+  if (SYM && cur < nitems) tb_cur = __ldg(a.tiles + cur / S);
+  while (cur < nitems) {
+    const GtItem it = gt_decode<SYM>(a, cur, tb_cur);
+    // next item's tile (consumed at the next iteration) and the claim after it
+    int4 tb_nxt = make_int4(0, 0, 0, 0);
+    if (SYM && nxt < nitems) tb_nxt = __ldg(a.tiles + nxt / S);
+    const long long nxt2 = claim();
+    if (!it.valid) {   // warp-uniform
+      cur = nxt; nxt = nxt2; tb_cur = tb_nxt;
+      continue;
+    }
+    const double mu = (SYM && a.dim == 2) ? __ldg(a.mu1 + it.k1d) + __ldg(a.mu1 + it.rd)
+                                          : mode_mu(a.mu1, a.m, a.dim, it.kd);
+    const double c = __ldg(a.ghat + it.kd) * a.cscale;
+    const double c2 = it.hm ? __ldg(a.ghat + it.km) * a.cscale : 0.0;
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    bool valid, hm = false;
-    long long kd, km = 0;
-    int k1d = 0, k1m = 0;
-    long long rd = 0, rm = 0;
-    if (SYM) {
-      const int4 tb = __ldg(a.tiles + tile);
-      if (a.dim == 2) {
-        const int k1 = tb.x, k2 = tb.y + warp;
-        valid = k2 < a.m && k2 >= k1;
-        kd = (long long)k1 * a.m + k2;
-        hm = valid && k2 != k1;
-        km = (long long)k2 * a.m + k1;
-        k1d = k1; rd = k2; k1m = k2; rm = k1;
-      } else {
-        const int k1 = tb.x, k2 = tb.y, k3 = tb.z + warp;
-        valid = k3 < a.m;
-        kd = ((long long)k1 * a.m + k2) * a.m + k3;
-        hm = valid && k1 != k2;
-        km = ((long long)k2 * a.m + k1) * a.m + k3;
-        k1d = k1; rd = (long long)k2 * a.m + k3; k1m = k2; rm = (long long)k1 * a.m + k3;
-      }
-      if (!valid) kd = 0;
-    } else {
-      const long long kl = tile * S + warp;
-      valid = kl < a.k_count;
-      kd = a.k_begin + (valid ? kl : 0);
-      const long long local = valid ? kl : 0;
-      if (wl.mode_major) { k1d = (int)(local / wl.P1); rd = local - (long long)k1d * wl.P1; }
-      else rd = local;
-    }
-    if (!valid) continue;
-    const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
-    const double c = __ldg(a.ghat + kd) * a.cscale;
-    const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
-    // 1. generator: row j1, slot 0 -> j2 = 0, slot 1 + p -> j2 = g^p;  j = (41 j1 + 25 j2) mod 1025
-    for (int i = lane; i < NL; i += 32) {
-      const double2 s = s_shg[i];
-      const double dr = s.x + mu, di = s.y;
-      const double den2 = dr * dr + di * di;
-      if (den2 <= s_thrg[i]) flag_singular(st, s_jg[i]);
-      const double inv = fast_rcp(den2);
-      buf[i] = make_double2(dr * inv, -di * inv);
-    }
-    __syncwarp();
-    // 2. A = FFT40(a) per row (natural order)
-    fft40([](double2* rowp, int q, double2 x) { rowp[q] = x; });
-    // 3. Y(row, 0) = y0 + A_0 (kept aside); slots <- conj(A_k * bhat_k)
-    for (int i = lane; i < kGtRows * 40; i += 32) {
-      const int row = i / 40, k = i - row * 40;
-      double2* p = buf + row * RS + 1 + k;
-      const double2 A = *p;
-      if (k == 0) x0[row] = cadd(buf[row * RS], A);
-      *p = cconj(cmul(A, s_bh[k]));
-    }
-    __syncwarp();
-    // 4. FFT40 again; conv_q = conj(out_q); Y(row, t2 = g^-q) = y0 + conv_q, stored at slot t2
-    //    (rounds hold whole rows, so the permuted stores stay inside the round's rows)
-    fft40([&](double2* rowp, int q, double2 x) { rowp[s_tq[q] - 1] = cadd(rowp[-1], cconj(x)); });
-    // slot 0 <- Y(row, 0)
-    if (lane < kGtRows) buf[lane * RS] = x0[lane];
-    __syncwarp();
-    // 5. 25-point DFTs down each column t2 (stride RS): radix 5 (Ns = 1) then radix 5 (Ns = 5, w25)
+    // ---- R1: generator + DFT8 over y, pencils p = x * 25 + j2 (x = alpha), two per lane at a time
 #pragma unroll 1
-    for (int st2 = 0; st2 < 2; ++st2) {
-      for (int c0 = 0; c0 < kGtLen; c0 += 6) {
-        const int col = c0 + lane / 5, b = lane % 5;
-        const bool act = lane < 30 && col < kGtLen;
-        double2 v[5];
-        double2* colp = buf + col;
-        if (act) {
+    for (int h = 0; h < 2; ++h) {
+      const int pa = lane + 64 * h, pb = pa + 32;
+      const bool okb = pb < 125;
+      double2 va[8], vb[8];
+      const int xa = pa / 25, ja = pa - xa * 25, xb = pb / 25, jb = pb - xb * 25;
 #pragma unroll
-          for (int r = 0; r < 5; ++r) v[r] = colp[(b + 5 * r) * RS];
-          if (st2 == 1) {
+      for (int y = 0; y < 8; ++y) {
+        const long long jja = CHECK ? 25LL * s_gpw[(8 * xa + 5 * y) % 40] + ja : 0;
+        const long long jjb = CHECK ? 25LL * s_gpw[(8 * xb + 5 * y) % 40] + jb : 0;
+        va[y] = gen_inv<CHECK>(s_sg[y * 128 + pa], mu, st, jja);
+        vb[y] = okb ? gen_inv<CHECK>(s_sg[y * 128 + pb], mu, st, jjb) : make_double2(0.0, 0.0);
+      }
+      Dft<8>::prep(va);
+      Dft<8>::prep(vb);
+      double2* rowa = Y + ja * RS;
+      double2* rowb = Y + jb * RS;
 #pragma unroll
-            for (int r = 1; r < 5; ++r) v[r] = cmul(v[r], s_t25[r - 1][b]);
-          }
-          sfft::Cod<5>::run(v);
-        }
-        __syncwarp();
-        if (act) {
-          // Stockham: stage 1 (Ns = 1) writes 5b + r; stage 2 (Ns = 5, k = b) writes b + 5r
+      for (int k = 0; k < 8; ++k) rowa[5 * k + xa] = va[k];
+      if (okb) {
 #pragma unroll
-          for (int r = 0; r < 5; ++r) colp[(st2 == 0 ? 5 * b + r : b + 5 * r) * RS] = v[r];
-        }
-        __syncwarp();
+        for (int k = 0; k < 8; ++k) rowb[5 * k + xb] = vb[k];
       }
     }
-    // 6. store: X_t at (t mod 25, t mod 41); W = c Re(Gamma^-1 X), residue norms
-    const int nsl = wl.mode_major ? wl.nsl : 1;
-    double zr2 = 0.0, zi2 = 0.0;
-    for (int sl = 0; sl < nsl; ++sl) {
-      const int t0 = wl.mode_major ? wl.sl_c[sl] : 0;
-      const int t1 = wl.mode_major ? wl.sl_c[sl + 1] : NL;
-      long long pd, pm, step;
-      if (wl.mode_major) {
-        const long long lo = (long long)(lane >> 3) * wl.P1 * kTBL + (lane & 7);
-        pd = wl.row_off(sl, k1d) + rd * kTBL + lo;
-        pm = wl.row_off(sl, k1m) + rm * kTBL + lo;
-        step = 4 * wl.P1 * kTBL;
-      } else {
-        pd = rd + (long long)lane * wl.w_ld;
-        pm = pd;
-        step = 32 * wl.w_ld;
+    if (lane < 25) Y[lane * RS + 40] = gen_inv<CHECK>(s_sg[1024 + lane], mu, st, lane);   // y0 = v_{j2}
+    __syncwarp();
+    // ---- R2: DFT5 over x, * bhat, conj, DFT5; pencils p = y * 25 + j2, two per lane at a time
+#pragma unroll 1
+    for (int h = 0; h < 4; ++h) {
+      const int pa = lane + 64 * h, pb = pa + 32;
+      const bool oka = pa < 200, okb = pb < 200;
+      const int ya = pa / 25, ja = pa - ya * 25, yb = pb / 25, jb = pb - yb * 25;
+      double2* rowa = Y + ja * RS;
+      double2* rowb = Y + jb * RS;
+      double2 ua[5], ub[5];
+#pragma unroll
+      for (int x = 0; x < 5; ++x) {
+        ua[x] = oka ? rowa[5 * ya + x] : make_double2(0.0, 0.0);
+        ub[x] = okb ? rowb[5 * yb + x] : make_double2(0.0, 0.0);
       }
-      double* __restrict__ wd = wl.sl_base[sl] + pd;
-      double* __restrict__ wmr = wl.sl_base[sl] + pm;
-      for (int t = t0 + lane; t < t1; t += 32, wd += step, wmr += step) {
-        const double2 X = buf[(t % kGtRows) * RS + (t % kGtLen)];
-        const double2 g = __ldg(a.gaminv + t);
-        const double zr = X.x * g.x - X.y * g.y;
-        const double zi = X.x * g.y + X.y * g.x;
-        zr2 = fma(zr, zr, zr2);
-        zi2 = fma(zi, zi, zi2);
-        *wd = c * zr;
-        if (hm) *wmr = c2 * zr;
+      sfft::Cod<5>::run(ua);
+      sfft::Cod<5>::run(ub);
+      if (oka && ya == 0) rowa[41] = cadd(rowa[40], ua[0]);   // Y(j2, 0) = y0 + A_0
+#pragma unroll
+      for (int x = 0; x < 5; ++x) {
+        ua[x] = cconj(cmul(ua[x], s_bh[(oka ? ya : 0) * 5 + x]));
+        ub[x] = cconj(cmul(ub[x], s_bh[(okb ? yb : 0) * 5 + x]));
+      }
+      sfft::Cod<5>::run(ua);
+      sfft::Cod<5>::run(ub);
+      if (oka) {
+#pragma unroll
+        for (int x = 0; x < 5; ++x) rowa[5 * ya + x] = ua[x];
+      }
+      if (okb) {
+#pragma unroll
+        for (int x = 0; x < 5; ++x) rowb[5 * yb + x] = ub[x];
+      }
+    }
+    __syncwarp();
+    // ---- R3: DFT8 over y, conv = conj, Y = y0 + conv; pencils p = x * 25 + j2, two per lane at a time
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int pa = lane + 64 * h, pb = pa + 32;
+      const bool okb = pb < 125;
+      const int xa = pa / 25, ja = pa - xa * 25, xb = pb / 25, jb = pb - xb * 25;
+      double2* rowa = Y + ja * RS;
+      double2* rowb = Y + jb * RS;
+      double2 va[8], vb[8];
+#pragma unroll
+      for (int y = 0; y < 8; ++y) {
+        va[y] = rowa[5 * y + xa];
+        vb[y] = okb ? rowb[5 * y + xb] : make_double2(0.0, 0.0);
+      }
+      const double2 y0a = rowa[40];
+      const double2 y0b = okb ? rowb[40] : make_double2(0.0, 0.0);
+      Dft<8>::prep(va);
+      Dft<8>::prep(vb);
+#pragma unroll
+      for (int y = 0; y < 8; ++y) rowa[5 * y + xa] = make_double2(y0a.x + va[y].x, y0a.y - va[y].y);
+      if (okb) {
+#pragma unroll
+        for (int y = 0; y < 8; ++y) rowb[5 * y + xb] = make_double2(y0b.x + vb[y].x, y0b.y - vb[y].y);
+      }
+    }
+    __syncwarp();
+    // ---- C: column k1 per lane: twiddle, DFT25 over j2, Gamma^-1, Re, norms, stores
+    double zr2 = 0.0, zi2 = 0.0;
+    const long long dstride = fast_store ? wl.P1 * kTBL : 0;
+    double* const based = fast_store ? wl.sl_base[0] + wl.row_off(0, it.k1d) + it.rd * kTBL : nullptr;
+    double* const basem = fast_store ? wl.sl_base[0] + wl.row_off(0, it.k1m) + it.rm * kTBL : nullptr;
+#pragma unroll 1
+    for (int cp = lane; cp < 41; cp += 32) {
+      const int k1 = s_ck1[cp];
+      const double2* col = Y + s_csl[cp];
+      double2 z[25];
+      z[0] = col[0];
+#pragma unroll
+      for (int j2 = 1; j2 < 25; ++j2) z[j2] = cmul(col[j2 * RS], s_tw[j2 * 41 + cp]);
+      // DFT25, j2 = 5 a + b, k2 = q + 5 d: DFT5 over a, twiddle w25^{b q}, DFT5 over b
+#pragma unroll
+      for (int b = 0; b < 5; ++b) {
+        double2 u[5] = {z[b], z[5 + b], z[10 + b], z[15 + b], z[20 + b]};
+        sfft::Cod<5>::run(u);
+        z[b] = u[0];
+#pragma unroll
+        for (int q = 1; q < 5; ++q) {
+          if (b == 0) z[5 * q + b] = u[q];
+          else z[5 * q + b] = cmulc(u[q], c_cos25[b * q], -c_sin25[b * q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        double2 u[5] = {z[5 * q], z[5 * q + 1], z[5 * q + 2], z[5 * q + 3], z[5 * q + 4]};
+        sfft::Cod<5>::run(u);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          const int k2 = q + 5 * d;
+          const int t = k1 + 41 * k2;
+          const double2 gi = s_gi[k2 * 41 + cp];
+          const double zr = fma(u[d].x, gi.x, -u[d].y * gi.y);
+          const double zi = fma(u[d].x, gi.y, u[d].y * gi.x);
+          zr2 = fma(zr, zr, zr2);
+          zi2 = fma(zi, zi, zi2);
+          if (fast_store) {
+            const long long off = (long long)(t >> 3) * dstride + (t & 7);
+            based[off] = c * zr;
+            if (it.hm) basem[off] = c2 * zr;
+          } else {
+            *w_level_ptr(wl, it.k1d, it.rd, t) = c * zr;
+            if (it.hm) *w_level_ptr(wl, it.k1m, it.rm, t) = c2 * zr;
+          }
+        }
       }
     }
     const double cc = c * c + c2 * c2;
     sre = fma(cc, zr2, sre);
     sim = fma(cc, zi2, sim);
-    __syncwarp();   // buf is rewritten by the next mode
+    __syncwarp();   // Y is rewritten by the next mode
+    cur = nxt; nxt = nxt2; tb_cur = tb_nxt;
   }
   block_sum2(sre, sim, red);
   if (threadIdx.x == 0) {
     atomicAdd(&a.st->sum_re2, sre);
     atomicAdd(&a.st->sum_im2, sim);
+    // the last CTA out resets the work counter for the next launch on this status block
+    __threadfence();
+    if (atomicAdd(&st->done, 1ull) == gridDim.x - 1) {
+      st->work = 0;
+      st->done = 0;
+      __threadfence();
+    }
   }
 }
 
-constexpr size_t gt_smem() { return sizeof(double2) * kGtN * GtPlan::S; }
+constexpr size_t gt_smem() { return sizeof(double2) * ((size_t)kGt2Total + (size_t)kGtRowWords * GtPlan::S); }
 
 }  // namespace fastk
 }  // namespace bhcp

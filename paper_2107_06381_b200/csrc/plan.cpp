@@ -285,7 +285,17 @@ bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx
   return true;
 }
 
-bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::string* err) {
+// n = 1025 = 41 x 25, Cooley-Tukey with a Rader 41-point first stage (gt_modes.cuh).
+// Layout (double2): sgen [8][128] shifts of the generator (beta, pencil p =
+// alpha * 25 + j2: j = 25 * g^((8 alpha + 5 beta) mod 40) + j2) | y0 shifts [32]
+// (j = j2) | tw [25][41] w1025^(j2 * k1(cpos)) | gi [25][41] 1/gamma_(k1(cpos) +
+// 41 k2) | bh [8][5] bhat40[K], K = CRT(k1' mod 5, k2 mod 8).
+// int: ck1 [41] k1 per stage-C lane position | csl [41] slot of Y(j2, k1) in a
+// row | gpw [40] g^e mod 41 (generator index recovery on the singular path).
+// Stage-C lane positions: 5 groups of 8 (k1 = 1..40) whose row slots are
+// distinct mod 8 (conflict-free 16-byte reads), then k1 = 0 (slot 41 = y0 + A0).
+bool build_gt2_tables(const double* shifts, const double* gaminv, std::vector<double2>* cplx, std::vector<int>* idx,
+                      std::string* err) {
   const int p = 41, NP = 40;
   auto powmod = [p](long long b, long long e) {
     long long r = 1;
@@ -296,29 +306,64 @@ bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::str
   int g = 2;   // smallest primitive root: g^(40/2) != 1 and g^(40/5) != 1
   while (powmod(g, NP / 2) == 1 || powmod(g, NP / 5) == 1) ++g;
   const long long ginv = powmod(g, p - 2);
-  cplx->assign(40 + 25 + 40, make_double2(0.0, 0.0));
-  idx->assign(80, 0);
-  for (int k = 0; k < 40; ++k) {
-    const long double a = -2.0L * kPi * (long double)k / 40.0L;
-    (*cplx)[k] = make_double2((double)cosl(a), (double)sinl(a));
+  cplx->assign(kGt2Total, make_double2(0.0, 0.0));
+  idx->assign(41 + 41 + 40, 0);
+  // generator order
+  for (int beta = 0; beta < 8; ++beta)
+    for (int pc = 0; pc < 125; ++pc) {
+      const int alpha = pc / 25, j2 = pc % 25;
+      const int j = 25 * (int)powmod(g, (8 * alpha + 5 * beta) % 40) + j2;
+      (*cplx)[kGt2Sg + beta * 128 + pc] = make_double2(shifts[2 * j], shifts[2 * j + 1]);
+    }
+  for (int j2 = 0; j2 < 25; ++j2) (*cplx)[kGt2Sg + 1024 + j2] = make_double2(shifts[2 * j2], shifts[2 * j2 + 1]);
+  // row slot of Y(j2, k1): the second FFT40's output (q1, q2) sits at 5 q2 + q1, q = (8 q1 + 5 q2) mod 40,
+  // k1 = g^-q; k1 = 0 at slot 41
+  std::vector<int> sigma(41, 41);
+  for (int q1 = 0; q1 < 5; ++q1)
+    for (int q2 = 0; q2 < 8; ++q2) {
+      const int q = (8 * q1 + 5 * q2) % 40;
+      sigma[powmod(ginv, q)] = 5 * q2 + q1;
+    }
+  // stage-C lane positions: the i-th k1 of each residue class (slot mod 8) goes to group i
+  std::vector<int> ck1(41, 0);
+  {
+    std::vector<int> cnt(8, 0);
+    for (int k1 = 1; k1 <= 40; ++k1) {
+      const int r = sigma[k1] % 8;
+      const int grp = cnt[r]++;
+      if (grp >= 5) { *err = "gt2: slot classes unbalanced"; return false; }
+      ck1[8 * grp + r] = k1;
+    }
+    ck1[40] = 0;
   }
-  for (int k = 0; k < 25; ++k) {
-    const long double a = -2.0L * kPi * (long double)k / 25.0L;
-    (*cplx)[40 + k] = make_double2((double)cosl(a), (double)sinl(a));
+  for (int c = 0; c < 41; ++c) {
+    (*idx)[c] = ck1[c];
+    (*idx)[41 + c] = sigma[ck1[c]];
   }
+  for (int e = 0; e < 40; ++e) (*idx)[82 + e] = (int)powmod(g, e);
+  for (int j2 = 0; j2 < 25; ++j2)
+    for (int c = 0; c < 41; ++c) {
+      const long long e = (long long)j2 * ck1[c] % 1025;
+      const long double a = -2.0L * kPi * (long double)e / 1025.0L;
+      (*cplx)[kGt2Tw + j2 * 41 + c] = make_double2((double)cosl(a), (double)sinl(a));
+      const int t = ck1[c] + 41 * j2;   // here j2 plays k2
+      (*cplx)[kGt2Gi + j2 * 41 + c] = make_double2(gaminv[2 * t], gaminv[2 * t + 1]);
+    }
+  // bhat40 = DFT40(b) / 40, b_m = w41^(g^-m)
   std::vector<cld> bb(NP);
-  long long gp = 1, gm = 1;
+  long long gm = 1;
   for (int q = 0; q < NP; ++q) {
-    (*idx)[q] = (int)gp;        // g^q
-    (*idx)[40 + q] = (int)gm;   // g^-q
     const long double a = -2.0L * kPi * (long double)gm / (long double)p;
-    bb[q] = cld(cosl(a), sinl(a));   // b_q = w41^(g^-q)
-    gp = gp * g % p;
+    bb[q] = cld(cosl(a), sinl(a));
     gm = gm * ginv % p;
   }
   host_dft(bb);
-  for (int k = 0; k < NP; ++k) (*cplx)[65 + k] = to_d2(bb[k] / (long double)NP);
-  (void)err;
+  for (int k2 = 0; k2 < 8; ++k2)
+    for (int k1 = 0; k1 < 5; ++k1) {
+      int K = 0;
+      while (K % 5 != k1 || K % 8 != k2) ++K;
+      (*cplx)[kGt2Bh + k2 * 5 + k1] = to_d2(bb[K] / (long double)NP);
+    }
   return true;
 }
 

@@ -46,10 +46,13 @@ bool build_rader_tables(int n, std::vector<double2>* cplx, std::vector<int>* idx
 
 // Good-Thomas / Rader tables for n = 1025 = 25 x 41 (see fastk::k_modes_gt):
 // cplx = w40 (40) | w25 (25) | bhat40 (40); idx = perm (40) g^p mod 41 | tq (40) g^-q mod 41.
-bool build_gt_tables(std::vector<double2>* cplx, std::vector<int>* idx, std::string* err);
 
 // Prime-factor / Rader tables for n = 4097 = 17 x 241 (see fastk::k_modes_pf):
 // cplx = w240 (240) | bhat240 (240); tq (240) = g^-q mod 241; perm (240) = g^p mod 241.
+// n = 1025 tables of k_modes_gt (gt_modes.cuh); offsets in double2
+constexpr int kGt2Sg = 0, kGt2Tw = 1056, kGt2Gi = kGt2Tw + 1025, kGt2Bh = kGt2Gi + 1025, kGt2Total = kGt2Bh + 40;
+bool build_gt2_tables(const double* shifts, const double* gaminv, std::vector<double2>* cplx, std::vector<int>* idx,
+                      std::string* err);
 bool build_pf_tables(std::vector<double2>* cplx, std::vector<int>* tq, std::vector<int>* perm, std::string* err);
 
 // Upload the odd-radix codelet constants to the current device (idempotent).

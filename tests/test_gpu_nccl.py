@@ -65,4 +65,4 @@ def test_bench_sharded_line_world1(transport):
     for key in ("metric", "value", "unit", "n_gpus", "ms_per_step", "e2e", "gpu_launches", "clocks", "roofline"):
         assert key in line
     assert line["value"] > 0
-    assert line["config"]["transport"] == transport
+    assert line["transport"] == transport
