@@ -847,10 +847,14 @@ void set_all_attributes() {
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
-  allow_smem(fastk::k_modes_gt<false, false>);
-  allow_smem(fastk::k_modes_gt<true, false>);
-  allow_smem(fastk::k_modes_gt<false, true>);
-  allow_smem(fastk::k_modes_gt<true, true>);
+  allow_smem(fastk::k_modes_gt<false, false, false>);
+  allow_smem(fastk::k_modes_gt<true, false, false>);
+  allow_smem(fastk::k_modes_gt<false, true, false>);
+  allow_smem(fastk::k_modes_gt<true, true, false>);
+  allow_smem(fastk::k_modes_gt<false, false, true>);
+  allow_smem(fastk::k_modes_gt<true, false, true>);
+  allow_smem(fastk::k_modes_gt<false, true, true>);
+  allow_smem(fastk::k_modes_gt<true, true, true>);
   allow_smem(fastk::k_modes_rader<257, false>);
   allow_smem(fastk::k_modes_rader<257, true>);
   allow_smem(fastk::k_modes_fast<513, false>);
@@ -1205,16 +1209,16 @@ bool may_be_singular(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
   return false;
 }
 
-template <bool CHECK>
+template <bool CHECK, bool FAST>
 int gt_launch(const fastk::GtModesArgs& a, bool sym, size_t sm, cudaStream_t s) {
   using namespace fastk;
   if (sym) {
-    const long long grid = std::min<long long>(a.ntiles, resident_ctas(k_modes_gt<true, CHECK>, GtPlan::T, sm));
-    k_modes_gt<true, CHECK><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+    const long long grid = std::min<long long>(a.ntiles, resident_ctas(k_modes_gt<true, CHECK, FAST>, GtPlan::T, sm));
+    k_modes_gt<true, CHECK, FAST><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
   } else {
     const long long work = (a.k_count + GtPlan::S - 1) / GtPlan::S;
-    const long long grid = std::min<long long>(work, resident_ctas(k_modes_gt<false, CHECK>, GtPlan::T, sm));
-    k_modes_gt<false, CHECK><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
+    const long long grid = std::min<long long>(work, resident_ctas(k_modes_gt<false, CHECK, FAST>, GtPlan::T, sm));
+    k_modes_gt<false, CHECK, FAST><<<(unsigned)grid, GtPlan::T, sm, s>>>(a);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_gt launch");
   return BHCP_OK;
@@ -1229,17 +1233,20 @@ int gt_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
   a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin; a.W = W; a.m = sp->m; a.dim = sp->dim;
   a.st = st; a.wl = wl; a.tab = tp->gt; a.itab = tp->gt_idx;
   const size_t sm = gt_smem();
-  const bool sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
+  const bool want_sym = sr.on || (sp->dim >= 2 && k_begin == 0 && k_end == sp->nx && wl.nmodes == sp->nx);
   long long cnt = 0;
-  a.tiles = sym ? seg_tiles(sp, GtPlan::S, &cnt) : nullptr;
-  if (sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
+  a.tiles = want_sym ? seg_tiles(sp, GtPlan::S, &cnt) : nullptr;
+  if (want_sym && !a.tiles && sr.on) return fail(BHCP_ERR_INVALID, "symmetric tile list not built for this plan");
   if (a.tiles) {
     window(sr, a.tiles, cnt);
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
   }
-  return may_be_singular(sp, tp) ? gt_launch<true>(a, a.tiles != nullptr, sm, s)
-                                 : gt_launch<false>(a, a.tiles != nullptr, sm, s);
+  const bool sym = a.tiles != nullptr;
+  const bool fast = wl.mode_major && wl.nsl == 1 && !wl.sl_koff[0] && wl.P1 * fastk::kTBL * 129 < (1LL << 31);
+  if (may_be_singular(sp, tp))
+    return fast ? gt_launch<true, true>(a, sym, sm, s) : gt_launch<true, false>(a, sym, sm, s);
+  return fast ? gt_launch<false, true>(a, sym, sm, s) : gt_launch<false, false>(a, sym, sm, s);
 }
 
 int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* ghat, double cscale,

@@ -18,7 +18,7 @@
 // slot 5y + x for FFT40 position (x, y), slot 40 = y0, slot 41 = Y(j2, 0)),
 // and every small DFT runs in registers:
 //   R1  (4 rounds, pencils (x, j2)): generator 1/(s_j + mu) -> DFT8 over y
-//   R2  (7 rounds, pencils (y, j2)): DFT5 over x -> * bhat, conj -> DFT5
+//   R2  (7 rounds, lane = (y, j2 mod 4)): DFT5 over x -> * bhat, conj -> DFT5
 //   R3  (4 rounds, pencils (x, j2)): DFT8 over y -> y0 + conj
 //   C   (2 rounds, lane = column k1): twiddle, DFT25 (5 x 5) over j2,
 //       Gamma^-1, Re, residue norms, and the store of W[t] straight from
@@ -131,7 +131,10 @@ __device__ __forceinline__ GtItem gt_decode(const GtModesArgs& a, long long item
   return it;
 }
 
-template <bool SYM, bool CHECK>
+// FAST: one level slab without a block table (the single-GPU blocked W): the
+// store offset of level t is (t / 8) * P1 * 8 + t % 8 from the mode's base;
+// otherwise w_level_ptr walks the slabs (multi-GPU layouts, 1D level-major W).
+template <bool SYM, bool CHECK, bool FAST>
 __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
   constexpr int S = GtPlan::S, T = GtPlan::T, RS = kGtRS;
   extern __shared__ double2 smem[];
@@ -152,7 +155,6 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
   double2* Y = smem + kGt2Total + warp * kGtRowWords;
   StatusDev* st = a.st;
   const WLayout& wl = a.wl;
-  const bool fast_store = wl.mode_major && wl.nsl == 1 && !wl.sl_koff[0];
   double sre = 0.0, sim = 0.0;
   const long long nitems = SYM ? a.ntiles * S : a.k_count;
 
@@ -211,37 +213,46 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
     }
     if (lane < 25) Y[lane * RS + 40] = gen_inv<CHECK>(s_sg[1024 + lane], mu, st, lane);   // y0 = v_{j2}
     __syncwarp();
-    // ---- R2: DFT5 over x, * bhat, conj, DFT5; pencils p = y * 25 + j2, two per lane at a time
+    // ---- R2: DFT5 over x, * bhat, conj, DFT5. Lane l keeps y = l % 8 (its five
+    // bhat factors stay in registers) and takes rows j2 = l / 8 + 4 r, two rows at a time
+    {
+      const int y = lane & 7;
+      double2 bh[5];
+#pragma unroll
+      for (int x = 0; x < 5; ++x) bh[x] = s_bh[y * 5 + x];
 #pragma unroll 1
-    for (int h = 0; h < 4; ++h) {
-      const int pa = lane + 64 * h, pb = pa + 32;
-      const bool oka = pa < 200, okb = pb < 200;
-      const int ya = pa / 25, ja = pa - ya * 25, yb = pb / 25, jb = pb - yb * 25;
-      double2* rowa = Y + ja * RS;
-      double2* rowb = Y + jb * RS;
-      double2 ua[5], ub[5];
+      for (int r = 0; r < 7; r += 2) {
+        const int ja = (lane >> 3) + 4 * r, jb = ja + 4;
+        const bool oka = ja < 25, okb = jb < 25 && r + 1 < 7;
+        double2* rowa = Y + ja * RS;
+        double2* rowb = Y + jb * RS;
+        double2 ua[5], ub[5];
 #pragma unroll
-      for (int x = 0; x < 5; ++x) {
-        ua[x] = oka ? rowa[5 * ya + x] : make_double2(0.0, 0.0);
-        ub[x] = okb ? rowb[5 * yb + x] : make_double2(0.0, 0.0);
-      }
-      sfft::Cod<5>::run(ua);
-      sfft::Cod<5>::run(ub);
-      if (oka && ya == 0) rowa[41] = cadd(rowa[40], ua[0]);   // Y(j2, 0) = y0 + A_0
+        for (int x = 0; x < 5; ++x) {
+          ua[x] = oka ? rowa[5 * y + x] : make_double2(0.0, 0.0);
+          ub[x] = okb ? rowb[5 * y + x] : make_double2(0.0, 0.0);
+        }
+        sfft::Cod<5>::run(ua);
+        sfft::Cod<5>::run(ub);
+        if (y == 0) {   // Y(j2, 0) = y0 + A_0
+          if (oka) rowa[41] = cadd(rowa[40], ua[0]);
+          if (okb) rowb[41] = cadd(rowb[40], ub[0]);
+        }
 #pragma unroll
-      for (int x = 0; x < 5; ++x) {
-        ua[x] = cconj(cmul(ua[x], s_bh[(oka ? ya : 0) * 5 + x]));
-        ub[x] = cconj(cmul(ub[x], s_bh[(okb ? yb : 0) * 5 + x]));
-      }
-      sfft::Cod<5>::run(ua);
-      sfft::Cod<5>::run(ub);
-      if (oka) {
+        for (int x = 0; x < 5; ++x) {
+          ua[x] = cconj(cmul(ua[x], bh[x]));
+          ub[x] = cconj(cmul(ub[x], bh[x]));
+        }
+        sfft::Cod<5>::run(ua);
+        sfft::Cod<5>::run(ub);
+        if (oka) {
 #pragma unroll
-        for (int x = 0; x < 5; ++x) rowa[5 * ya + x] = ua[x];
-      }
-      if (okb) {
+          for (int x = 0; x < 5; ++x) rowa[5 * y + x] = ua[x];
+        }
+        if (okb) {
 #pragma unroll
-        for (int x = 0; x < 5; ++x) rowb[5 * yb + x] = ub[x];
+          for (int x = 0; x < 5; ++x) rowb[5 * y + x] = ub[x];
+        }
       }
     }
     __syncwarp();
@@ -273,9 +284,9 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
     __syncwarp();
     // ---- C: column k1 per lane: twiddle, DFT25 over j2, Gamma^-1, Re, norms, stores
     double zr2 = 0.0, zi2 = 0.0;
-    const long long dstride = fast_store ? wl.P1 * kTBL : 0;
-    double* const based = fast_store ? wl.sl_base[0] + wl.row_off(0, it.k1d) + it.rd * kTBL : nullptr;
-    double* const basem = fast_store ? wl.sl_base[0] + wl.row_off(0, it.k1m) + it.rm * kTBL : nullptr;
+    const int dstride = FAST ? (int)(wl.P1 * kTBL) : 0;
+    double* const based = FAST ? wl.sl_base[0] + wl.row_off(0, it.k1d) + it.rd * kTBL : nullptr;
+    double* const basem = FAST ? wl.sl_base[0] + wl.row_off(0, it.k1m) + it.rm * kTBL : nullptr;
 #pragma unroll 1
     for (int cp = lane; cp < 41; cp += 32) {
       const int k1 = s_ck1[cp];
@@ -309,8 +320,8 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
           const double zi = fma(u[d].x, gi.y, u[d].y * gi.x);
           zr2 = fma(zr, zr, zr2);
           zi2 = fma(zi, zi, zi2);
-          if (fast_store) {
-            const long long off = (long long)(t >> 3) * dstride + (t & 7);
+          if (FAST) {
+            const int off = (t >> 3) * dstride + (t & 7);
             based[off] = c * zr;
             if (it.hm) basem[off] = c2 * zr;
           } else {
