@@ -3,11 +3,13 @@
 usage: python tools/ncu_summary.py <full.ncu-rep> <launches.csv> <out_prefix>
 writes <out_prefix>_ncu_full.csv (selected raw metrics per captured kernel),
 <out_prefix>_launches.csv (copy) and <out_prefix>_summary.md, and updates
-profiles/ncu_traffic_c2.json (DRAM bytes per launch per kernel, used by bench.py).
+profiles/ncu_traffic_<config>.json (DRAM bytes per launch per kernel, used by bench.py;
+the config is the prefix's _cN part, default c2).
 """
 import csv
 import io
 import json
+import re
 import shutil
 import subprocess
 import sys
@@ -89,6 +91,7 @@ for d in out_rows:
                  f"{d.get('sm__warps_active.avg.pct_of_peak_sustained_active','')} | "
                  f"{d.get('launch__registers_per_thread','')} |")
 Path(f"{prefix}_summary.md").write_text("\n".join(lines) + "\n")
-tf = Path("profiles/ncu_traffic_c2.json")
+cfg = next((p for p in Path(prefix).name.split("_") if re.fullmatch(r"c[1-5]", p)), "c2")
+tf = Path(f"profiles/ncu_traffic_{cfg}.json")
 tf.write_text(json.dumps({k: v[1] for k, v in traffic.items()}, indent=1) + "\n")
 print("\n".join(lines))
