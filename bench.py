@@ -252,6 +252,9 @@ def main():
         sp, tp = plan.sp.handle, plan.tp.handle
         ev = None
         wax = bool(lib.bhcp_pint_w_passes_supported(sp))
+        # the one-kernel level-group pass (k_dst_lvl4: 2D, m + 1 = 1024)
+        lvl_sync = int(lib.bhcp_pint_levels_sync_bytes(sp, n))
+        sync_buf = torch.zeros(max(lvl_sync, 8) // 4 + 1, dtype=torch.int32, device=dev)
 
         def step(record=None):
             # phases: [0] ghat, [1] k_modes, [2 + a] DST axis pass a
@@ -266,7 +269,11 @@ def main():
                 record[2].record()
             # the solve's own pass order (bhcp_pint_levels): strided axes in place
             # on W (k_dst_wax), then the last axis W -> y (k_dst_blk2)
-            if wax:
+            if lvl_sync:
+                _lib.check(lib.bhcp_pint_levels_fused(sp, W, plans.ptr(y), n, plans.ptr(sync_buf), sh), "levels")
+                if record:
+                    record[3].record()
+            elif wax:
                 for a in range(w.dim - 1):
                     _lib.check(lib.bhcp_pint_w_pass(sp, W, n, a, sh), "w pass")
                     if record:
@@ -280,7 +287,9 @@ def main():
                     if record:
                         record[3 + a].record()
 
-        launches_per_step = 1 + w.dim + 1 + w.dim  # graph of bhcp_pint_solve: reset, ghat passes, modes, level passes
+        # kernels in the graph of bhcp_pint_solve: reset, ghat passes, modes, level
+        # passes (the level-group pass is one kernel after a memset node)
+        launches_per_step = 1 + w.dim + 1 + (1 if lvl_sync else w.dim)
         sampler = ClockSampler(local)
         sampler.start()
         time.sleep(0.5)  # let nvidia-smi start sampling before the GPU is loaded
@@ -288,7 +297,7 @@ def main():
             step()
         torch.cuda.synchronize()
         plan.check_status()
-        nph = 3 + w.dim
+        nph = 4 if lvl_sync else 3 + w.dim
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nph)] for _ in range(args.steps)]
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -317,7 +326,9 @@ def main():
         phase_ms /= args.steps
         modes_kernel = {257: "k_modes_rader", 513: "k_modes_fast", 1025: "k_modes_gt", 4097: "k_modes_pf"}.get(n, "k_modes")
         names = ["ghat (DST of g)", f"{modes_kernel} (shifts + time FFT + Gamma^-1 + Re)"]
-        if wax:
+        if lvl_sync:
+            names += ["k_dst_lvl4 level phase (both axes, W -> y, L2-resident level tiles)"]
+        elif wax:
             names += [("k_dst_wax2" if w.num_cells == 512 else "k_dst_wax") +
                       f" W pass (spatial axis {a}, in place, TMA)" for a in range(w.dim - 1)]
             names += ["k_dst_blk3 level pass (axis -1, W -> y)"]
@@ -327,7 +338,7 @@ def main():
         dom = int(np.argmax(phase_ms))
         # algorithmic bytes per launch of each kernel
         dof = w.dof
-        alg_bytes = [16.0 * nx, 8.0 * dof + 8.0 * nx] + [16.0 * dof] * w.dim
+        alg_bytes = [16.0 * nx, 8.0 * dof + 8.0 * nx] + [16.0 * dof] * (nph - 3)
         hbm, peak_kind = peaks()
         # DRAM bytes per launch of each kernel from the committed ncu --set full capture
         tfile = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"

@@ -107,6 +107,7 @@ __device__ __forceinline__ double2 shifted_divide(double2 x, double2 s, double m
 #include "pf_modes.cuh"
 #include "wax_dst.cuh"
 #include "wax2_dst.cuh"
+#include "lvl_dst.cuh"
 #include <cudaTypedefs.h>
 namespace bhcp {
 
@@ -844,6 +845,7 @@ void set_all_attributes() {
   allow_smem(wax2::k_dst_blk3<512>);
   allow_smem(wax2::k_dst_blk3<256>);
   allow_smem(wax2::k_dst_blk4);
+  allow_smem(lvl::k_dst_lvl4);
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
@@ -907,6 +909,8 @@ void cols_fast(const bhcp_space_plan* sp, const double* in, double* out, int cpl
 
 bool fast_dst_length(int L) { return L == 512 || L == 1024 || L == 2048 || L == 8192; }
 bool g_disable_fast = false;
+int g_lvl4 = 1;          // BHCP_LVL4=0: c3 level phase as two sweeps (k_dst_blk4 + k_dst_cols3)
+int g_lvl4_kfirst = -1;  // BHCP_LVL4_KFIRST: row-task pairs of a phase before its column tasks (default: grid)
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -1699,6 +1703,69 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
   return fail(BHCP_ERR_INVALID, "w_pass length");
 }
 
+// m + 1 = 1024 in 2D (c3): the whole level phase as one persistent kernel over
+// L2-resident level tiles (k_dst_lvl4, lvl_dst.cuh): row tasks W -> y, then
+// column tasks in place on y while the level tile is still in L2. gsync: one
+// counter per level tile, zeroed on the stream before the launch.
+bool lvl4_ok(const bhcp_space_plan* sp) {
+  return g_lvl4 != 0 && !g_disable_fast && sp->dim == 2 && sp->m + 1 == 1024;
+}
+// scratch of the level-group pass: per-level-tile counters, then the two Z
+// slots (8 levels x m rows x 1024 doubles each)
+size_t lvl4_counter_bytes(long long nlev) {
+  return (2 * sizeof(unsigned) * (size_t)((nlev + fastk::kTBL - 1) / fastk::kTBL + 1) + 255) & ~size_t(255);
+}
+size_t lvl4_sync_bytes(long long nlev) {
+  return lvl4_counter_bytes(nlev) + sizeof(double) * 2 * 8 * (size_t)1023 * lvl::kZPitch;
+}
+
+int lvl4_launch(const bhcp_space_plan* sp, const double* W, double* y, long long nlev, unsigned* gsync,
+                cudaStream_t s) {
+  const long long m = sp->m;
+  const long long NT = (nlev + fastk::kTBL - 1) / fastk::kTBL;
+  if (NT == 0) return BHCP_OK;
+  const long long No = m * NT;                // W blocks
+  const long long nct = (m + 7) / 8;          // column tiles per level (128)
+  const long long ntasks = NT * lvl::kRowTasks + nlev * nct;
+  if (ntasks > 0x7fffffffLL || m != 1023) return fail(BHCP_ERR_INVALID, "level-group pass: bad shape");
+  if (reinterpret_cast<uintptr_t>(W) % 16 != 0 || reinterpret_cast<uintptr_t>(gsync) % 256 != 0)
+    return fail(BHCP_ERR_INVALID, "W must be 16-byte and the scratch 256-byte aligned");
+  double* z = reinterpret_cast<double*>(reinterpret_cast<char*>(gsync) + lvl4_counter_bytes(nlev));
+  alignas(64) CUtensorMap tm, tz;
+  int rc = tensor_map_3d(&tm, const_cast<double*>(W), fastk::kTBL, m, No, fastk::kTBL, fastk::kTBL * m,
+                         fastk::kTBL, 64);
+  if (rc) return rc;
+  // Z: {1024 columns, m rows, 16 slot levels}, box 8 columns x 256 rows (64 B rows)
+  rc = tensor_map_3d(&tz, z, lvl::kZPitch, m, 16, lvl::kZPitch, lvl::kZPitch * m, 8, 64);
+  if (rc) return rc;
+  // y row pairs: {2046 = parity x 1023 + column, floor(rows / 2) pairs}, pitch 2 * 1023 doubles
+  if (reinterpret_cast<uintptr_t>(y) % 16 != 0) return fail(BHCP_ERR_INVALID, "y must be 16-byte aligned");
+  alignas(64) CUtensorMap ty256, ty255;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * m), (cuuint64_t)(nlev * m / 2)};
+    const cuuint64_t strides[1] = {(cuuint64_t)(2 * m * sizeof(double))};
+    const cuuint32_t estr[2] = {1, 1};
+    for (int k = 0; k < 2; ++k) {
+      const cuuint32_t box[2] = {8, (cuuint32_t)(k ? 255 : 256)};
+      CUresult r = g_encode_tiled(k ? &ty255 : &ty256, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, y, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(BHCP_ERR_INVALID, "cuTensorMapEncodeTiled (y pairs) failed (code " + std::to_string((int)r) + ")");
+    }
+  }
+  const size_t sm = lvl::smem_bytes();
+  // every CTA must be resident at once (column tasks wait for row tasks of other CTAs)
+  const long long grid = std::min<long long>((ntasks + 1) / 2, resident_ctas(lvl::k_dst_lvl4, lvl::kThreads, sm));
+  if (cudaMemsetAsync(gsync, 0, lvl4_counter_bytes(nlev), s) != cudaSuccess) return cuda_fail("lvl4 sync reset");
+  const int kfirst = g_lvl4_kfirst >= 0 ? g_lvl4_kfirst : (int)grid;
+  lvl::ArgsLV a{sp->twN, sp->snN, sqrt(2.0 / 1024), y, z, gsync, gsync + (NT + 1), (int)m, (int)NT, (int)nlev,
+                (int)nct, (int)ntasks, kfirst};
+  lvl::k_dst_lvl4<<<(unsigned)grid, lvl::kThreads, sm, s>>>(tm, tz, ty256, ty255, a);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_lvl4 launch");
+  return BHCP_OK;
+}
+
 // All spatial passes of the fused solve: W (blocked) -> y.
 // koff == null: k1 blocks at the uniform stride NT * P1 * 8 (the single-slab
 // W and every slab receive buffer). Fast lengths in 2D/3D then run the strided
@@ -1708,7 +1775,8 @@ int w_pass(const bhcp_space_plan* sp, double* W, long long nlev, int axis, cudaS
 // general passes (pass 0 into y by k_dst_blk2 / unpack + rows, then the
 // strided axes in place on y); W is left untouched.
 int levels_all(const bhcp_space_plan* sp, double* W, const long long* koff, double* y, long long nlev,
-               cudaStream_t s) {
+               cudaStream_t s, unsigned* gsync = nullptr) {
+  if (!koff && gsync && lvl4_ok(sp)) return lvl4_launch(sp, W, y, nlev, gsync, s);
   if (!koff && wax_ok(sp)) {
     for (int a = 0; a < sp->dim - 1; ++a) {
       int rc = w_pass(sp, W, nlev, a, s);
@@ -1754,6 +1822,10 @@ bool ensure_device_constants(int device, std::string* err) {
   {
     const char* e = getenv("BHCP_DISABLE_FAST");
     g_disable_fast = (e && e[0] == '1');
+    const char* l4 = getenv("BHCP_LVL4");
+    if (l4) g_lvl4 = atoi(l4);
+    const char* kf = getenv("BHCP_LVL4_KFIRST");
+    if (kf) g_lvl4_kfirst = atoi(kf);
 
   }
   set_all_attributes();
@@ -2051,7 +2123,8 @@ int bhcp_from_eigenspace(const bhcp_time_plan* tp, const void* in, int64_t batch
 size_t bhcp_pint_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp) {
   if (!sp || !tp) return 0;
   return align256(sizeof(StatusDev)) + align256(sizeof(double) * sp->nx) +
-         align256(sizeof(double) * (size_t)native_w_elems(sp, tp->n));
+         align256(sizeof(double) * (size_t)native_w_elems(sp, tp->n)) +
+         (lvl4_ok(sp) ? align256(lvl4_sync_bytes(tp->n)) : 0);
 }
 
 void* bhcp_pint_status_ptr(const bhcp_space_plan*, const bhcp_time_plan*, void* ws) { return ws; }
@@ -2201,13 +2274,32 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   StatusDev* st = (StatusDev*)w;
   double* ghat = (double*)(w + align256(sizeof(StatusDev)));
   double* W = (double*)(w + align256(sizeof(StatusDev)) + align256(sizeof(double) * sp->nx));
+  unsigned* gsync = (unsigned*)((char*)W + align256(sizeof(double) * (size_t)native_w_elems(sp, tp->n)));
   k_status_reset<<<1, 32, 0, s>>>(st);
   int rc = sine_passes(sp, g_dev, ghat, 0, 1, s);
   if (rc) return rc;
   const double cscale = 1.0 / (divisor * (double)tp->n);
   rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, native_layout(sp, sp->nx, tp->n), st, s);
   if (rc) return rc;
-  return levels_all(sp, W, nullptr, y_dev, tp->n, s);
+  return levels_all(sp, W, nullptr, y_dev, tp->n, s, gsync);
+}
+
+size_t bhcp_pint_levels_sync_bytes(const bhcp_space_plan* sp, int64_t nlev) {
+  if (!sp || nlev <= 0 || !lvl4_ok(sp)) return 0;
+  return lvl4_sync_bytes(nlev);
+}
+
+int bhcp_pint_levels_fused(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t nlev,
+                           void* sync_dev, void* stream) {
+  if (!sp || !in_dev || !out_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
+  if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  if (lvl4_ok(sp)) {
+    if (!sync_dev) return fail(BHCP_ERR_INVALID, "the level-group pass needs a sync buffer");
+    return lvl4_launch(sp, in_dev, out_dev, nlev, (unsigned*)sync_dev, s);
+  }
+  return levels_all(sp, const_cast<double*>(in_dev), nullptr, out_dev, nlev, s);
 }
 
 int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev, const int64_t* koff_dev,

@@ -5,7 +5,9 @@ inverse DST moved after the time transform). For m + 1 in
 {256, 512} the strided axes run in place on the blocked W (k_dst_wax /
 k_dst_wax2, TMA tiles) and the last axis moves W -> y (k_dst_blk3); for 1024
 the last axis moves W -> y first (k_dst_blk4, two warps per line pair) and the
-strided axis runs on y (k_dst_cols3). These
+strided axis runs on y (k_dst_cols3); in 2D the solve runs both as one
+persistent level-group kernel over L2-resident level tiles (k_dst_lvl4,
+bhcp_pint_levels_fused). These
 tests feed seeded random blocked W -- with NaN in the padding levels of the
 last level tile, which pass A never writes -- through every entry point that
 runs those kernels and compare with the oracle's orthonormal DST
@@ -59,6 +61,11 @@ def run_levels(sp, W_host, L, dim, m, how):
         else:
             for p in range(dim):
                 _lib.check(lib.bhcp_pint_level_pass(sp, plans.ptr(W), None, plans.ptr(y), L, p, sh), "level pass")
+    elif how == "fused":
+        # the one-kernel level-group pass (k_dst_lvl4 where the sync size is > 0)
+        nb = lib.bhcp_pint_levels_sync_bytes(sp, L)
+        sync = torch.full((max(nb, 8) // 4 + 1,), 12345, dtype=torch.int32, device="cuda")   # the call zeroes it
+        _lib.check(lib.bhcp_pint_levels_fused(sp, plans.ptr(W), plans.ptr(y), L, plans.ptr(sync), sh), "levels_fused")
     elif how == "blocked":
         # an all-to-all receive buffer at the uniform k1 stride (koff NULL): the TMA passes
         _lib.check(lib.bhcp_pint_levels_blocked(sp, plans.ptr(W), None, plans.ptr(y), L, sh), "levels_blocked")
@@ -77,7 +84,8 @@ def run_levels(sp, W_host, L, dim, m, how):
 
 @pytest.mark.parametrize("dim,cells,L", [(2, 512, 1), (2, 512, 7), (2, 512, 8), (2, 512, 9), (2, 512, 13),
                                          (2, 512, 16), (2, 256, 5), (2, 256, 8), (2, 256, 11), (3, 256, 1),
-                                         (3, 256, 3), (2, 1024, 1), (2, 1024, 6), (2, 1024, 9), (2, 1024, 16)])
+                                         (3, 256, 3), (2, 1024, 1), (2, 1024, 6), (2, 1024, 9), (2, 1024, 16),
+                                         (2, 1024, 23), (2, 1024, 41)])
 def test_level_passes_vs_oracle(dim, cells, L):
     grid = B.build_grid(dim, 1.0, cells)
     m = cells - 1
@@ -99,6 +107,17 @@ def test_level_passes_vs_oracle(dim, cells, L):
     assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "blocked"), y)
     yt = run_levels(plan.handle, W, L, dim, m, "table")
     assert rel(yt, ref) <= 1e-13, "explicit block table"
+    # the level-group kernel (m + 1 = 1024 in 2D; elsewhere the same passes as above)
+    fused = lib.bhcp_pint_levels_sync_bytes(plan.handle, L) > 0
+    assert fused == (dim == 2 and cells == 1024)
+    yf = run_levels(plan.handle, W, L, dim, m, "fused")
+    assert np.isfinite(yf).all(), "padding NaN leaked into a valid level (fused)"
+    assert rel(yf, ref) <= 1e-13, f"fused rel-L2 {rel(yf, ref):.2e}"
+    if not fused:
+        assert np.array_equal(yf, y)
+    else:
+        # deterministic: a second run gives the same bits
+        assert np.array_equal(run_levels(plan.handle, W, L, dim, m, "fused"), yf)
 
 
 @pytest.mark.parametrize("dim,cells", [(2, 512), (3, 256)])
