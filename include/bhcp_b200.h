@@ -257,6 +257,22 @@ int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev,
  * concurrent calls. Where the sync size is 0 this is bhcp_pint_levels (the
  * input may be overwritten) and sync_dev is ignored. Reference: the per-level
  * DSTs of pint.py:94-96 / space.py:163-177. */
+/* bhcp_pint_solve_batch: nb independent fused solves of one g on one space
+ * plan (BASELINE config 5: the alpha sweep, 64 alpha x 2 kinds), each with its
+ * own time plan tps[i] (its omega) and divisor divisors[i] (host array), all
+ * time plans of one length. y_dev holds the nb trajectories one after the
+ * other ((nb, n_levels, n_space) float64); status_dev holds nb status blocks
+ * (bhcp_status_bytes() each, read with bhcp_read_status). One DST of g serves
+ * every pair; for 1D with n = 4097 pass A of up to 32 pairs runs as one launch
+ * and the level phase of all pairs as one transpose and one rows DST, so a
+ * chunk of the sweep needs no host synchronisation. Each trajectory is bitwise
+ * the one bhcp_pint_solve gives for that pair. Reference: solve_pint
+ * (pint.py:69-110) per (kind, alpha) as the driver's sweep calls it
+ * (bench.py:196-209, 265-271). */
+size_t bhcp_pint_batch_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, int nb);
+int bhcp_pint_solve_batch(const bhcp_space_plan* sp, const bhcp_time_plan* const* tps, int nb,
+                          const double* g_dev, const double* divisors, double* y_dev, void* status_dev,
+                          void* ws, size_t ws_bytes, void* stream);
 size_t bhcp_pint_levels_sync_bytes(const bhcp_space_plan* sp, int64_t nlev);
 int bhcp_pint_levels_fused(const bhcp_space_plan* sp, const double* in_dev, double* out_dev,
                            int64_t nlev, void* sync_dev, void* stream);

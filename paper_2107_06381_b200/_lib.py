@@ -76,6 +76,8 @@ SIGNATURES = {
     "bhcp_pint_w_passes_supported": (_int, [_vp]),
     "bhcp_pint_levels": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "bhcp_pint_levels_sync_bytes": (ctypes.c_size_t, [_vp, _i64]),
+    "bhcp_pint_batch_workspace_bytes": (ctypes.c_size_t, [_vp, _vp, _int]),
+    "bhcp_pint_solve_batch": (_int, [_vp, _vp, _int, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "bhcp_pint_levels_fused": (_int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "bhcp_pint_levels_blocked": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "bhcp_spectral_workspace_bytes": (ctypes.c_size_t, [_vp, _i64]),

@@ -551,6 +551,15 @@ __global__ void __launch_bounds__(VT<V>::T, VT<V>::MINB) k_modes(ModesArgs a) {
 }
 
 // ------------------------------------------------------------------ small kernels
+__global__ void k_status_reset_n(StatusDev* st, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    st[i].bad_col = ~0ull;
+    st[i].sum_re2 = 0.0;
+    st[i].sum_im2 = 0.0;
+    st[i].work = 0;
+    st[i].done = 0;
+  }
+}
 __global__ void k_status_reset(StatusDev* st) {
   if (threadIdx.x == 0) {
     st->bad_col = ~0ull;
@@ -589,6 +598,24 @@ __global__ void k_transpose_ld(const double* __restrict__ in, long long ld, doub
   for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
     const long long c = c0 + dy, r = r0 + threadIdx.x;
     if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][dy];
+  }
+}
+
+// k_transpose_ld over a batch of matrices (blockIdx.z): in + z * in_stride -> out + z * rows * cols
+__global__ void k_transpose_ld_batch(const double* __restrict__ in, long long ld, long long in_stride,
+                                     double* __restrict__ out, long long rows, long long cols) {
+  __shared__ double tile[32][33];
+  const double* src = in + (long long)blockIdx.z * in_stride;
+  double* dst = out + (long long)blockIdx.z * rows * cols;
+  const long long c0 = (long long)blockIdx.x * 32, r0 = (long long)blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[dy][threadIdx.x] = src[r * ld + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const long long c = c0 + dy, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][dy];
   }
 }
 
@@ -849,6 +876,7 @@ void set_all_attributes() {
 
   allow_smem(fastk::k_modes_pf<false>);
   allow_smem(fastk::k_modes_pf<true>);
+  allow_smem(fastk::k_modes_pf<false, true>);
   allow_smem(fastk::k_modes_gt<false, false, false>);
   allow_smem(fastk::k_modes_gt<true, false, false>);
   allow_smem(fastk::k_modes_gt<false, true, false>);
@@ -1271,12 +1299,45 @@ int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
     if (cnt == 0) return BHCP_OK;
     a.ntiles = cnt;
     const long long grid = std::min<long long>(cnt, resident_ctas(k_modes_pf<true>, PfPlan::T, sm));
-    k_modes_pf<true><<<(unsigned)grid, PfPlan::T, sm, s>>>(a);
+    k_modes_pf<true><<<(unsigned)grid, PfPlan::T, sm, s>>>(a, PfPairs{});
   } else {
     const long long grid = std::min<long long>(a.k_count, resident_ctas(k_modes_pf<false>, PfPlan::T, sm));
-    k_modes_pf<false><<<(unsigned)grid, PfPlan::T, sm, s>>>(a);
+    k_modes_pf<false><<<(unsigned)grid, PfPlan::T, sm, s>>>(a, PfPairs{});
   }
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_pf launch");
+  return BHCP_OK;
+}
+
+// Pass A of nb independent solves (one launch per kPfMaxPairs pairs): 1D,
+// n = 4097 (BASELINE config 5). Pair i: time plan tps[i], coefficient scale
+// cscales[i], status sts[i], W at W + i * w_stride.
+int pf_modes_batch(const bhcp_space_plan* sp, const bhcp_time_plan* const* tps, int nb, const double* ghat,
+                   const double* cscales, const fastk::WLayout& wl, long long w_stride, StatusDev* sts,
+                   cudaStream_t s) {
+  using namespace fastk;
+  const bhcp_time_plan* tp = tps[0];
+  double* W = wl.sl_base[0];
+  for (int p0 = 0; p0 < nb; p0 += kPfMaxPairs) {
+    const int np = std::min(kPfMaxPairs, nb - p0);
+    PfModesArgs a{};
+    a.shg = tp->pf + 2 * kPfNp; a.thrg = tp->pf_thr; a.jg = tp->pf_idx + kPfNp; a.gaminv = tp->tables + tp->n;
+    a.mu1 = sp->mu1_dev; a.ghat = ghat; a.cscale = cscales[p0]; a.k_begin = 0; a.k_count = sp->nx;
+    a.m = sp->m; a.dim = sp->dim; a.st = sts + p0; a.tab = tp->pf; a.tq = tp->pf_idx;
+    a.wl = wl;
+    a.wl.sl_base[0] = W + (long long)p0 * w_stride;
+    PfPairs pp{};
+    pp.n = np;
+    pp.w_stride = w_stride;
+    for (int i = 0; i < np; ++i) {
+      const bhcp_time_plan* t = tps[p0 + i];
+      pp.shg[i] = t->pf + 2 * kPfNp; pp.thrg[i] = t->pf_thr; pp.gaminv[i] = t->tables + t->n;
+      pp.cscale[i] = cscales[p0 + i]; pp.st[i] = sts + p0 + i;
+    }
+    const size_t sm = pf_smem();
+    const long long grid = std::min<long long>(a.k_count * np, resident_ctas(k_modes_pf<false, true>, PfPlan::T, sm));
+    k_modes_pf<false, true><<<(unsigned)grid, PfPlan::T, sm, s>>>(a, pp);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_modes_pf (batch) launch");
+  }
   return BHCP_OK;
 }
 
@@ -2282,6 +2343,64 @@ int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const d
   rc = launch_modes(sp, tp, ghat, cscale, 0, sp->nx, W, native_layout(sp, sp->nx, tp->n), st, s);
   if (rc) return rc;
   return levels_all(sp, W, nullptr, y_dev, tp->n, s, gsync);
+}
+
+size_t bhcp_pint_batch_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, int nb) {
+  if (!sp || !tp || nb < 1) return 0;
+  return align256(sizeof(double) * sp->nx) + (size_t)nb * align256(sizeof(double) * (size_t)native_w_elems(sp, tp->n));
+}
+
+int bhcp_pint_solve_batch(const bhcp_space_plan* sp, const bhcp_time_plan* const* tps, int nb, const double* g_dev,
+                          const double* divisors, double* y_dev, void* status_dev, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (!sp || !tps || nb < 1 || !g_dev || !divisors || !y_dev || !status_dev || !ws)
+    return fail(BHCP_ERR_INVALID, "null argument");
+  const bhcp_time_plan* tp0 = tps[0];
+  for (int i = 0; i < nb; ++i) {
+    if (!tps[i]) return fail(BHCP_ERR_INVALID, "null time plan");
+    if (tps[i]->n != tp0->n) return fail(BHCP_ERR_INVALID, "time plans of different lengths");
+    if (tps[i]->device != sp->device) return fail(BHCP_ERR_INVALID, "plans on different devices");
+    if (!(divisors[i] != 0.0)) return fail(BHCP_ERR_INVALID, "divisor must be nonzero");
+  }
+  if (ws_bytes < bhcp_pint_batch_workspace_bytes(sp, tp0, nb)) return fail(BHCP_ERR_INVALID, "workspace too small");
+  DeviceGuard g(sp->device);
+  cudaStream_t s = as_stream(stream);
+  StatusDev* st = (StatusDev*)status_dev;
+  double* ghat = (double*)ws;
+  double* W = (double*)((char*)ws + align256(sizeof(double) * sp->nx));
+  const long long w_stride = (long long)(align256(sizeof(double) * (size_t)native_w_elems(sp, tp0->n)) / sizeof(double));
+  const long long n = tp0->n, nx = sp->nx;
+  k_status_reset_n<<<1, 128, 0, s>>>(st, nb);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("status reset");
+  int rc = sine_passes(sp, g_dev, ghat, 0, 1, s);   // one DST of g serves every pair
+  if (rc) return rc;
+  std::vector<double> cs(nb);
+  for (int i = 0; i < nb; ++i) cs[i] = 1.0 / (divisors[i] * (double)n);
+  if (sp->dim == 1 && !g_disable_fast && n == 4097 && tp0->pf) {
+    for (int i = 0; i < nb; ++i)
+      if (!tps[i]->pf) return fail(BHCP_ERR_INVALID, "time plan without prime-factor tables");
+    fastk::WLayout wl = native_layout(sp, nx, n);
+    wl.sl_base[0] = W;
+    rc = pf_modes_batch(sp, tps, nb, ghat, cs.data(), wl, w_stride, st, s);
+    if (rc) return rc;
+    // level phase of every pair at once: mode-major W -> level-major y, then the
+    // rows DST over nb * n levels, lines paired inside each solve (lpl = n: the
+    // pairs of a single solve, so every trajectory is bitwise the unbatched one)
+    const long long NT1 = (n + fastk::kTBL - 1) / fastk::kTBL;
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((sp->m + 31) / 32), (unsigned)nb);
+    k_transpose_ld_batch<<<grid, dim3(32, 8), 0, s>>>(W, NT1 * fastk::kTBL, w_stride, y_dev, sp->m, n);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_transpose_ld_batch");
+    return launch_rows(sp, y_dev, y_dev, 0, (long long)nb * n, 0, nullptr, nullptr, s, Blocked(), n);
+  }
+  // other shapes: the single-solve pipeline per pair (W slots of the workspace)
+  for (int i = 0; i < nb; ++i) {
+    double* Wi = W + (long long)i * w_stride;
+    rc = launch_modes(sp, tps[i], ghat, cs[i], 0, nx, Wi, native_layout(sp, nx, n), st + i, s);
+    if (rc) return rc;
+    rc = levels_all(sp, Wi, nullptr, y_dev + (long long)i * n * nx, n, s);
+    if (rc) return rc;
+  }
+  return BHCP_OK;
 }
 
 size_t bhcp_pint_levels_sync_bytes(const bhcp_space_plan* sp, int64_t nlev) {

@@ -39,6 +39,22 @@ struct PfModesArgs {
   long long ntiles;
 };
 
+// A batch of independent solves of one g on one space grid with n = 4097
+// (BASELINE config 5: 64 alpha x 2 kinds): pair p has its own
+// shift / threshold / 1/gamma tables (its omega), coefficient scale
+// 1/(divisor_p n), status block and W. Tiles run over pairs x modes, so one
+// launch covers the batch with no per-solve launch tail.
+constexpr int kPfMaxPairs = 32;
+struct PfPairs {
+  int n;                              // pairs in this launch (0: unbatched, use PfModesArgs)
+  long long w_stride;                 // doubles between consecutive pairs' W
+  const double2* shg[kPfMaxPairs];
+  const double* thrg[kPfMaxPairs];
+  const double2* gaminv[kPfMaxPairs];
+  double cscale[kPfMaxPairs];
+  StatusDev* st[kPfMaxPairs];
+};
+
 // 9 warps (at most two of the 17 rows each) and two CTAs per SM: 96
 // registers, some spills, but measured faster (c5: 464 us) than 8 warps with
 // a rotating third row (507 us) or 17 warps, one CTA per SM (490 us)
@@ -80,8 +96,9 @@ __device__ __forceinline__ void pf_warp_stage(const double2* rowp, int lane, con
   __syncwarp();
 }
 
-template <bool SYM>
-__global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArgs a) {
+template <bool SYM, bool BATCH = false>
+__global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArgs a,
+                                                                     const __grid_constant__ PfPairs pp) {
   constexpr int NL = kPfN, T = PfPlan::T;
   extern __shared__ double2 smem[];
   __shared__ double2 s_w[kPfNp], s_bh[kPfNp];
@@ -98,9 +115,36 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
   StatusDev* st = a.st;
   const WLayout& wl = a.wl;
   double sre = 0.0, sim = 0.0;
-  const long long ntiles = SYM ? a.ntiles : a.k_count;
+  const long long ntiles = SYM ? a.ntiles : (BATCH ? a.k_count * pp.n : a.k_count);
+  // batch: the pair of the current tile; residue sums flushed to its status block
+  // whenever the CTA moves on to another pair (tiles are uniform across the CTA)
+  int pair = -1;
+  const double2* shg = a.shg;
+  const double* thrg = a.thrg;
+  const double2* gaminv = a.gaminv;
+  double cscale = a.cscale;
+  long long wofs = 0;
   __syncthreads();
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (long long tile0 = blockIdx.x; tile0 < ntiles; tile0 += gridDim.x) {
+    long long tile = tile0;
+    if (BATCH) {
+      const int pr = (int)(tile0 / a.k_count);
+      tile = tile0 - (long long)pr * a.k_count;
+      if (pr != pair) {
+        if (pair >= 0) {
+          block_sum2(sre, sim, red);
+          if (threadIdx.x == 0) {
+            atomicAdd(&st->sum_re2, sre);
+            atomicAdd(&st->sum_im2, sim);
+          }
+          sre = 0.0; sim = 0.0;
+          __syncthreads();   // red is reused
+        }
+        pair = pr;
+        shg = pp.shg[pr]; thrg = pp.thrg[pr]; gaminv = pp.gaminv[pr]; cscale = pp.cscale[pr];
+        st = pp.st[pr]; wofs = (long long)pr * pp.w_stride;
+      }
+    }
     bool valid, hm = false;
     long long kd, km = 0;
     int k1d = 0, k1m = 0;
@@ -131,8 +175,8 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
     }
     if (!valid) continue;   // uniform across the CTA
     const double mu = mode_mu(a.mu1, a.m, a.dim, kd);
-    const double c = __ldg(a.ghat + kd) * a.cscale;
-    const double c2 = hm ? __ldg(a.ghat + km) * a.cscale : 0.0;
+    const double c = __ldg(a.ghat + kd) * cscale;
+    const double c2 = hm ? __ldg(a.ghat + km) * cscale : 0.0;
     // 1-4. rows, one warp per row (warp-synchronous, no CTA barrier): the
     // generator in prime-factor order (slot 0: j2 = 0; slot 1 + p: j2 = g^p),
     // A = FFT240(a), Y(row, 0) = y0 + A_0 kept aside, slots <- conj(A_k bhat_k),
@@ -144,10 +188,10 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
 #pragma unroll
       for (int sl = lane; sl < kPfLen; sl += 32) {
         const int i = row * kPfLen + sl;
-        const double2 s = __ldg(a.shg + i);
+        const double2 s = __ldg(shg + i);
         const double dr = s.x + mu, di = s.y;
         const double den2 = dr * dr + di * di;
-        if (den2 <= __ldg(a.thrg + i)) flag_singular(st, __ldg(a.jg + i));
+        if (den2 <= __ldg(thrg + i)) flag_singular(st, __ldg(a.jg + i));
         const double inv = fast_rcp(den2);
         rowb[sl] = make_double2(dr * inv, -di * inv);
       }
@@ -222,12 +266,12 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
         pm = pd;
         step = (long long)T * wl.w_ld;
       }
-      double* __restrict__ wd = wl.sl_base[sl] + pd;
-      double* __restrict__ wmr = wl.sl_base[sl] + pm;
+      double* __restrict__ wd = wl.sl_base[sl] + wofs + pd;
+      double* __restrict__ wmr = wl.sl_base[sl] + wofs + pm;
 #pragma unroll 4
       for (int t = t0 + threadIdx.x; t < t1; t += T, wd += step, wmr += step) {
         const double2 X = buf[(t % kPfRows) * kPfLen + (t % kPfLen)];
-        const double2 g = __ldg(a.gaminv + t);
+        const double2 g = __ldg(gaminv + t);
         const double zr = X.x * g.x - X.y * g.y;
         const double zi = X.x * g.y + X.y * g.x;
         zr2 = fma(zr, zr, zr2);
@@ -242,9 +286,9 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
     __syncthreads();   // buf is rewritten by the next mode
   }
   block_sum2(sre, sim, red);
-  if (threadIdx.x == 0) {
-    atomicAdd(&a.st->sum_re2, sre);
-    atomicAdd(&a.st->sum_im2, sim);
+  if (threadIdx.x == 0 && (!BATCH || pair >= 0)) {
+    atomicAdd(&st->sum_re2, sre);
+    atomicAdd(&st->sum_im2, sim);
   }
 }
 

@@ -157,16 +157,18 @@ class PintPlan:
         ws = self.workspace()
         return ctypes.c_void_p(ws.data_ptr())
 
-    def read_status(self, tol: float = RESIDUE_TOL) -> _lib.Status:
+    def read_status(self, tol: float = RESIDUE_TOL, status: Optional[ctypes.c_void_p] = None) -> _lib.Status:
         """The status block of the last solve (synchronises): code, first singular
-        column, ||Im Y|| (residue) and ||Y|| (norm) of circulant.py:182-185."""
+        column, ||Im Y|| (residue) and ||Y|| (norm) of circulant.py:182-185.
+        ``status``: another status block written for this plan (a batched solve)."""
         st = _lib.Status()
-        _lib.check(_lib.lib().bhcp_read_status(self.status_ptr(), tol, ctypes.byref(st), plans.stream_handle()),
+        ptr = status if status is not None else self.status_ptr()
+        _lib.check(_lib.lib().bhcp_read_status(ptr, tol, ctypes.byref(st), plans.stream_handle()),
                    "bhcp_read_status")
         return st
 
-    def check_status(self, tol: float = RESIDUE_TOL) -> _lib.Status:
-        st = self.read_status(tol)
+    def check_status(self, tol: float = RESIDUE_TOL, status: Optional[ctypes.c_void_p] = None) -> _lib.Status:
+        st = self.read_status(tol, status)
         if st.code == _lib.BHCP_ERR_SINGULAR_SHIFT:
             j = int(st.bad_column)
             raise SingularShiftError(f"column {j}: {singular_message(complex(self.shifts[j]))}")
@@ -187,6 +189,51 @@ class PintPlan:
                                                plans.ptr(ws), nb, plans.stream_handle()),
                    "bhcp_pint_solve_unfused")
         return y, ws
+
+
+class PintBatch:
+    """Independent fused solves of one g on one grid and time length, each with
+    its own (kind, alpha) plan (BASELINE config 5: the alpha sweep), enqueued as
+    one batched call (``bhcp_pint_solve_batch``): one DST of g, pass A of up to
+    32 solves per launch, one level phase for all. No host synchronisation; the
+    status blocks are read with ``check(i)``. Each trajectory is bitwise the one
+    ``PintPlan.solve_device`` gives for that plan."""
+
+    def __init__(self, plans_: "list[PintPlan]", ws: Optional[torch.Tensor] = None):
+        if not plans_:
+            raise ValueError("empty batch")
+        n = plans_[0].n
+        if any(p.n != n or p.grid != plans_[0].grid for p in plans_):
+            raise ValueError("a batch needs one grid and one number of levels")
+        self.plans = list(plans_)
+        self.nb = len(self.plans)
+        lib = _lib.lib()
+        self.sp = self.plans[0].sp
+        self.ws_bytes = int(lib.bhcp_pint_batch_workspace_bytes(self.sp.handle, self.plans[0].tp.handle, self.nb))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        if ws is not None and (ws.dtype != torch.uint8 or ws.numel() < self.ws_bytes):
+            raise ValueError(f"workspace of {ws.numel()} bytes, this batch needs {self.ws_bytes}")
+        # a shared workspace is reused in stream order (the caller serialises the batches)
+        self.ws = ws if ws is not None else torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.sbytes = int(lib.bhcp_status_bytes())
+        self.status = torch.empty(self.nb * self.sbytes, dtype=torch.uint8, device=dev)
+        self._tps = (ctypes.c_void_p * self.nb)(*[p.tp.handle.value for p in self.plans])
+
+    def solve_device(self, g: torch.Tensor, divisors, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Enqueue every solve; returns y (nb, n, n_space)."""
+        lib = _lib.lib()
+        nx = self.plans[0].grid.n_interior
+        y = out if out is not None else torch.empty((self.nb, self.plans[0].n, nx), dtype=torch.float64,
+                                                    device=g.device)
+        div = (ctypes.c_double * self.nb)(*[float(d) for d in divisors])
+        _lib.check(lib.bhcp_pint_solve_batch(self.sp.handle, self._tps, self.nb, plans.ptr(g), div, plans.ptr(y),
+                                             plans.ptr(self.status), plans.ptr(self.ws), self.ws_bytes,
+                                             plans.stream_handle()), "bhcp_pint_solve_batch")
+        return y
+
+    def check(self, i: int, tol: float = RESIDUE_TOL) -> _lib.Status:
+        """Status of solve i (synchronises); raises like ``PintPlan.check_status``."""
+        return self.plans[i].check_status(tol, ctypes.c_void_p(self.status.data_ptr() + i * self.sbytes))
 
 
 _plan_cache: dict = {}

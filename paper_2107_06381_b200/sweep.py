@@ -8,10 +8,11 @@ bench.py:265-271). Multi-GPU is replicas: rank r takes the
 (kind, alpha) pairs i = r, r + P, ... and the 128 scalars are gathered on
 every rank. No collective on the data path.
 
-Per solve on the device: the plan for that (kind, alpha) -- its omega sets
-Gamma and the shifts, so the host tables (diagonalize, pint.py:87) are built
-per pair, while the next pair's tables are built as the current solve runs --
-then the fused solve, then y[0] (one level) back to the host.
+On the device the pairs run batched (``pint.PintBatch``): each (kind, alpha)
+keeps its own plan (its omega sets Gamma and the shifts, the host tables of
+diagonalize, pint.py:87), a chunk of solves is one ``bhcp_pint_solve_batch``
+call (one DST of g, pass A of the whole chunk per launch, one level phase),
+e_h of each solve is reduced on the device, and the host synchronises once.
 """
 
 from __future__ import annotations
@@ -91,44 +92,61 @@ def run_pairs(pairs: Sequence[Tuple[str, float]], solve_one: Callable[[str, floa
 
 
 def alpha_sweep(grid, timegrid, g_delta, z0, kinds: Sequence[str], alphas: Sequence[float],
-                rank: int = 0, world: int = 1, comm=None) -> SweepResult:
-    """The device sweep: one fused solve per (kind, alpha) on this rank's GPU."""
+                rank: int = 0, world: int = 1, comm=None, chunk: int = 16) -> SweepResult:
+    """The device sweep: this rank's (kind, alpha) pairs as batched fused solves
+    (``pint.PintBatch``, ``chunk`` solves per call), e_h of every solve reduced on
+    the device, one host synchronisation at the end."""
     import torch
 
     from . import _lib, methods, pint, plans
-    from .workloads import l2_error
 
     _lib.lib()   # fails loudly without the CUDA library / a GPU
     g_dev = plans.to_device(np.asarray(g_delta, dtype=np.float64), torch.float64)
-    y = torch.empty((timegrid.n_levels, grid.n_interior), dtype=torch.float64, device=g_dev.device)
+    z0_dev = plans.to_device(np.asarray(z0, dtype=np.float64), torch.float64)
     pairs = [(k, float(a)) for k in kinds for a in alphas]
-
-    def build(kind, alpha):
-        system = methods.assemble(methods.MethodKind(kind), alpha, grid, timegrid, g_delta)
-        plan = pint.PintPlan(grid, timegrid.n_levels, timegrid.tau, system.omega)
-        return plan, system.method.condition_divisor(timegrid.tau)
-
     mine = [pairs[i] for i in assign(len(pairs), rank, world)]
-    built = {}
+    t0 = time.perf_counter()
+    local: List[SweepPoint] = []
     if mine:
-        built[mine[0]] = build(*mine[0])
-    ws_shared = [None]
+        nb = min(chunk, len(mine))
+        y = torch.empty((nb, timegrid.n_levels, grid.n_interior), dtype=torch.float64, device=g_dev.device)
+        e_h = torch.empty(len(mine), dtype=torch.float64, device=g_dev.device)
+        scale = float(np.sqrt(grid.h ** grid.dim))   # l2_error (bench.py:154-162)
+        batches, events = [], []
+        ws = None
+        for c0 in range(0, len(mine), nb):
+            c1 = min(c0 + nb, len(mine))
+            # this chunk's plans (host tables of diagonalize, pint.py:87) are built
+            # while the previous chunk runs on the device
+            systems = [methods.assemble(methods.MethodKind(k), a, grid, timegrid, g_delta) for k, a in mine[c0:c1]]
+            b = pint.PintBatch([pint.PintPlan(grid, timegrid.n_levels, timegrid.tau, sy.omega) for sy in systems], ws)
+            ws = b.ws   # one workspace for every chunk (stream order)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            yb = b.solve_device(g_dev, [sy.method.condition_divisor(timegrid.tau) for sy in systems], out=y[: c1 - c0])
+            e1.record()
+            # e_h = sqrt(h^dim) ||y(0) - z0|| of every solve, before y is reused
+            e_h[c0:c1] = torch.linalg.vector_norm(yb[:, 0, :] - z0_dev, dim=1) * scale
+            batches.append((c0, b))
+            events.append((e0, e1, c1 - c0))
+        e_host = e_h.cpu().numpy()   # the one synchronisation
+        for c0, b in batches:
+            for i in range(b.nb):
+                b.check(i)
+        for (c0, b), (e0, e1, cnt) in zip(batches, events):
+            ms = e0.elapsed_time(e1) / cnt
+            for i in range(cnt):
+                k, a = mine[c0 + i]
+                local.append(SweepPoint(k, a, float(e_host[c0 + i]), ms, rank))
+    wall = time.perf_counter() - t0
+    pts = gather(local, world, comm)
+    if world > 1:
+        import torch.distributed as dist
 
-    def solve_one(kind, alpha):
-        plan, div = built.pop((kind, alpha))
-        if ws_shared[0] is None:
-            ws_shared[0] = plan.workspace()
-        plan.use_workspace(ws_shared[0])   # every (kind, alpha) plan has the same workspace size
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        plan.solve_device(g_dev, div, out=y)
-        e1.record()
-        # the next pair's host tables are built while this solve runs
-        j = mine.index((kind, alpha))
-        if j + 1 < len(mine):
-            built[mine[j + 1]] = build(*mine[j + 1])
-        y0 = y[0].cpu().numpy()          # synchronises
-        plan.check_status()
-        return l2_error(y0, z0, grid.h, grid.dim), e0.elapsed_time(e1)
-
-    return run_pairs(pairs, solve_one, rank, world, comm)
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(comm) == "nccl" else "cpu"
+        w = torch.tensor([wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(w, op=dist.ReduceOp.MAX, group=comm)
+        wall = float(w.item())
+    order = {(k, float(a)): j for j, (k, a) in enumerate(pairs)}
+    pts.sort(key=lambda p: order[(p.kind, p.alpha)])
+    return SweepResult(pts, wall)

@@ -100,3 +100,34 @@ def test_device_sweep_matches_oracle_curve(config, idx):
         e_ref = workloads.l2_error(ref[0], w.z0, grid.h, w.dim)
         assert abs(p.e_h - e_ref) <= 5e-4 * e_ref, (p.kind, p.alpha, p.e_h, e_ref)
         assert p.ms > 0.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cells,steps,nalpha", [(64, 4096, 18), (48, 64, 3)])
+def test_batched_solves_bitwise_equal_single(cells, steps, nalpha):
+    """bhcp_pint_solve_batch (pint.PintBatch): every trajectory bitwise the single
+    fused solve of its (kind, alpha); residue norms per solve. n = 4097 runs the
+    batched prime-factor pass A (36 solves: two launches of <= 32 pairs), n = 65
+    the per-pair fallback."""
+    import torch
+
+    import paper_2107_06381_b200 as B
+    from paper_2107_06381_b200 import pint
+
+    w = workloads.make_small(1, cells, steps, seed=4, length=np.pi, horizon=1.0, delta=1e-3)
+    grid = B.build_grid(1, w.length, w.num_cells)
+    tg = B.TimeGrid(w.horizon, w.num_steps)
+    alphas = list(np.logspace(-6, -1, nalpha))
+    systems = [B.assemble(B.MethodKind(k), a, grid, tg, w.g_delta) for k in ("pint-qbvm", "pint-mqbvm") for a in alphas]
+    plans_ = [pint.PintPlan(grid, tg.n_levels, tg.tau, s.omega) for s in systems]
+    divs = [s.method.condition_divisor(tg.tau) for s in systems]
+    g = torch.from_numpy(w.g_delta).cuda()
+    batch = pint.PintBatch(plans_)
+    yb = batch.solve_device(g, divs).cpu().numpy()
+    for i, (p, d) in enumerate(zip(plans_, divs)):
+        y1 = p.solve_device(g, d).cpu().numpy()
+        st1 = p.check_status()
+        stb = batch.check(i)
+        assert np.array_equal(yb[i], y1), f"solve {i}"
+        assert abs(stb.residue - st1.residue) <= 1e-9 * st1.residue + 1e-300
+        assert abs(stb.norm - st1.norm) <= 1e-12 * st1.norm
