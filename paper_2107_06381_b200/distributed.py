@@ -205,9 +205,16 @@ def make_transport(kind: str, layout: SlabLayout, rank: int, device):
         return None
     try:
         return PeerTransport(layout, rank, device)
-    except Exception:
+    except Exception as e:
         if kind == "peer":
             raise
+        # not silent: the sharded bench line reports the transport it used, and the
+        # reason the peer (symmetric-memory) path was not available is logged here
+        import warnings
+
+        warnings.warn(f"rank {rank}: peer transport unavailable ({type(e).__name__}: {e}); "
+                      "falling back to the NCCL all-to-all (set BHCP_TRANSPORT=nccl to select it explicitly)",
+                      RuntimeWarning, stacklevel=2)
         return None
 
 
@@ -413,12 +420,21 @@ def solve_pint_sharded(system, comm=None, transport: str = "auto"):
 
 # ---------------------------------------------------------------- bench (N > 1)
 
+# NVLink 5 per GPU and direction: 770 GB/s measured peer copy on this pool's
+# B200s, 900 GB/s nominal (/opt/skills/guides/B200_PROFILING.md, NVLink
+# references); the fraction is reported against the measured figure
+NVLINK_MEASURED_GBPS = 770.0
+NVLINK_NOMINAL_GBPS = 900.0
+
+
 def _nvlink_stats(nbytes: float, ms: float, transport: str) -> dict:
     """Bytes each rank sends to its peers and the rate over the phase that
     carries them (the all-to-all, or pass A itself for peer stores)."""
     gbps = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
     return {"bytes_per_rank": nbytes, "carried_by": "pass A stores" if transport == "peer" else "all_to_all",
-            "achieved_GBps": gbps, "peak_GBps": 770.0, "frac": gbps / 770.0}
+            "transport": transport, "achieved_GBps": gbps, "peak_GBps": NVLINK_MEASURED_GBPS,
+            "peak_source": "measured peer copy per direction (B200_PROFILING.md); nominal 900",
+            "frac": gbps / NVLINK_MEASURED_GBPS, "frac_nominal": gbps / NVLINK_NOMINAL_GBPS}
 
 
 def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric, unit, config_of):
@@ -503,6 +519,22 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     alg = [8.0 * local_dof_a, 0.0, 32.0 * local_dof_b]
     dom = 0 if ph[0] >= ph[2] else 2
     achieved = alg[dom] / (ph[dom] * 1e-3) / 1e9
+    modes_kernel = {257: "k_modes_rader", 513: "k_modes_fast", 1025: "k_modes_gt", 4097: "k_modes_pf"}.get(
+        tg.n_levels, "k_modes")
+    level_kernels = {256: "k_dst_wax + k_dst_blk3", 512: "k_dst_wax2 + k_dst_blk3",
+                     1024: "k_dst_blk4 + k_dst_cols3"}.get(grid.num_cells, "level passes")
+    # the same per-kernel breakdown as the N = 1 line (rank 0's phases, algorithmic bytes of its slab)
+    kernels = [
+        {"kernel": f"{modes_kernel} (pass A, this rank's modes, W stores" +
+                   (" into the owners over NVLink)" if peer is not None else ")"),
+         "ms": ph[0], "alg_bytes": alg[0], "achieved_GBps": alg[0] / (ph[0] * 1e-3) / 1e9 if ph[0] > 0 else 0.0},
+        {"kernel": "rank barrier" if peer is not None else "NCCL all_to_all", "ms": ph[1], "alg_bytes": a2a_bytes,
+         "achieved_GBps": a2a_bytes / (ph[1] * 1e-3) / 1e9 if ph[1] > 0 else 0.0},
+        {"kernel": f"{level_kernels} (level passes of this rank's level slab)", "ms": ph[2], "alg_bytes": alg[2],
+         "achieved_GBps": alg[2] / (ph[2] * 1e-3) / 1e9 if ph[2] > 0 else 0.0},
+    ]
+    for k in kernels:
+        k["hbm_frac"] = k["achieved_GBps"] / hbm
     launches = 1 + (grid.dim + 1) + 1 + grid.dim  # status reset, ghat (dim passes + scale), modes, level passes
     if rank != 0:
         return None
@@ -516,11 +548,12 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
                         f"level-slab owners over NVLink peer memory -> level slabs, P={world}")
                        if peer is not None else
                        f"mode slabs -> NCCL all-to-all -> level slabs, P={world}",
-        "roofline": {"bound": "hbm", "kernel": ["pass A (k_modes_fast)", "", "pass B (level passes)"][dom],
+        "roofline": {"bound": "hbm", "kernel": kernels[dom]["kernel"],
                      "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": kind},
         "phases_ms_rank0": {"pass_a_modes": ph[0], ("rank_barrier" if peer is not None else "all_to_all"): ph[1],
                             "pass_b_levels": ph[2]},
+        "kernels": kernels,
         "nvlink": _nvlink_stats(a2a_bytes, ph[0] if peer is not None else ph[1], transport),
         "e2e": {"value": w.dof / (e2e_ms * 1e-3), "unit": unit, "h2d_bytes_per_step": 8 * w.n_space,
                 "d2h_bytes_per_step": 8 * (c1 - c0) * w.n_space, "ms_per_step": e2e_ms},

@@ -127,3 +127,64 @@ def test_duck_typed_reference_system(kind):
     assert res.residual_norm() <= 1e-9
     orc = B.solve_spectral_oracle(kind, 1e-3, grid, tg, data)
     assert np.linalg.norm(orc.initial_state - ref[0]) / np.linalg.norm(ref[0]) <= 1e-12
+
+
+# ------------------------------------------------- the reference driver itself on the B200 (f4)
+
+def _reference_package():
+    """The reference package as test data: the read-only source tree where it
+    exists (this container), else the copy pip-installed into baseline/_ref
+    (git-ignored; it travels to the GPU box with the snapshot). Never imported by
+    the product package."""
+    from pathlib import Path
+
+    for root in (REF_SRC, str(Path(__file__).resolve().parents[1] / "baseline" / "_ref")):
+        if os.path.isdir(os.path.join(root, "bhcp")):
+            return root
+    return None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("example,meshes", [(1, ((32, 32), (64, 64))), (2, ((16, 16),))])
+def test_reference_driver_rows_on_device(example, meshes, tmp_path):
+    """bhcp.bench.run_experiment (bench.py:172-272) with its solve rebound to the
+    device by integration.install, against the same experiment on the reference's
+    own numpy path: every row ok, CSV error_l2 equal to 3 significant digits (the
+    north-star bar for the reconstruction error), residual of the device row at
+    the reference's level. The reference's own fixed-alpha tripwire row (M, N) =
+    (16, 8) at alpha 1e-12 must fail on both paths (ImaginaryResidueError,
+    circulant.py:182-189)."""
+    root = _reference_package()
+    if root is None:
+        pytest.skip("reference package not available (neither /root/reference nor baseline/_ref)")
+    sys.path.insert(0, root)
+    try:
+        import bhcp
+        from bhcp.bench import ExperimentConfig, emit_csv, parse_csv, run_experiment
+        from bhcp.methods import MethodKind
+
+        from paper_2107_06381_b200 import integration
+
+        kinds = (MethodKind.PINT_QBVM, MethodKind.PINT_MQBVM)
+        cfg = ExperimentConfig(example=example, methods=kinds, solver="pint", meshes=meshes, eps_values=(1e-2, 1e-3),
+                               seed=11)
+        cpu = run_experiment(cfg)
+        with integration.install(bhcp):
+            dev = run_experiment(cfg)
+        emit_csv(dev, str(tmp_path / "dev.csv"))
+        emit_csv(cpu, str(tmp_path / "cpu.csv"))
+        rd, rc = parse_csv(str(tmp_path / "dev.csv")), parse_csv(str(tmp_path / "cpu.csv"))
+        assert len(rd) == len(rc) == len(kinds) * len(meshes) * 2
+        for a, b in zip(rd, rc):
+            assert a.status == b.status == "ok", (a.status, b.status)
+            assert float(f"{a.error_l2:.3g}") == float(f"{b.error_l2:.3g}"), (a.error_l2, b.error_l2)
+            assert a.residual <= max(10 * b.residual, 1e-9)
+        trip = ExperimentConfig(example=1, methods=kinds, solver="pint", meshes=((16, 8),), eps_values=(1e-2,),
+                                seed=3, alpha_rule="fixed:1e-12")
+        with integration.install(bhcp):
+            dev_trip = run_experiment(trip)
+        assert [r.status for r in run_experiment(trip)] == [r.status for r in dev_trip]
+    finally:
+        sys.path.remove(root)
+        for k in [k for k in sys.modules if k == "bhcp" or k.startswith("bhcp.")]:
+            del sys.modules[k]
