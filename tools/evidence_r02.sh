@@ -20,9 +20,15 @@ python tools/run_configs.py --cpu > $out/configs.json 2> $out/configs.err; echo 
 python bench.py --quick --steps 3 --warmup 3 > $out/bench_short.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $out/launches_c3.csv \
       python bench.py --quick --steps 3 --warmup 3 > $out/ncu_launch.log 2>&1; echo "ncu launches rc=$?" | tee -a $out/rc.txt
+# --set full captures, summarised on the box (the reports themselves exceed what
+# gpurun copies back): raw metrics CSV, summary table, DRAM traffic, hot source lines
 for cfg in c3 c2 c4 c5 c1; do
   python tools/profile_step.py $cfg 1 > $out/profile_step_$cfg.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -c 14 \
-        -o $out/${cfg}_full -f python tools/profile_step.py $cfg 1 > $out/ncu_full_$cfg.log 2>&1
+        -o /tmp/${cfg}_full -f python tools/profile_step.py $cfg 1 > $out/ncu_full_$cfg.log 2>&1
   echo "ncu full $cfg rc=$?" | tee -a $out/rc.txt
+  lf=-; [ "$cfg" = c3 ] && lf=$out/launches_c3.csv
+  python tools/ncu_summary.py /tmp/${cfg}_full.ncu-rep $lf $out/r02_$cfg > /dev/null 2>&1
+  python tools/src_hot.py /tmp/${cfg}_full.ncu-rep 40 > $out/r02_${cfg}_src_hot.txt 2>&1
+  rm -f /tmp/${cfg}_full.ncu-rep
 done

@@ -15,7 +15,7 @@ import subprocess
 import sys
 from pathlib import Path
 
-rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]
+rep, launches, prefix = sys.argv[1], sys.argv[2], sys.argv[3]   # launches: a CSV or "-" (none)
 extra = sys.argv[4:]  # optional further launch lists (e.g. the whole bench command), summarised too
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -48,23 +48,26 @@ with open(f"{prefix}_ncu_full.csv", "w", newline="") as f:
     w = csv.DictWriter(f, fieldnames=list(out_rows[0].keys()))
     w.writeheader()
     w.writerows(out_rows)
-shutil.copy(launches, f"{prefix}_launches.csv")
-# launch list shares
-lrows = list(csv.reader(open(launches)))
-h = next(i for i, r in enumerate(lrows) if "Kernel Name" in r)
-lh = lrows[h]
-ki, vi = lh.index("Kernel Name"), lh.index("Metric Value")
-agg = {}
-for r in lrows[h + 1:]:
-    if len(r) <= vi:
-        continue
-    name = r[ki].split("(")[0].replace("void ", "")
-    agg.setdefault(name, []).append(float(r[vi].replace(",", "")))
-tot = sum(sum(v) for v in agg.values())
-lines = [f"# ncu summary ({Path(prefix).name})", "", "## Launch list (gpu__time_duration.sum, cold-cache, serialised)", "",
-         "| kernel | launches | total us | share |", "|---|---|---|---|"]
-for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-    lines.append(f"| {name} | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/tot*100:.1f}% |")
+lines = [f"# ncu summary ({Path(prefix).name})"]
+ki = vi = None
+if launches != "-":
+    shutil.copy(launches, f"{prefix}_launches.csv")
+    # launch list shares
+    lrows = list(csv.reader(open(launches)))
+    h = next(i for i, r in enumerate(lrows) if "Kernel Name" in r)
+    lh = lrows[h]
+    ki, vi = lh.index("Kernel Name"), lh.index("Metric Value")
+    agg = {}
+    for r in lrows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        agg.setdefault(name, []).append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in agg.values())
+    lines += ["", "## Launch list (gpu__time_duration.sum, cold-cache, serialised)", "",
+              "| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for name, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| {name} | {len(v)} | {sum(v)/1e3:.1f} | {sum(v)/tot*100:.1f}% |")
 for ex in extra:
     shutil.copy(ex, f"{prefix}_{Path(ex).stem}.csv")
     er = list(csv.reader(open(ex)))
@@ -92,6 +95,8 @@ for d in out_rows:
                  f"{d.get('launch__registers_per_thread','')} |")
 Path(f"{prefix}_summary.md").write_text("\n".join(lines) + "\n")
 cfg = next((p for p in Path(prefix).name.split("_") if re.fullmatch(r"c[1-5]", p)), "c2")
-tf = Path(f"profiles/ncu_traffic_{cfg}.json")
-tf.write_text(json.dumps({k: v[1] for k, v in traffic.items()}, indent=1) + "\n")
+tj = json.dumps({k: v[1] for k, v in traffic.items()}, indent=1) + "\n"
+Path(f"{prefix}_traffic.json").write_text(tj)
+if Path("profiles").is_dir():
+    Path(f"profiles/ncu_traffic_{cfg}.json").write_text(tj)
 print("\n".join(lines))
