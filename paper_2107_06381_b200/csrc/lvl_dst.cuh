@@ -79,7 +79,7 @@ using wax2::at;
 constexpr int kN = 1024;
 constexpr int kNB = 3;        // tile buffers
 constexpr int kCW = 8;        // consumer warps
-constexpr int kSW = 3;        // storer warps
+constexpr int kSW = 1;        // storer warps
 constexpr int kThreads = (kCW + 1 + kSW) * 32;
 constexpr int kTD2 = kN * 4;  // double2 per tile (8 lines x 1024 rows)
 
@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
     // ----------------------------------------------------------------- storers
     const int sw = warp - kCW - 1;
     const unsigned long long pol = evict_first_policy();
-    const int rr = lane >> 3, l = lane & 7;
     for (int it = 0; it < ntiles_cta; ++it) {
       const int b = it % kNB;
       LP_T0(ts0);
@@ -303,35 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
         const int lev = tk.idx / a.nct, ct = tk.idx % a.nct, c0 = ct * 8;
         const int t = tk.g * 8 + lev;
         const long long R0 = (long long)t * m;
-        const bool lv = c0 + l < a.m;
-        double* dst = a.y + R0 * m + (lv ? c0 + l : 0);
-        if (t < a.nlev - 1 && ct < a.nct - 1) {
-          // plane pe holds the rows e = 2 j + pe; the plane whose rows are even in y
-          // (a 16-byte aligned 64 B chunk) leaves by two TMA boxes of the row-pair
-          // view (the second one 255 rows if it is plane 1: row e = 1023 is the
-          // DST's zero row); the other plane, whose chunks start 8 bytes off, by
-          // 8-byte stores of both storer warps
+        if (t < a.nlev - 1 && ct < a.nct - 1 && sw == 0 && lane == 0) {
+          // the plane whose rows are even in y (a 16-byte aligned 64 B chunk) leaves
+          // by two TMA boxes of the row-pair view (the second one 255 rows if it is
+          // plane 1: row e = 1023 is the DST's zero row); the consumers stored the
+          // other plane
           const int pe = (int)(R0 & 1);   // plane with (R0 + pe) even
-          if (sw == 0 && lane == 0) {
-            const int P0 = (int)((R0 + pe) >> 1);
-            tma_store2_hint(&ty256, c0, P0, T + (pe * 512) * 4, pol);
-            tma_store2_hint(pe ? &ty255 : &ty256, c0, P0 + 256, T + (pe * 512 + 256) * 4, pol);
-            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-          }
-          const int po = pe ^ 1;
-          for (int j = 4 * sw + rr; j < 512; j += 4 * kSW) {
-            const int e = 2 * j + po;
-            const double v = reinterpret_cast<const double*>(at_par(const_cast<double2*>(T), e, l >> 1))[l & 1];
-            if (lv && e < a.m) st_hint(dst + (long long)e * m, v, pol);
-          }
-          if (sw == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
-        } else {
-          // the last column tile (column 1023 is not in y) and the last level (its
-          // final row has no pair partner in the view): 8-byte stores
-          for (int e = 4 * sw + rr; e < kN; e += 4 * kSW) {
-            const double v = reinterpret_cast<const double*>(at_par(const_cast<double2*>(T), e, l >> 1))[l & 1];
-            if (lv && e < a.m) st_hint(dst + (long long)e * m, v, pol);
-          }
+          const int P0 = (int)((R0 + pe) >> 1);
+          tma_store2_hint(&ty256, c0, P0, T + (pe * 512) * 4, pol);
+          tma_store2_hint(pe ? &ty255 : &ty256, c0, P0 + 256, T + (pe * 512 + 256) * 4, pol);
+          asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         }
         if ((ct & 1) && sw == kSW - 1) {
           // both column tiles of this 128-byte Z column pair are loaded (same CTA, in
@@ -401,6 +382,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
     } else {
       ParitySink sink{T, q, K.j1, K.j2};
       wax2::warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+      // all four line pairs are in the tile: the consumers store the rows TMA cannot
+      // (chunks 8 bytes off 16-byte alignment; every row for the last column tile
+      // and the last level) with 8-byte stores, 8 lanes per row
+      asm volatile("bar.sync 5, %0;\n" ::"r"(kCW * 32) : "memory");
+      const int lev = tk.idx / a.nct, c0 = (tk.idx % a.nct) * 8;
+      const int t = tk.g * 8 + lev;
+      const long long R0 = (long long)t * m;
+      const int l = lane & 7, rr = 4 * warp + (lane >> 3);   // 32 rows per round over the 8 warps
+      const bool lv = c0 + l < a.m;
+      double* dst = a.y + R0 * m + (lv ? c0 + l : 0);
+      if (t < a.nlev - 1 && tk.idx % a.nct < a.nct - 1) {
+        const int po = (int)(R0 & 1) ^ 1;   // the plane whose y rows start 8 bytes off
+#pragma unroll 4
+        for (int j = rr; j < 512; j += 32) {
+          const int e = 2 * j + po;
+          const double v = reinterpret_cast<const double*>(at_par(T, e, l >> 1))[l & 1];
+          if (e < a.m) dst[(long long)e * m] = v;
+        }
+      } else {
+        for (int e = rr; e < a.m; e += 32) {
+          const double v = reinterpret_cast<const double*>(at_par(T, e, l >> 1))[l & 1];
+          if (lv) dst[(long long)e * m] = v;
+        }
+      }
     }
 #ifdef LVL4_PROF
     if (warp == 0 && lane == 0) LP_ADD(tk.kind == 0 ? 8 : 9, tc1);
