@@ -363,7 +363,11 @@ def test_full_size_solve_vs_device_oracle(name):
     y = B.solve_pint(system).trajectory_device
     P._plan_cache.clear()
     torch.cuda.empty_cache()
-    levels = np.array([0, w.num_steps // 3, w.num_steps])
+    # level 0, both sides of the first level-tile boundaries (8-level W tiles; the
+    # level-group kernel's group and Z-slot boundaries at 8 and 16), the middle, and
+    # the partial last level tile (n = 1025: levels 1024 = 128 * 8 alone; 257: 256)
+    N = w.num_steps
+    levels = np.array(sorted({0, 1, 7, 8, 15, 16, 17, N // 3, N - 9, N - 8, N - 1, N}))
     ref_host = O.spectral_oracle(kind.value, w.alphas[0], w.dim, w.length, w.num_cells, w.horizon, w.num_steps,
                                  w.g_delta, levels=levels)
     tol = O.parity_tolerance(tg.n_levels, system.omega)
