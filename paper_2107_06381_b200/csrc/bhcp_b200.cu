@@ -789,8 +789,7 @@ struct bhcp_time_plan {
   int* gt_idx;           //           stage-C lane map | row slots | powers of g
   std::vector<double2> shifts_h;   // host copy of the shifts (may_be_singular)
   double2* pf;           // n = 4097: w240 | bhat240 | shifts in prime-factor order (4097)
-  double* pf_thr;        //           singular thresholds, prime-factor order (4097)
-  int* pf_idx;           //           tq241 (240) | time index j per (row, slot) (4097)
+  int* pf_idx;           //           tq241 (240): g^-q mod 241
 };
 
 namespace {
@@ -1286,7 +1285,7 @@ int pf_modes(const bhcp_space_plan* sp, const bhcp_time_plan* tp, const double* 
              const SymRange& sr = SymRange()) {
   using namespace fastk;
   PfModesArgs a{};
-  a.shg = tp->pf + 2 * kPfNp; a.thrg = tp->pf_thr; a.jg = tp->pf_idx + kPfNp; a.gaminv = tp->tables + tp->n;
+  a.shg = tp->pf + 2 * kPfNp; a.gaminv = tp->tables + tp->n;
   a.mu1 = sp->mu1_dev; a.ghat = ghat; a.cscale = cscale; a.k_begin = k_begin; a.k_count = k_end - k_begin;
   a.m = sp->m; a.dim = sp->dim; a.st = st; a.tab = tp->pf; a.tq = tp->pf_idx; a.wl = wl;
   const size_t sm = pf_smem();
@@ -1320,7 +1319,7 @@ int pf_modes_batch(const bhcp_space_plan* sp, const bhcp_time_plan* const* tps, 
   for (int p0 = 0; p0 < nb; p0 += kPfMaxPairs) {
     const int np = std::min(kPfMaxPairs, nb - p0);
     PfModesArgs a{};
-    a.shg = tp->pf + 2 * kPfNp; a.thrg = tp->pf_thr; a.jg = tp->pf_idx + kPfNp; a.gaminv = tp->tables + tp->n;
+    a.shg = tp->pf + 2 * kPfNp; a.gaminv = tp->tables + tp->n;
     a.mu1 = sp->mu1_dev; a.ghat = ghat; a.cscale = cscales[p0]; a.k_begin = 0; a.k_count = sp->nx;
     a.m = sp->m; a.dim = sp->dim; a.st = sts + p0; a.tab = tp->pf; a.tq = tp->pf_idx;
     a.wl = wl;
@@ -1330,7 +1329,7 @@ int pf_modes_batch(const bhcp_space_plan* sp, const bhcp_time_plan* const* tps, 
     pp.w_stride = w_stride;
     for (int i = 0; i < np; ++i) {
       const bhcp_time_plan* t = tps[p0 + i];
-      pp.shg[i] = t->pf + 2 * kPfNp; pp.thrg[i] = t->pf_thr; pp.gaminv[i] = t->tables + t->n;
+      pp.shg[i] = t->pf + 2 * kPfNp; pp.gaminv[i] = t->tables + t->n;
       pp.cscale[i] = cscales[p0 + i]; pp.st[i] = sts + p0 + i;
     }
     const size_t sm = pf_smem();
@@ -2034,32 +2033,25 @@ int bhcp_time_plan_create(int device, int n_levels, const double* gamma_host, co
   tp->gt = nullptr;
   tp->gt_idx = nullptr;
   tp->pf = nullptr;
-  tp->pf_thr = nullptr;
   tp->pf_idx = nullptr;
   if (n_levels == 4097) {
     std::vector<double2> pc;
     std::vector<int> tq, perm;
     if (!build_pf_tables(&pc, &tq, &perm, &err)) { bhcp_time_plan_destroy(tp); return fail(BHCP_ERR_INVALID, err); }
-    std::vector<double> thr(4097);
-    std::vector<int> idx(tq);
-    idx.resize(240 + 4097);
+    // shifts in prime-factor input order (row, slot); the kernel derives the
+    // singular thresholds and, when one fires, the time index from them and tq
     for (int i = 0; i < 4097; ++i) {
       const int row = i / 241, slot = i - row * 241;
       const int j2 = slot ? perm[slot - 1] : 0;
       const int j = (241 * row + 17 * j2) % 4097;
-      const double sr = shifts_host[2 * j], si = shifts_host[2 * j + 1];
-      pc.push_back(make_double2(sr, si));
-      thr[i] = 1e-28 * (sr * sr + si * si);
-      idx[240 + i] = j;
+      pc.push_back(make_double2(shifts_host[2 * j], shifts_host[2 * j + 1]));
     }
     if (cudaMalloc(&tp->pf, sizeof(double2) * pc.size()) != cudaSuccess ||
-        cudaMalloc(&tp->pf_thr, sizeof(double) * thr.size()) != cudaSuccess ||
-        cudaMalloc(&tp->pf_idx, sizeof(int) * idx.size()) != cudaSuccess) {
+        cudaMalloc(&tp->pf_idx, sizeof(int) * tq.size()) != cudaSuccess) {
       bhcp_time_plan_destroy(tp); return cuda_fail("cudaMalloc pf tables");
     }
     cudaMemcpy(tp->pf, pc.data(), sizeof(double2) * pc.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(tp->pf_thr, thr.data(), sizeof(double) * thr.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(tp->pf_idx, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(tp->pf_idx, tq.data(), sizeof(int) * tq.size(), cudaMemcpyHostToDevice);
   }
   tp->shifts_h.resize(n_levels);
   for (int j = 0; j < n_levels; ++j) tp->shifts_h[j] = make_double2(shifts_host[2 * j], shifts_host[2 * j + 1]);
@@ -2108,7 +2100,6 @@ void bhcp_time_plan_destroy(bhcp_time_plan* tp) {
   if (tp->gt) cudaFree(tp->gt);
   if (tp->gt_idx) cudaFree(tp->gt_idx);
   if (tp->pf) cudaFree(tp->pf);
-  if (tp->pf_thr) cudaFree(tp->pf_thr);
   if (tp->pf_idx) cudaFree(tp->pf_idx);
   delete tp;
 }

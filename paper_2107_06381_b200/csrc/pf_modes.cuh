@@ -23,8 +23,6 @@ constexpr int kPfRows = 17, kPfLen = 241, kPfN = kPfRows * kPfLen, kPfNp = 240;
 
 struct PfModesArgs {
   const double2* shg;   // shifts in prime-factor input order (row j1, slot)
-  const double* thrg;   // singular thresholds 1e-28 |s|^2, same order
-  const int* jg;        // time index j of each (row, slot)
   const double2* gaminv;
   const double* mu1;
   const double* ghat;
@@ -41,7 +39,7 @@ struct PfModesArgs {
 
 // A batch of independent solves of one g on one space grid with n = 4097
 // (BASELINE config 5: 64 alpha x 2 kinds): pair p has its own
-// shift / threshold / 1/gamma tables (its omega), coefficient scale
+// shift and 1/gamma tables (its omega), coefficient scale
 // 1/(divisor_p n), status block and W. Tiles run over pairs x modes, so one
 // launch covers the batch with no per-solve launch tail.
 constexpr int kPfMaxPairs = 32;
@@ -49,7 +47,6 @@ struct PfPairs {
   int n;                              // pairs in this launch (0: unbatched, use PfModesArgs)
   long long w_stride;                 // doubles between consecutive pairs' W
   const double2* shg[kPfMaxPairs];
-  const double* thrg[kPfMaxPairs];
   const double2* gaminv[kPfMaxPairs];
   double cscale[kPfMaxPairs];
   StatusDev* st[kPfMaxPairs];
@@ -120,7 +117,6 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
   // whenever the CTA moves on to another pair (tiles are uniform across the CTA)
   int pair = -1;
   const double2* shg = a.shg;
-  const double* thrg = a.thrg;
   const double2* gaminv = a.gaminv;
   double cscale = a.cscale;
   long long wofs = 0;
@@ -141,7 +137,7 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
           __syncthreads();   // red is reused
         }
         pair = pr;
-        shg = pp.shg[pr]; thrg = pp.thrg[pr]; gaminv = pp.gaminv[pr]; cscale = pp.cscale[pr];
+        shg = pp.shg[pr]; gaminv = pp.gaminv[pr]; cscale = pp.cscale[pr];
         st = pp.st[pr]; wofs = (long long)pr * pp.w_stride;
       }
     }
@@ -191,7 +187,14 @@ __global__ void __launch_bounds__(PfPlan::T, PfPlan::MINB) k_modes_pf(PfModesArg
         const double2 s = __ldg(shg + i);
         const double dr = s.x + mu, di = s.y;
         const double den2 = dr * dr + di * di;
-        if (den2 <= __ldg(thrg + i)) flag_singular(st, __ldg(a.jg + i));
+        // singular-shift threshold 1e-28 |s_j|^2 (space.py:237-240), rounded exactly as
+        // the host forms it (no contraction), and the time index j of (row, slot)
+        // only when it fires: j2 = g^(slot - 1) = tq[(241 - slot) % 240] (tq = g^-q)
+        const double thr = __dmul_rn(1e-28, __dadd_rn(__dmul_rn(s.x, s.x), __dmul_rn(s.y, s.y)));
+        if (den2 <= thr) {
+          const int j2 = sl ? (int)s_tq[(241 - sl) % kPfNp] : 0;
+          flag_singular(st, (kPfLen * row + kPfRows * j2) % kPfN);
+        }
         const double inv = fast_rcp(den2);
         rowb[sl] = make_double2(dr * inv, -di * inv);
       }
