@@ -254,8 +254,8 @@ int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev,
  * tile is still L2-resident; 16 instead of 32 B/DOF of HBM traffic). sync_dev:
  * a device buffer of at least that many bytes, used as per-level-tile
  * counters (the call zeroes it on the stream); it must not be shared by
- * concurrent calls. Where the sync size is 0 this is bhcp_pint_levels (the
- * input may be overwritten) and sync_dev is ignored. Reference: the per-level
+ * concurrent calls. Where the sync size is 0 this is bhcp_pint_levels (any
+ * dim; the input may be overwritten) and sync_dev is ignored. Reference: the per-level
  * DSTs of pint.py:94-96 / space.py:163-177. */
 /* bhcp_pint_solve_batch: nb independent fused solves of one g on one space
  * plan (BASELINE config 5: the alpha sweep, 64 alpha x 2 kinds), each with its

@@ -2402,7 +2402,6 @@ size_t bhcp_pint_levels_sync_bytes(const bhcp_space_plan* sp, int64_t nlev) {
 int bhcp_pint_levels_fused(const bhcp_space_plan* sp, const double* in_dev, double* out_dev, int64_t nlev,
                            void* sync_dev, void* stream) {
   if (!sp || !in_dev || !out_dev || nlev < 0) return fail(BHCP_ERR_INVALID, "bad argument");
-  if (sp->dim < 2) return fail(BHCP_ERR_INVALID, "blocked level input needs dim >= 2");
   DeviceGuard g(sp->device);
   cudaStream_t s = as_stream(stream);
   if (lvl4_ok(sp)) {

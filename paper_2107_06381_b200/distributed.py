@@ -282,6 +282,7 @@ class DeviceOps:
         self._tables = {}
         self._W = None
         self._y = None
+        self._sync = None   # level-group kernel scratch (bhcp_pint_levels_sync_bytes)
 
     def prepare(self):
         """status reset + ghat = DST(g) / (divisor * n) (replicated on every rank)."""
@@ -359,10 +360,20 @@ class DeviceOps:
         if self._y is None or self._y.shape != (L, self.nx):
             self._y = torch.empty((L, self.nx), dtype=torch.float64, device=self.g.device)
         if L > 0:
-            # tables() verified koff is the uniform stride: pass NULL so the TMA passes run
-            self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), None,
-                                                              p.ptr(self._y), L, p.stream_handle()),
-                            "levels_blocked")
+            # tables() verified koff is the uniform stride: the receive buffer is a
+            # single-slab W of this rank's L levels, so the level-group kernel
+            # (k_dst_lvl4, 2D m + 1 = 1024) or the TMA passes (koff NULL) run on it
+            nsync = int(self.lib.bhcp_pint_levels_sync_bytes(self.plan.sp.handle, L))
+            if nsync:
+                if self._sync is None or self._sync.numel() < nsync:
+                    self._sync = torch.empty(nsync, dtype=torch.uint8, device=self.g.device)
+                self._lib.check(self.lib.bhcp_pint_levels_fused(self.plan.sp.handle, p.ptr(recv), p.ptr(self._y), L,
+                                                                p.ptr(self._sync), p.stream_handle()),
+                                "levels_fused")
+            else:
+                self._lib.check(self.lib.bhcp_pint_levels_blocked(self.plan.sp.handle, p.ptr(recv), None,
+                                                                  p.ptr(self._y), L, p.stream_handle()),
+                                "levels_blocked")
         return self._y
 
     def local_status(self):
@@ -522,7 +533,7 @@ def bench_sharded(args, w, system, rank, world, dev, ClockSampler, peaks, metric
     modes_kernel = {257: "k_modes_rader", 513: "k_modes_fast", 1025: "k_modes_gt", 4097: "k_modes_pf"}.get(
         tg.n_levels, "k_modes")
     level_kernels = {256: "k_dst_wax + k_dst_blk3", 512: "k_dst_wax2 + k_dst_blk3",
-                     1024: "k_dst_blk4 + k_dst_cols3"}.get(grid.num_cells, "level passes")
+                     1024: "k_dst_lvl4"}.get(grid.num_cells, "level passes")
     # the same per-kernel breakdown as the N = 1 line (rank 0's phases, algorithmic bytes of its slab)
     kernels = [
         {"kernel": f"{modes_kernel} (pass A, this rank's modes, W stores" +

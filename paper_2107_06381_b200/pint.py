@@ -131,7 +131,12 @@ class PintPlan:
                    "bhcp_pint_modes")
         if events:
             events[2].record()
-        _lib.check(lib.bhcp_pint_levels(self.sp.handle, W, plans.ptr(y), self.n, stream), "bhcp_pint_levels")
+        # the level phase exactly as bhcp_pint_solve runs it: the level-group kernel
+        # where the plan has one, its scratch in the workspace right after W
+        nw = nx * 8 * ((self.n + 7) // 8)
+        sync = ctypes.c_void_p(W.value + ((8 * nw + 255) // 256) * 256)
+        _lib.check(lib.bhcp_pint_levels_fused(self.sp.handle, W, plans.ptr(y), self.n, sync, stream),
+                   "bhcp_pint_levels_fused")
         if events:
             events[3].record()
         return y

@@ -241,11 +241,13 @@ def emulate(system, world):
 @pytest.mark.parametrize("dim,cells,steps,world", [(2, 16, 12, 2), (2, 20, 9, 3), (3, 8, 6, 2), (3, 9, 7, 4),
                                                    (2, 12, 256, 2), (3, 7, 256, 3), (2, 10, 1024, 2),
                                                    (2, 20, 512, 3), (2, 6, 4096, 2), (3, 6, 1024, 2),
-                                                   (2, 512, 512, 8)])
+                                                   (2, 512, 512, 8), (2, 1024, 19, 3)])
 def test_emulated_ranks_bitwise_equal_single_gpu(dim, cells, steps, world):
+    """(2, 1024, 19, 3): the c3 grid, whose receivers run the level-group kernel
+    (k_dst_lvl4) on their level slabs (3 ranks: 8 + 8 + 4 levels)."""
     import paper_2107_06381_b200 as B
 
-    w = workloads.make_small(dim, cells, steps, seed=3) if cells < 512 else workloads.make("c2")
+    w = workloads.make_small(dim, cells, steps, seed=3) if cells != 512 else workloads.make("c2")
     grid = B.build_grid(dim, w.length, cells)
     tg = B.TimeGrid(w.horizon, steps)
     system = B.assemble(B.MethodKind.PINT_MQBVM, 1e-2, grid, tg, w.g_delta)
