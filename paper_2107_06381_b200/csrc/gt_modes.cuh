@@ -140,6 +140,12 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
   extern __shared__ double2 smem[];
   __shared__ double red[2 * S];
   __shared__ int s_ck1[41], s_csl[41], s_gpw[40];
+  // generic (multi-slab / block-table) W stores: level tile -> slab, and per warp
+  // the mode's (and its mirror's) base pointer in every slab, biased so that
+  // level t lands at base[slab(t)] + (t >> 3) * P1 * 8 + (t & 7) (slabs start at
+  // multiples of 8 levels)
+  __shared__ unsigned char s_slab[FAST ? 1 : 136];
+  __shared__ double* s_sb[FAST ? 1 : S][2][8];
   double2* s_sg = smem;                       // [8][128] + y0 [32]
   double2* s_tw = smem + kGt2Tw;              // [25][41]
   double2* s_gi = smem + kGt2Gi;              // [25][41]
@@ -149,6 +155,13 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
     s_ck1[i] = __ldg(a.itab + i);
     s_csl[i] = __ldg(a.itab + 41 + i);
     if (i < 40) s_gpw[i] = __ldg(a.itab + 82 + i);
+  }
+  if (!FAST && a.wl.mode_major) {
+    for (int i = threadIdx.x; i < 136; i += T) {
+      int sl = 0;
+      while (sl + 1 < a.wl.nsl && 8 * i >= a.wl.sl_c[sl + 1]) ++sl;
+      s_slab[i] = (unsigned char)sl;
+    }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -283,6 +296,14 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
     }
     __syncwarp();
     // ---- C: column k1 per lane: twiddle, DFT25 over j2, Gamma^-1, Re, norms, stores
+    if (!FAST && wl.mode_major) {
+      if (lane < wl.nsl) {
+        const long long bias = (long long)(wl.sl_c[lane] >> 3) * wl.P1 * kTBL;
+        s_sb[FAST ? 0 : warp][0][lane] = wl.sl_base[lane] + (wl.row_off(lane, it.k1d) + it.rd * kTBL - bias);
+        if (it.hm) s_sb[FAST ? 0 : warp][1][lane] = wl.sl_base[lane] + (wl.row_off(lane, it.k1m) + it.rm * kTBL - bias);
+      }
+      __syncwarp();
+    }
     double zr2 = 0.0, zi2 = 0.0;
     const int dstride = FAST ? (int)(wl.P1 * kTBL) : 0;
     double* const based = FAST ? wl.sl_base[0] + wl.row_off(0, it.k1d) + it.rd * kTBL : nullptr;
@@ -324,6 +345,11 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
             const int off = (t >> 3) * dstride + (t & 7);
             based[off] = c * zr;
             if (it.hm) basem[off] = c2 * zr;
+          } else if (wl.mode_major) {
+            const int sl = s_slab[t >> 3];
+            const long long off = (long long)(t >> 3) * wl.P1 * kTBL + (t & 7);
+            s_sb[FAST ? 0 : warp][0][sl][off] = c * zr;
+            if (it.hm) s_sb[FAST ? 0 : warp][1][sl][off] = c2 * zr;
           } else {
             *w_level_ptr(wl, it.k1d, it.rd, t) = c * zr;
             if (it.hm) *w_level_ptr(wl, it.k1m, it.rm, t) = c2 * zr;
@@ -334,7 +360,7 @@ __global__ void __launch_bounds__(GtPlan::T, 1) k_modes_gt(GtModesArgs a) {
     const double cc = c * c + c2 * c2;
     sre = fma(cc, zr2, sre);
     sim = fma(cc, zi2, sim);
-    __syncwarp();   // Y is rewritten by the next mode
+    __syncwarp();   // Y (and the warp's slab base pointers) are rewritten by the next mode
     cur = nxt; nxt = nxt2; tb_cur = tb_nxt;
   }
   block_sum2(sre, sim, red);
