@@ -1821,8 +1821,21 @@ int lvl4_launch(const bhcp_space_plan* sp, const double* W, double* y, long long
   const int kfirst = g_lvl4_kfirst >= 0 ? g_lvl4_kfirst : (int)grid;
   lvl::ArgsLV a{sp->twN, sp->snN, sqrt(2.0 / 1024), y, z, gsync, gsync + (NT + 1), (int)m, (int)NT, (int)nlev,
                 (int)nct, (int)ntasks, kfirst};
-  lvl::k_dst_lvl4<<<(unsigned)grid, lvl::kThreads, sm, s>>>(tm, tz, ty256, ty255, a);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k_dst_lvl4 launch");
+  // cooperative launch: the driver schedules the whole grid at once or refuses,
+  // so a concurrent kernel can never leave part of it waiting on CTAs that
+  // cannot become resident
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(lvl::kThreads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, lvl::k_dst_lvl4, tm, tz, ty256, ty255, a) != cudaSuccess)
+    return cuda_fail("k_dst_lvl4 launch");
   return BHCP_OK;
 }
 
