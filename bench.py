@@ -362,6 +362,10 @@ def main():
         roof_hbm = {"bound": "hbm", "kernel": names[mdom], "achieved": kernels[mdom]["achieved_GBps"], "peak": hbm,
                     "unit": "GB/s", "frac": kernels[mdom]["hbm_frac"], "traffic": kernels[mdom]["traffic"],
                     "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes[mdom]}
+        if lvl_sync and w.num_cells == 1024:
+            roof_hbm["note"] = ("k_dst_lvl4 moves its 16 B/DOF of compulsory traffic (read W, write y) at well under "
+                                "the HBM peak: it is bound by the DST work of its consumer warps (FP64 pipe ~37%, "
+                                "issue ~42% in ncu, profiles/r02_c3_summary.md), not by HBM")
         # pass A against the measured FP64 peak (reported whichever kernel dominates)
         fpk, fpk_kind = fp64_peak()
         flops = modes_alg_flops(w.dim, w.num_cells - 1, n)
