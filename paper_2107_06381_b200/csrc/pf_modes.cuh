@@ -86,8 +86,23 @@ __device__ __forceinline__ void pf_warp_stage(const double2* rowp, int lane, con
     const int b = lane + 32 * i;
     if (b < NB) {
       const int k = b % Ns, base = (b - k) * R + k;
+      if constexpr (R == 4 && (Ns == 1 || Ns == 4)) {
+        // radix-4 stores land at base + Ns r: with base = 4b (Ns = 1) or
+        // 16 (b / 4) + b % 4 (Ns = 4) the 8 lanes of a 16-byte wavefront share 2
+        // (resp. 4) bank groups for a common r. Lane b issues its r in the rotated
+        // order r = (rr + f) & 3, f = b / 2 (resp. b / 4): 8 distinct bank groups.
+        const int f = (Ns == 1 ? (b >> 1) : (b >> 2)) & 3;
+        double2 w0 = v[i][0], w1 = v[i][1], w2 = v[i][2], w3 = v[i][3];
+        if (f & 1) { const double2 t0 = w0; w0 = w1; w1 = w2; w2 = w3; w3 = t0; }
+        if (f & 2) { double2 t0 = w0; w0 = w2; w2 = t0; t0 = w1; w1 = w3; w3 = t0; }
+        store(base + Ns * (f & 3), w0);
+        store(base + Ns * ((f + 1) & 3), w1);
+        store(base + Ns * ((f + 2) & 3), w2);
+        store(base + Ns * ((f + 3) & 3), w3);
+      } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) store(base + Ns * r, v[i][r]);
+        for (int r = 0; r < R; ++r) store(base + Ns * r, v[i][r]);
+      }
     }
   }
   __syncwarp();
