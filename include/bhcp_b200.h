@@ -146,7 +146,11 @@ int bhcp_read_status(const void* status_dev, double tol, bhcp_status* st, void* 
 /* Fused solve: y (n_levels, n_space) float64 from the
  * final data g (n_space float64) and the condition divisor (methods.py:85-96).
  * ws must hold bhcp_pint_workspace_bytes() bytes of device memory; the status
- * block is inside ws (bhcp_pint_status_ptr). */
+ * block is inside ws (bhcp_pint_status_ptr). Kernels: status reset, the DST of
+ * g, pass A, and the level passes -- for 2D m + 1 = 1024 one level-group kernel
+ * (bhcp_pint_levels_fused), whose scratch (counters + two level tiles of Z,
+ * 134 MB) is part of ws. Capturable in a CUDA graph; the level-group kernel is
+ * a cooperative launch. */
 size_t bhcp_pint_workspace_bytes(const bhcp_space_plan* sp, const bhcp_time_plan* tp);
 void* bhcp_pint_status_ptr(const bhcp_space_plan* sp, const bhcp_time_plan* tp, void* ws);
 int bhcp_pint_solve(const bhcp_space_plan* sp, const bhcp_time_plan* tp,
