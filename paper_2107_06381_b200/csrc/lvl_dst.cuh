@@ -47,11 +47,15 @@
 // lines survive in L2 for the next reader up to about 64 MB
 // (tools/probe_l2.cu), which is what one 67 MB level tile leans on.
 //
-// Warps: 8 consumers (4 line pairs x 2 halves: warp_dst1024), 1 producer (TMA
-// loads of both task kinds, after the counters), 3 storers (column tiles to
-// y, Z discards, the release increments of the counters). Three 64 KB
-// buffers, per buffer the mbarriers full (producer -> consumers), done
-// (consumers -> storers) and free (storers -> producer).
+// Warps: 8 consumers (4 line pairs x 2 halves: warp_dst1024; two warpgroups at
+// 232 registers after setmaxnreg), 1 producer (TMA loads of both task kinds,
+// after the counters), 1 storer (the TMA half of a column tile to y, Z
+// discards, the release increments of the counters) and two idle warps that
+// only donate their registers. Three 64 KB buffers, per buffer the mbarriers
+// full (producer -> consumers), done (consumers -> storer) and free (storer ->
+// producer). Variants that lost (round 2): an FP64 ping-pong between line
+// pairs through named barriers (no change); two consumer teams of 8 warps at
+// 112 registers on alternate tiles (each team twice as slow: 9.4 ms).
 #pragma once
 #include "wax2_dst.cuh"
 
@@ -80,7 +84,14 @@ constexpr int kN = 1024;
 constexpr int kNB = 3;        // tile buffers
 constexpr int kCW = 8;        // consumer warps
 constexpr int kSW = 1;        // storer warps
-constexpr int kThreads = (kCW + 1 + kSW) * 32;
+// Warpgroups 0, 1 = the consumers; warpgroup 2 = producer, storer, two idle warps.
+// The kernel launches at 168 registers per thread (384 threads); the auxiliary
+// warpgroup then drops to kRegsAux and the consumers rise to kRegsCons
+// (setmaxnreg moves registers inside the CTA's allocation: 256 x 232 + 128 x 40
+// = 384 x 168), so the consumers' 16 complex values, twiddles and addresses stay
+// in registers with room for the scheduler to hoist loads.
+constexpr int kThreads = 384;
+constexpr int kRegsCons = 232, kRegsAux = 40;
 constexpr int kTD2 = kN * 4;  // double2 per tile (8 lines x 1024 rows)
 
 constexpr size_t smem_bytes() {
@@ -234,6 +245,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
     }
   }
   const long long m = a.m, lvl = m * m;
+  if (warp >= kCW) {
+  // the auxiliary warpgroup hands its registers to the two consumer warpgroups
+  // (no path from here joins the consumers' code again: ptxas allocates each
+  // region for the register count set on every path into it)
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsAux));
+  if (warp > kCW + kSW) return;
   if (warp == kCW) {
     // ---------------------------------------------------------------- producer
     if (lane != 0) return;
@@ -337,9 +354,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
     if (sw == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     return;
   }
+  return;
+  }
   // ------------------------------------------------------------------ consumers
-  const int q = warp & 3, h = warp >> 2, bar = 1 + q;
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsCons));
+  // warp w: half w >> 2 of line pair w (w < 4) or (w + 2) & 3: each scheduler
+  // hosts halves of two different line pairs (warps w and w + 4), which are not
+  // in lockstep at the pair barriers
+  const int q = warp >= 4 ? ((warp + 2) & 3) : warp, h = warp >> 2, bar = 1 + q;
   const wax2::LaneK1024 K(lane, h, a.tw, a.scale);
+  const wax2::SnRegs snr(sn, K.j1, K.j2);
   for (int it = 0; it < ntiles_cta; ++it) {
     const int b = it % kNB;
     double2* T = tiles + b * kTD2;
@@ -373,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
       double* za_row = a.z + rowa;
       double* zb_row = za_row + m * kZPitch;
       wax2::RowSink<128> sink{za_row, zb_row, kv && !za, kv && !zb, K.j1, K.j2};
-      wax2::warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+      wax2::warp_dst1024<Sw64>(T, q, h, K, snr, xch + q * 42, bar, sink);
       // Z column 1023 (line 7 of the last column tile) must be finite: zero it
       if (kv && h == 0 && lane == 0) {
         if (!za) za_row[1023] = 0.0;
@@ -381,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
       }
     } else {
       ParitySink sink{T, q, K.j1, K.j2};
-      wax2::warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+      wax2::warp_dst1024<Sw64>(T, q, h, K, snr, xch + q * 42, bar, sink);
       // all four line pairs are in the tile: the consumers store the rows TMA cannot
       // (chunks 8 bytes off 16-byte alignment; every row for the last column tile
       // and the last level) with 8-byte stores, 8 lanes per row

@@ -458,9 +458,28 @@ struct LaneK1024 {
 
 __device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
 
+// The pre-step's sin(pi j / N) factors of a unit's 16 rows: read from the
+// shared-memory table per tile (SnTable), or held in registers for the whole
+// kernel (SnRegs: k_dst_lvl4, whose consumers have the registers after setmaxnreg).
+struct SnTable {
+  const double* sn;
+  int j1, j2;
+  __device__ __forceinline__ double a(int r) const { return sn[j1 + 128 * r]; }
+  __device__ __forceinline__ double b(int r) const { return sn[j2 + 128 * r]; }
+};
+struct SnRegs {
+  double va[8], vb[8];
+  __device__ __forceinline__ SnRegs(const double* sn, int j1, int j2) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) { va[r] = sn[j1 + 128 * r]; vb[r] = sn[j2 + 128 * r]; }
+  }
+  __device__ __forceinline__ double a(int r) const { return va[r]; }
+  __device__ __forceinline__ double b(int r) const { return vb[r]; }
+};
+
 // xch: 42 doubles per line pair (block totals and U_0 exchanged between the two warps)
-template <class L, class Sink>
-__device__ __forceinline__ void warp_dst1024(double2* T, int q, int h, const LaneK1024& K, const double* sn,
+template <class L, class Sink, class Sn>
+__device__ __forceinline__ void warp_dst1024(double2* T, int q, int h, const LaneK1024& K, const Sn& sn,
                                              double* xch, int bar, Sink& sink) {
   constexpr int N = 1024;
   constexpr int R128 = 128 * L::RS, R64 = 64 * L::RS;
@@ -481,7 +500,7 @@ __device__ __forceinline__ void warp_dst1024(double2* T, int q, int h, const Lan
     for (int r = 0; r < 8; ++r) {
       const double2 pa = v == 0 ? xa[(8 - r) & 7] : xb[7 - r];
       const double2 pb2 = v == 0 ? xb[7 - r] : xa[7 - r];
-      const double sa = sn[j1 + 128 * r], sb = sn[j2 + 128 * r];
+      const double sa = sn.a(r), sb = sn.b(r);
       A[r] = make_double2(fma(sa, xa[r].x + pa.x, 0.5 * (xa[r].x - pa.x)), fma(sa, xa[r].y + pa.y, 0.5 * (xa[r].y - pa.y)));
       B[r] = make_double2(fma(sb, xb[r].x + pb2.x, 0.5 * (xb[r].x - pb2.x)), fma(sb, xb[r].y + pb2.y, 0.5 * (xb[r].y - pb2.y)));
     }
@@ -893,7 +912,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, 1) k_dst_blk4(const __grid_con
     const long long rowa = ((long long)((long long)t0 * m + k1) * b3.idiv + r2) * m;
     const long long rowb = rowa + m * m * b3.idiv;
     RowSink<128> sink{b3.y + rowa, b3.y + rowb, !za, !zb, K.j1, K.j2};
-    warp_dst1024<Sw64>(T, q, h, K, sn, xch + q * 42, bar, sink);
+    warp_dst1024<Sw64>(T, q, h, K, SnTable{sn, K.j1, K.j2}, xch + q * 42, bar, sink);
     release_buffer(done + b, lane);
   }
 }
