@@ -190,6 +190,23 @@ __device__ __forceinline__ double2* at_par(double2* T, int e, int q) {
   const int j = e >> 1;
   return T + ((e & 1) * 512 + j) * 4 + (q ^ ((j >> 1) & 3));
 }
+// Row-task output sink: the two Z rows of the line pair, straight from
+// registers. Z stores element e of a row at column e + 1, so a unit's outputs
+// S_{2k} (element 2k - 1) and S_{2k+1} (element 2k) are ONE aligned 16-byte
+// store at column 2k, consecutive lanes writing consecutive chunks (k = 0:
+// the pad column 0 gets the zero the column tasks read as element -1).
+struct ZRowSink {
+  double* za;
+  double* zb;
+  bool va, vb;
+  int j1, j2;
+  __device__ __forceinline__ void put(int r, bool hi, int v, double2 ev, double2 od) {
+    const int k = (hi ? j2 : j1) + 128 * r;
+    const bool he = k > 0;
+    if (va) *reinterpret_cast<double2*>(za + 2 * k) = make_double2(he ? ev.x : 0.0, od.x);
+    if (vb) *reinterpret_cast<double2*>(zb + 2 * k) = make_double2(he ? ev.y : 0.0, od.y);
+  }
+};
 struct ParitySink {
   double2* T;
   int q;
@@ -319,15 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
         const int lev = tk.idx / a.nct, ct = tk.idx % a.nct, c0 = ct * 8;
         const int t = tk.g * 8 + lev;
         const long long R0 = (long long)t * m;
-        if (t < a.nlev - 1 && ct < a.nct - 1 && sw == 0 && lane == 0) {
-          // the plane whose rows are even in y (a 16-byte aligned 64 B chunk) leaves
-          // by two TMA boxes of the row-pair view (the second one 255 rows if it is
-          // plane 1: row e = 1023 is the DST's zero row); the consumers stored the
-          // other plane
-          const int pe = (int)(R0 & 1);   // plane with (R0 + pe) even
-          const int P0 = (int)((R0 + pe) >> 1);
-          tma_store2_hint(&ty256, c0, P0, T + (pe * 512) * 4, pol);
-          tma_store2_hint(pe ? &ty255 : &ty256, c0, P0 + 256, T + (pe * 512 + 256) * 4, pol);
+        if (t < a.nlev - 1 && ct > 0 && sw == 0 && lane == 0) {
+          // the tile's 8 lines are elements c0 - 1 .. c0 + 6 (Z column = element + 1).
+          // The plane whose rows are ODD in y (their 64 B chunk at column c0 - 1 is
+          // 16-byte aligned) leaves by two TMA boxes of the row-pair view, second row
+          // of each pair: inner coordinate 1023 + c0 - 1 (the second box 255 rows if
+          // it is plane 1: row e = 1023 is the DST's zero row); the consumers stored
+          // the other plane, and every row of the first column tile (its line 0 is
+          // the pad column)
+          const int pe = (int)(R0 & 1) ^ 1;   // plane with (R0 + pe) odd
+          const int P0 = (int)((R0 + pe - 1) >> 1);
+          tma_store2_hint(&ty256, 1022 + c0, P0, T + (pe * 512) * 4, pol);
+          tma_store2_hint(pe ? &ty255 : &ty256, 1022 + c0, P0 + 256, T + (pe * 512 + 256) * 4, pol);
           asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
           asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         }
@@ -396,13 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
       const long long rowa = ((long long)((tk.g & 1) * 8 + 2 * q) * m + k1) * kZPitch;
       double* za_row = a.z + rowa;
       double* zb_row = za_row + m * kZPitch;
-      wax2::RowSink<128> sink{za_row, zb_row, kv && !za, kv && !zb, K.j1, K.j2};
+      ZRowSink sink{za_row, zb_row, kv && !za, kv && !zb, K.j1, K.j2};
       wax2::warp_dst1024<Sw64>(T, q, h, K, snr, xch + q * 42, bar, sink);
-      // Z column 1023 (line 7 of the last column tile) must be finite: zero it
-      if (kv && h == 0 && lane == 0) {
-        if (!za) za_row[1023] = 0.0;
-        if (!zb) zb_row[1023] = 0.0;
-      }
     } else {
       ParitySink sink{T, q, K.j1, K.j2};
       wax2::warp_dst1024<Sw64>(T, q, h, K, snr, xch + q * 42, bar, sink);
@@ -414,10 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_dst_lvl4(const __grid_constant_
       const int t = tk.g * 8 + lev;
       const long long R0 = (long long)t * m;
       const int l = lane & 7, rr = 4 * warp + (lane >> 3);   // 32 rows per round over the 8 warps
-      const bool lv = c0 + l < a.m;
-      double* dst = a.y + R0 * m + (lv ? c0 + l : 0);
-      if (t < a.nlev - 1 && tk.idx % a.nct < a.nct - 1) {
-        const int po = (int)(R0 & 1) ^ 1;   // the plane whose y rows start 8 bytes off
+      const bool lv = c0 + l >= 1;   // tile line l = Z column c0 + l = element c0 + l - 1 (Z column 0: pad)
+      double* dst = a.y + R0 * m + (lv ? c0 + l - 1 : 0);
+      if (t < a.nlev - 1 && c0 > 0) {
+        const int po = (int)(R0 & 1);   // the plane whose y rows (even global row, column c0 - 1) start 8 bytes off
 #pragma unroll 4
         for (int j = rr; j < 512; j += 32) {
           const int e = 2 * j + po;
