@@ -11,13 +11,17 @@
 //               the scratch Z (the k_dst_blk4 work; W read from HBM by TMA
 //               with an evict-first hint). Z holds one level tile per slot
 //               (two slots) with a 1024-double row pitch, so unlike y
-//               (1023-double rows) it is a TMA tensor.
-//   column task C(g, t, c): 8 adjacent columns of level t, all 1023 rows,
-//               loaded from Z by TMA (still in L2), transformed into a
-//               row-parity-split tile (at_par) and stored to y: the rows
-//               whose 64 B chunk is 16-byte aligned by two TMA boxes of the
-//               row-pair view of y, the others by 8-byte stores (a TMA box
-//               must start 16-byte aligned); after the odd column tile of a
+//               (1023-double rows) it is a TMA tensor. Element e of a row
+//               sits at Z column e + 1 (column 0 is a zero pad), so a lane's
+//               outputs S_2k, S_2k+1 are one aligned 16-byte store.
+//   column task C(g, t, c): 8 adjacent Z columns of level t (elements
+//               8c - 1 .. 8c + 6), all 1023 rows, loaded from Z by TMA (still
+//               in L2), transformed into a row-parity-split tile (at_par) and
+//               stored to y: the rows whose 64 B chunk is 16-byte aligned (odd
+//               global rows) by two TMA boxes of the row-pair view of y, the
+//               others by 8-byte stores (a TMA box must start 16-byte
+//               aligned; the first column tile and the last level entirely
+//               by 8-byte stores); after the odd column tile of a
 //               pair (both on one CTA) the Z lines are discarded from L2
 //               (discard.global.L2) instead of being written back.
 // W is read and y written once; Z lines that L2 evicts before their discard
@@ -55,7 +59,13 @@
 // full (producer -> consumers), done (consumers -> storer) and free (storer ->
 // producer). Variants that lost (round 2): an FP64 ping-pong between line
 // pairs through named barriers (no change); two consumer teams of 8 warps at
-// 112 registers on alternate tiles (each team twice as slow: 9.4 ms).
+// 112 registers on alternate tiles (each team twice as slow: 9.4 ms); the
+// misaligned y rows stored by three / two storer warps instead of the consumers
+// (storers become the bottleneck: 9.9 / 10.2 ms); a product tree for the
+// twiddle powers (no change). What bounds the consumers (round-2 ablations,
+// DESIGN.md section 7): not the butterflies (removing them: -0.4 ms) but the
+// LSU / shared-memory pipe -- 3.6 K LDS/STS wavefronts, 1.4 K shuffles of the
+// odd-output prefix sums and the global stores per 7.7 K-cycle tile.
 #pragma once
 #include "wax2_dst.cuh"
 
