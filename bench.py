@@ -364,8 +364,10 @@ def main():
                     "peak_source": peak_kind, "alg_bytes_per_launch": alg_bytes[mdom]}
         if lvl_sync and w.num_cells == 1024:
             roof_hbm["note"] = ("k_dst_lvl4 moves its 16 B/DOF of compulsory traffic (read W, write y) at well under "
-                                "the HBM peak: it is bound by the DST work of its consumer warps (FP64 pipe ~37%, "
-                                "issue ~42% in ncu, profiles/r02_c3_summary.md), not by HBM")
+                                "the HBM peak: it is bound by the LSU / shared-memory pipe of its consumer warps (six "
+                                "conflict-free 16 KB passes per 1024-point line pair, the prefix-sum shuffles and the "
+                                "global stores: ~75% busy; FP64 pipe 38%; removing every butterfly saves 0.4 of 8.8 ms "
+                                "-- DESIGN.md 3.3, profiles/r02_c3_summary.md), not by HBM or FP64")
         # pass A against the measured FP64 peak (reported whichever kernel dominates)
         fpk, fpk_kind = fp64_peak()
         flops = modes_alg_flops(w.dim, w.num_cells - 1, n)
