@@ -173,6 +173,61 @@ def cpu_sample(w, kind, alpha, fraction, workers):
     return dof, secs
 
 
+def reference_package_check(w, kind, alpha, cores, levels=33):
+    """The UNMODIFIED reference package (pip-installed into baseline/_ref, test data
+    only) on this config's spatial grid with a reduced number of time levels, next
+    to the oracle port on exactly the same reduced problem: pins the port's timing
+    (and its trajectory) to the reference's own solve_pint (pint.py:69-110) on the
+    box the bench runs on. None when the package is not there."""
+    ref_root = ROOT / "baseline" / "_ref"
+    if not (ref_root / "bhcp").is_dir():
+        return None
+    import time
+
+    import numpy as np
+
+    sys.path.insert(0, str(ref_root))
+    try:
+        from bhcp.circulant import TimeGrid
+        from bhcp.methods import MethodKind, assemble
+        from bhcp.pint import solve_pint
+        from bhcp.space import build_grid
+    except Exception as e:  # noqa: BLE001 -- reported, not fatal
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    finally:
+        sys.path.pop(0)
+    from oracle import bhcp_oracle as O
+
+    if w.dim > 2:
+        return {"unavailable": "the reference rejects dim 3 (space.py:42-43)"}
+    steps = min(levels - 1, w.num_steps)
+    horizon = w.horizon * steps / w.num_steps   # the same tau as the full config
+    grid = build_grid(w.dim, w.length, w.num_cells)
+    tg = TimeGrid(horizon, steps)
+    system = assemble(MethodKind(kind), alpha, grid, tg, w.g_delta)
+    dof = (steps + 1) * w.g_delta.shape[0]
+    out = {"levels": steps + 1, "dof": dof, "note": "same spatial grid and tau, reduced time levels"}
+    try:
+        for label, workers in (("workers_none", None), ("workers_all", cores)):
+            t0 = time.perf_counter()
+            res = solve_pint(system, workers=workers)
+            out[label] = {"seconds": time.perf_counter() - t0, "DOF_s": dof / (time.perf_counter() - t0),
+                          "workers": workers}
+        traj = np.asarray(res.trajectory)
+    except Exception as e:  # noqa: BLE001 -- e.g. ImaginaryResidueError at this size
+        out["unavailable"] = f"{type(e).__name__}: {e}"
+        return out
+    d1, s1 = O.solve_pint_sample(kind, alpha, w.dim, w.length, w.num_cells, horizon, steps, w.g_delta, 1.0,
+                                 workers=None)
+    dn, sn = O.solve_pint_sample(kind, alpha, w.dim, w.length, w.num_cells, horizon, steps, w.g_delta, 1.0,
+                                 workers=cores)
+    out["port_workers_none"] = {"seconds": s1, "DOF_s": d1 / s1}
+    out["port_workers_all"] = {"seconds": sn, "DOF_s": dn / sn, "workers": cores}
+    orc, _ = O.solve_pint(kind, alpha, w.dim, w.length, w.num_cells, horizon, steps, w.g_delta)
+    out["port_vs_reference_rel_l2"] = float(np.linalg.norm(orc - traj) / np.linalg.norm(traj))
+    return out
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU algorithm (oracle port) on host cores."""
     if rank != 0:
@@ -191,6 +246,7 @@ def run_reference(args, rank, world):
         total_dof += dof
         total_s += s
     value = total_dof / total_s
+    pkg = reference_package_check(w, kind, alpha, cores)
     sample = (f"{args.config}: per step, fraction {frac} of every per-unit op of the reference 3-step solve "
               f"(time FFTs of {frac:.1%} of the spatial rows, shifted solves incl. the singular-shift scan of "
               f"{frac:.1%} of the levels on a {cores}-thread pool, back transform + residue + transposed copy of "
@@ -204,6 +260,8 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if pkg is not None:
+        line["reference_package"] = pkg
     print(json.dumps(line), flush=True)
 
 

@@ -166,3 +166,26 @@ def test_residue_no_raise_cases(golden):
     traj, ratio = O.solve_pint(O.PINT_QBVM, 1e-3, 1, np.pi, 256, 1.0, 256, golden["c1_gdelta"])
     raised_ref, ratio_ref, _ = golden["trip_c1_pint-qbvm"]
     assert not raised_ref and ratio == ratio_ref
+
+
+def test_reference_package_check_pins_port_timing_leg():
+    """bench.py --impl reference runs the unmodified reference package (when it is
+    installed under baseline/_ref) next to the oracle port on the same reduced
+    problem: the trajectories must be bit-identical (pint.py:69-110)."""
+    import importlib.util
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    if not (root / "baseline" / "_ref" / "bhcp").is_dir():
+        pytest.skip("reference package not installed under baseline/_ref")
+    spec = importlib.util.spec_from_file_location("bench_mod", root / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_2107_06381_b200 import workloads
+
+    w = workloads.make_small(2, 16, 40, kmax=4)
+    out = bench.reference_package_check(w, "pint-mqbvm", 1e-2, 2, levels=9)
+    assert out is not None and "unavailable" not in out, out
+    assert out["levels"] == 9 and out["dof"] == 9 * 15 * 15
+    assert out["port_vs_reference_rel_l2"] == 0.0
+    assert out["workers_none"]["DOF_s"] > 0 and out["port_workers_all"]["DOF_s"] > 0
