@@ -254,10 +254,11 @@ int bhcp_pint_levels_blocked(const bhcp_space_plan* sp, double* in_dev,
 /* bhcp_pint_levels_fused: all spatial passes, blocked W (uniform k1 stride, as
  * bhcp_pint_levels) -> y, as ONE persistent kernel over level groups that stay
  * in L2 where bhcp_pint_levels_sync_bytes(sp, nlev) > 0 (dim 2, m + 1 = 1024:
- * k_dst_lvl4 -- row tasks W -> y, then the strided axis on y while the level
- * tile is still L2-resident; 16 instead of 32 B/DOF of HBM traffic). sync_dev:
- * a device buffer of at least that many bytes, used as per-level-tile
- * counters (the call zeroes it on the stream); it must not be shared by
+ * k_dst_lvl4 -- row tasks W -> a scratch Z inside sync_dev, column tasks Z -> y
+ * while the level tile is still L2-resident; 16 instead of 32 B/DOF of
+ * compulsory HBM traffic). sync_dev: a device buffer of at least that many
+ * bytes, used as per-level-tile counters and the two Z level-tile slots (the
+ * call zeroes the counters on the stream); it must not be shared by
  * concurrent calls. Where the sync size is 0 this is bhcp_pint_levels (any
  * dim; the input may be overwritten) and sync_dev is ignored. Reference: the per-level
  * DSTs of pint.py:94-96 / space.py:163-177. */
