@@ -443,6 +443,27 @@ def main():
             roofline = roof_hbm
         ms_per_step = total_ms / args.steps
         value = dof / (ms_per_step * 1e-3)
+        # the pipe that actually bounds both c3 kernels: L1 data-pipe (LSU) wavefronts
+        # -- shared-memory loads/stores, shuffles, global stores -- counted per launch
+        # by ncu (profiles/ncu_lsu_c3.json; fixed for a workload) over the live kernel
+        # time, against one wavefront per clock per SM at the sampled SM clock
+        roof_lsu = None
+        lsu_file = ROOT / "profiles" / "ncu_lsu_c3.json"
+        if args.config == "c3" and lsu_file.exists() and clocks.get("sm_mhz"):
+            cnt = json.loads(lsu_file.read_text())
+            peak_wf = 148 * clocks["sm_mhz"] * 1e6
+            roof_lsu = {"bound": "lsu", "unit": "G wavefronts/s", "peak": peak_wf / 1e9,
+                        "peak_source": "1 wavefront / clk / SM x 148 SMs x the SM clock sampled under load",
+                        "kernels": []}
+            for key, idx in (("fastk::k_modes_gt", 1), ("lvl::k_dst_lvl4", 2)):
+                if key in cnt and idx < len(names):
+                    wf = cnt[key]["lsu_data_wavefronts"]
+                    ach = wf / (phase_ms[idx] * 1e-3)
+                    roof_lsu["kernels"].append({"kernel": names[idx], "wavefronts_per_launch": wf,
+                                                "achieved": ach / 1e9, "frac": ach / peak_wf})
+            roof_lsu["note"] = ("both kernels issue their shared-memory passes in bursts (every warp reaches the same "
+                                "FFT stage together), so the average sits below 1 while the bursts saturate the pipe; "
+                                "see DESIGN.md 3.3 for the ablation runs")
 
         if args.quick:
             print(json.dumps({"config": args.config, "ms_per_step": ms_per_step, "value": value,
@@ -533,6 +554,7 @@ def main():
             "roofline": roofline,
             "roofline_hbm": roof_hbm,
             "roofline_fp64": roof_fp64,
+            "roofline_lsu": roof_lsu,
             "kernels": kernels,
             "phases_ms": {nm: float(t) for nm, t in zip(names, phase_ms)},
             "pipeline_72B_per_dof": {"achieved_GBps": 72.0 * dof / (ms_per_step * 1e-3) / 1e9,
